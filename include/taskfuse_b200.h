@@ -1,0 +1,198 @@
+/*
+ * taskfuse_b200.h — C ABI of the B200-native strategy-3 hydro hot path.
+ *
+ * Drop-in boundary for the per-sub-grid numerics and the aggregation
+ * executor of the reference `taskfuse` package (arXiv 2210.06438 artifact,
+ * /root/reference/pkg/src/taskfuse).  Every entry point is `extern "C"`,
+ * takes plain pointers and sizes (no torch types), is stream-ordered and
+ * returns an int: 0 on success, otherwise a cudaError_t value or one of the
+ * TF_E* codes below.  Nothing throws across this boundary.
+ *
+ * Memory layout (all FP64, C order, z fastest — the reference layout):
+ *   pool_ext : (pool_slices, E, E, E)      E = n + 6, ghost width 3
+ *              == HydroState.u[block] stacked in lexicographic block order
+ *              (reference scenario.py:52-96).
+ *   um/up/F  : (slots, 3, C, C, C)         C = n + 2
+ *              == make_scratch(n)["um"/"up"/"F"] stacked per slot
+ *              (reference kernels.py:27-36).
+ *   A "slot" is either the slice index inside the team (out_mode 0, the
+ *   team-buffer layout of aggregator.py:121-128: slice s owns
+ *   [s*len, (s+1)*len)) or the sub-grid id itself (out_mode 1: per-sub-grid
+ *   scratch, HydroSim.scratch[block], step.py:53).
+ *
+ * Supported sub-grid edges: n = 8 and n = 16 (strategy 1).
+ */
+#ifndef TASKFUSE_B200_H
+#define TASKFUSE_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* tf_stream_t; /* == cudaStream_t */
+
+enum {
+  TF_OK = 0,
+  TF_E_INVALID = 1001,     /* bad argument (n, T, pointer, id range) */
+  TF_E_NO_TMA = 1002,      /* cuTensorMapEncodeTiled unavailable */
+  TF_E_ORDERING = 1003,    /* aggregation: replay diverged / misuse */
+  TF_E_CAPACITY = 1004     /* aggregation: out of slots */
+};
+
+#define TF_MAX_TEAM 128 /* aggregator.py:42 MAX_TEAM */
+
+/* ---- numerics (reference hydro/kernels.py) ------------------------------ */
+
+/* Fused reconstruct + flux over T aggregated slices.
+ * Replaces reconstruct_body (kernels.py:73-81) followed by flux_body
+ * (kernels.py:84-93), batched over a team as slice_launch would
+ * (aggregator.py:143-166).  Slice s reads pool_ext[ids[s]] (ids == NULL:
+ * identity).  ids is a DEVICE pointer.  flux_form 0 = reference upwind
+ * (bit-exact), 1 = Kurganov-Tadmor central-upwind form (equal to upwind in
+ * exact arithmetic for f = a u; checked at 1e-12 relative).
+ * amax (may be NULL): per-slot max signal speed over all faces, the value
+ * reduce_body stores (kernels.py:96-97).                                   */
+int tf_recon_flux_f64(const double* pool_ext, int64_t pool_slices,
+                      const int32_t* ids, int32_t T, int32_t n,
+                      double ax, double ay, double az,
+                      double* um, double* up, double* F, int32_t out_mode,
+                      double* amax, int32_t flux_form, tf_stream_t stream);
+
+/* Same, with the team's sub-grid ids given in HOST memory (T <= 128); they
+ * travel inside the kernel parameters, so a team launch needs no copy.     */
+int tf_recon_flux_team_f64(const double* pool_ext, int64_t pool_slices,
+                           const int32_t* host_ids, int32_t T, int32_t n,
+                           double ax, double ay, double az,
+                           double* um, double* up, double* F,
+                           int32_t out_mode, double* amax, int32_t flux_form,
+                           tf_stream_t stream);
+
+/* reconstruct_body alone (kernels.py:73-81): w = pool_ext[ids[s]].          */
+int tf_reconstruct_f64(const double* pool_ext, int64_t pool_slices,
+                       const int32_t* ids, int32_t T, int32_t n,
+                       double* um, double* up, int32_t out_mode,
+                       tf_stream_t stream);
+
+/* flux_body alone (kernels.py:84-93): reads up (a>=0) / um (a<0) of the
+ * slot, writes F of the slot.                                              */
+int tf_flux_f64(const int32_t* ids, int32_t T, int32_t n,
+                double ax, double ay, double az,
+                const double* um, const double* up, double* F,
+                int32_t out_mode, tf_stream_t stream);
+
+/* update_body (kernels.py:100-111), no FMA contraction: writes the owned
+ * region of next_ext[ids[s]] = u_ext - dt_dx * div(F of the slot).         */
+int tf_update_f64(const double* pool_ext, const int32_t* ids, int32_t T,
+                  int32_t n, const double* F, int32_t out_mode, double dt_dx,
+                  double* next_ext, tf_stream_t stream);
+
+/* exchange_ghosts (scenario.py:124-142) for T sub-grids of a periodic
+ * per_axis^3 lattice (ids NULL: all per_axis^3 sub-grids).                 */
+int tf_ghost_fill_f64(double* pool_ext, const int32_t* ids, int32_t T,
+                      int32_t n, int32_t per_axis, tf_stream_t stream);
+
+/* prep_body (kernels.py:69-70): w[slot] = pool_ext[ids[s]].                */
+int tf_prep_f64(const double* pool_ext, const int32_t* ids, int32_t T,
+                int32_t n, double* w, int32_t out_mode, tf_stream_t stream);
+
+/* reduce_body (kernels.py:96-97): reduce_out[slot] = max(|ax|,|ay|,|az|).  */
+int tf_reduce_f64(const int32_t* ids, int32_t T, double ax, double ay,
+                  double az, double* reduce_out, int32_t out_mode,
+                  tf_stream_t stream);
+
+/* ---- aggregation formation core (reference aggregator.py:247-345) ------- */
+
+typedef struct tf_region tf_region;
+
+typedef struct {
+  int32_t parent;      /* parents[arrivals % P]                  (:298)   */
+  int32_t executor;    /* executor index the parent is pinned to (:273)   */
+  int64_t team;        /* region-local team sequence number              */
+  int32_t slice_id;    /* arrival order inside the team          (:303)   */
+  int32_t closed;      /* 0 forming, 1 cap, 2 solo fast path, 3 drain     */
+  int32_t queried;     /* 1 iff stream_busy was consulted (:316)          */
+} tf_enter_result;
+
+/* stream_busy hook (device.py:187-194): return nonzero iff busy.           */
+typedef int (*tf_busy_fn)(void* ctx, int32_t executor);
+
+/* AggregationRegion.__init__ (aggregator.py:250-282).                      */
+int tf_region_create(const char* name, int32_t max_team,
+                     int32_t parent_count, int32_t executors,
+                     tf_region** out);
+void tf_region_destroy(tf_region* r);
+/* executor index of parent i: (crc32(name) % E + i) % E  (:273-277)        */
+int32_t tf_region_parent_executor(const tf_region* r, int32_t parent);
+/* AggregationRegion.enter (aggregator.py:284-326) minus the task guard.    */
+int tf_region_enter(tf_region* r, int64_t tag, tf_busy_fn busy, void* ctx,
+                    tf_enter_result* out);
+/* Stream drained (device.py:364-370 -> aggregator.py:328-332): closes every
+ * forming team whose parent sits on `executor`, in watch order.  Writes up
+ * to cap closed team ids to out_teams; returns the count (or <0 error).    */
+int tf_region_stream_idle(tf_region* r, int32_t executor, int64_t* out_teams,
+                          int32_t cap);
+/* Team bookkeeping.  release frees a closed team's record. */
+int tf_region_release_team(tf_region* r, int64_t team);
+int tf_region_team_size(const tf_region* r, int64_t team);
+int tf_region_team_members(const tf_region* r, int64_t team, int64_t* tags,
+                           int32_t cap);
+int tf_region_team_parent(const tf_region* r, int64_t team);
+/* RegionStats (aggregator.py:237-244): counters + histogram[1..128].      */
+int tf_region_stats(const tf_region* r, int64_t* teams_formed,
+                    int64_t* solo_fast_path, int64_t* histogram129);
+
+/* ---- real-time bulk executor (strategy 3 on real CUDA streams) ---------- */
+
+typedef struct tf_executor tf_executor;
+
+/* An executor pool of `count` streams (executorpool.py:42-60) bound to one
+ * region; the region's parents round-robin over them.                      */
+int tf_executor_create(tf_region* region, int32_t count, tf_executor** out);
+void tf_executor_destroy(tf_executor* ex);
+tf_stream_t tf_executor_stream(const tf_executor* ex, int32_t executor);
+
+/* Submit `count` recon+flux task arrivals (sub-grid ids, host memory) in
+ * order.  Team formation runs in real time: a parent's stream is busy iff
+ * its last recorded CUDA event has not completed (cudaEventQuery); a
+ * closed team is one tf_recon_flux_team_f64 launch on its parent's stream.
+ * Remaining forming teams are flushed at the end.  Returns launches issued
+ * in *launches.  Completion: tf_executor_sync or events on the streams.    */
+int tf_executor_run_recon_flux(tf_executor* ex, const double* pool_ext,
+                               int64_t pool_slices, const int32_t* ids,
+                               int64_t count, int32_t n, double ax, double ay,
+                               double az, double* um, double* up, double* F,
+                               double* amax, int32_t flux_form,
+                               int64_t* launches);
+/* Make `stream` wait for all work issued so far on every executor stream.  */
+int tf_executor_join(tf_executor* ex, tf_stream_t stream);
+int tf_executor_sync(tf_executor* ex);
+
+/* ---- captured team plans (CUDA graphs) ----------------------------------- */
+
+typedef struct tf_plan tf_plan;
+
+/* Capture one iteration's formed teams (flat ids, team_offsets[nteams+1],
+ * executor per team) as a CUDA graph: one tf_recon_flux_team_f64 node per
+ * team on its executor's branch, outputs per sub-grid (out_mode 1).        */
+int tf_plan_capture_recon_flux(const int32_t* ids, const int64_t* team_offsets,
+                               const int32_t* team_executor, int64_t nteams,
+                               int32_t executors, const double* pool_ext,
+                               int64_t pool_slices, int32_t n, double ax,
+                               double ay, double az, double* um, double* up,
+                               double* F, double* amax, int32_t flux_form,
+                               tf_plan** out);
+int tf_plan_launch(tf_plan* plan, tf_stream_t stream);
+int64_t tf_plan_kernels(const tf_plan* plan);
+void tf_plan_destroy(tf_plan* plan);
+
+/* ---- misc ----------------------------------------------------------------*/
+const char* tf_version(void);
+/* sm_100a device check: 0 iff device `dev` is compute capability 10.0.    */
+int tf_check_device(int32_t dev);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TASKFUSE_B200_H */

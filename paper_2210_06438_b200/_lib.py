@@ -1,0 +1,117 @@
+"""ctypes binding of the C ABI in include/taskfuse_b200.h.
+
+This is the whole Python<->native seam: plain pointers, sizes and a CUDA
+stream handle cross it; every entry point returns an int status that is
+turned into `TaskfuseCudaError` here.  There is no fallback: if the library
+is missing the import of any compute op raises.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+from pathlib import Path
+
+from .errors import TaskfuseCudaError
+
+LIB_PATH = Path(__file__).resolve().parent / "libtaskfuse_b200.so"
+
+_i32, _i64, _f64 = C.c_int32, C.c_int64, C.c_double
+_p = C.c_void_p
+_pi32 = C.POINTER(C.c_int32)
+_pi64 = C.POINTER(C.c_int64)
+
+TF_E_INVALID = 1001
+TF_E_NO_TMA = 1002
+MAX_TEAM = 128
+
+
+class EnterResult(C.Structure):
+    _fields_ = [("parent", _i32), ("executor", _i32), ("team", _i64),
+                ("slice_id", _i32), ("closed", _i32), ("queried", _i32)]
+
+
+BUSY_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int32)
+
+# name -> (restype, argtypes); mirrors include/taskfuse_b200.h
+SIGNATURES = {
+    "tf_recon_flux_f64": (C.c_int, [_p, _i64, _p, _i32, _i32, _f64, _f64, _f64,
+                                    _p, _p, _p, _i32, _p, _i32, _p]),
+    "tf_recon_flux_team_f64": (C.c_int, [_p, _i64, _pi32, _i32, _i32, _f64,
+                                         _f64, _f64, _p, _p, _p, _i32, _p,
+                                         _i32, _p]),
+    "tf_reconstruct_f64": (C.c_int, [_p, _i64, _p, _i32, _i32, _p, _p, _i32,
+                                     _p]),
+    "tf_flux_f64": (C.c_int, [_p, _i32, _i32, _f64, _f64, _f64, _p, _p, _p,
+                              _i32, _p]),
+    "tf_update_f64": (C.c_int, [_p, _p, _i32, _i32, _p, _i32, _f64, _p, _p]),
+    "tf_ghost_fill_f64": (C.c_int, [_p, _p, _i32, _i32, _i32, _p]),
+    "tf_prep_f64": (C.c_int, [_p, _p, _i32, _i32, _p, _i32, _p]),
+    "tf_reduce_f64": (C.c_int, [_p, _i32, _f64, _f64, _f64, _p, _i32, _p]),
+    "tf_region_create": (C.c_int, [C.c_char_p, _i32, _i32, _i32,
+                                   C.POINTER(_p)]),
+    "tf_region_destroy": (None, [_p]),
+    "tf_region_parent_executor": (_i32, [_p, _i32]),
+    "tf_region_enter": (C.c_int, [_p, _i64, BUSY_FN, _p,
+                                  C.POINTER(EnterResult)]),
+    "tf_region_stream_idle": (C.c_int, [_p, _i32, _pi64, _i32]),
+    "tf_region_release_team": (C.c_int, [_p, _i64]),
+    "tf_region_team_size": (C.c_int, [_p, _i64]),
+    "tf_region_team_members": (C.c_int, [_p, _i64, _pi64, _i32]),
+    "tf_region_team_parent": (C.c_int, [_p, _i64]),
+    "tf_region_stats": (C.c_int, [_p, _pi64, _pi64, _pi64]),
+    "tf_executor_create": (C.c_int, [_p, _i32, C.POINTER(_p)]),
+    "tf_executor_destroy": (None, [_p]),
+    "tf_executor_stream": (_p, [_p, _i32]),
+    "tf_executor_run_recon_flux": (C.c_int, [_p, _p, _i64, _pi32, _i64, _i32,
+                                             _f64, _f64, _f64, _p, _p, _p, _p,
+                                             _i32, _pi64]),
+    "tf_executor_join": (C.c_int, [_p, _p]),
+    "tf_executor_sync": (C.c_int, [_p]),
+    "tf_plan_capture_recon_flux": (C.c_int, [_pi32, _pi64, _pi32, _i64, _i32,
+                                             _p, _i64, _i32, _f64, _f64, _f64,
+                                             _p, _p, _p, _p, _i32,
+                                             C.POINTER(_p)]),
+    "tf_plan_launch": (C.c_int, [_p, _p]),
+    "tf_plan_kernels": (_i64, [_p]),
+    "tf_plan_destroy": (None, [_p]),
+    "tf_version": (C.c_char_p, []),
+    "tf_check_device": (C.c_int, [_i32]),
+}
+
+_lib = None
+
+
+def load(build_if_missing: bool | None = None) -> C.CDLL:
+    """Load (building first when allowed) the in-tree C-ABI library."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if build_if_missing is None:
+        build_if_missing = os.environ.get("TASKFUSE_NO_BUILD", "0") != "1"
+    if build_if_missing:
+        from ._build import build
+        build()
+    if not LIB_PATH.exists():
+        raise TaskfuseCudaError(
+            f"native library {LIB_PATH} is missing; run "
+            "`python -c 'import __graft_entry__ as g; g.build()'` — there is "
+            "no CPU fallback")
+    lib = C.CDLL(str(LIB_PATH), mode=C.RTLD_GLOBAL)
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+def check(rc: int, what: str) -> None:
+    if rc != 0:
+        if rc == TF_E_INVALID:
+            msg = "invalid argument"
+        elif rc == TF_E_NO_TMA:
+            msg = "cuTensorMapEncodeTiled unavailable"
+        else:
+            msg = f"CUDA error {rc}"
+        raise TaskfuseCudaError(f"{what} failed: {msg} (rc={rc})")

@@ -1,0 +1,481 @@
+// aggregator.cpp — strategy-3 team formation core and the real-time bulk
+// executor that feeds the batched sm_100a kernels.
+//
+// The formation state machine restates AggregationRegion.enter/_close/
+// _close_if_forming (reference aggregator.py:284-345) with the device
+// queries abstracted behind two signals:
+//   * stream_busy(executor)   -> device.stream_busy        (device.py:187-194)
+//   * tf_region_stream_idle() <- the stream-drain callback (device.py:364-370)
+// Fed the same signal sequence, it produces the same teams, parents and
+// slice ids as the reference (checked against recorded reference traces in
+// tests/test_aggregation_replay.py).  The executor wires the signals to real
+// CUDA streams: busy == the parent stream's last event has not completed.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "../../include/taskfuse_b200.h"
+
+namespace {
+
+// zlib crc32 (IEEE 802.3, reflected 0xEDB88320) — the reference derives each
+// region's lead executor from crc32(name) (aggregator.py:273).
+uint32_t crc32_ieee(const char* s) {
+  static uint32_t table[256];
+  static bool init = false;
+  if (!init) {
+    for (uint32_t i = 0; i < 256; ++i) {
+      uint32_t c = i;
+      for (int k = 0; k < 8; ++k) c = (c & 1) ? 0xEDB88320u ^ (c >> 1) : c >> 1;
+      table[i] = c;
+    }
+    init = true;
+  }
+  uint32_t c = 0xFFFFFFFFu;
+  for (const unsigned char* p = (const unsigned char*)s; *p; ++p)
+    c = table[(c ^ *p) & 0xFFu] ^ (c >> 8);
+  return c ^ 0xFFFFFFFFu;
+}
+
+enum { FORMING = 0, CAP = 1, SOLO = 2, DRAIN = 3 };
+
+struct Team {
+  int32_t parent = 0;
+  int32_t state = FORMING;  // FORMING or the closure reason
+  std::vector<int64_t> tags;
+};
+
+struct Parent {
+  int32_t executor = 0;
+  int64_t forming = -1;
+};
+
+}  // namespace
+
+struct tf_region {
+  std::string name;
+  int32_t max_team = 1;
+  int32_t executors = 1;
+  std::vector<Parent> parents;
+  int64_t arrivals = 0;
+  int64_t next_team = 0;
+  std::unordered_map<int64_t, Team> teams;
+  // per executor: forming teams holding a stream-idle watch, in watch order
+  std::vector<std::vector<int64_t>> watchers;
+  int64_t teams_formed = 0;
+  int64_t solo_fast_path = 0;
+  int64_t histogram[TF_MAX_TEAM + 1] = {0};
+};
+
+namespace {
+
+void close_team(tf_region* r, int64_t id, Team& t, int reason) {
+  t.state = reason;
+  r->teams_formed += 1;
+  r->histogram[t.tags.size()] += 1;
+  (void)id;
+}
+
+void unwatch(tf_region* r, int32_t executor, int64_t id) {
+  auto& w = r->watchers[executor];
+  auto it = std::find(w.begin(), w.end(), id);
+  if (it != w.end()) w.erase(it);
+}
+
+}  // namespace
+
+extern "C" {
+
+int tf_region_create(const char* name, int32_t max_team, int32_t parent_count,
+                     int32_t executors, tf_region** out) {
+  if (!name || !out || max_team < 1 || max_team > TF_MAX_TEAM ||
+      parent_count < 1 || executors < 1)
+    return TF_E_INVALID;
+  tf_region* r = new tf_region();
+  r->name = name;
+  r->max_team = max_team;
+  r->executors = executors;
+  const uint32_t lead = crc32_ieee(name) % (uint32_t)executors;
+  r->parents.resize(parent_count);
+  for (int32_t i = 0; i < parent_count; ++i)
+    r->parents[i].executor = (int32_t)((lead + (uint32_t)i) % (uint32_t)executors);
+  r->watchers.resize(executors);
+  *out = r;
+  return 0;
+}
+
+void tf_region_destroy(tf_region* r) { delete r; }
+
+int32_t tf_region_parent_executor(const tf_region* r, int32_t parent) {
+  if (!r || parent < 0 || parent >= (int32_t)r->parents.size()) return -1;
+  return r->parents[parent].executor;
+}
+
+int tf_region_enter(tf_region* r, int64_t tag, tf_busy_fn busy, void* ctx,
+                    tf_enter_result* out) {
+  if (!r || !out) return TF_E_INVALID;
+  const int32_t pi = (int32_t)(r->arrivals % (int64_t)r->parents.size());
+  r->arrivals += 1;
+  Parent& p = r->parents[pi];
+  int64_t id = p.forming;
+  if (id < 0) {
+    id = r->next_team++;
+    Team t;
+    t.parent = pi;
+    r->teams.emplace(id, std::move(t));
+  }
+  Team& t = r->teams[id];
+  out->parent = pi;
+  out->executor = p.executor;
+  out->team = id;
+  out->slice_id = (int32_t)t.tags.size();
+  out->closed = FORMING;
+  out->queried = 0;
+  t.tags.push_back(tag);
+  if ((int32_t)t.tags.size() >= r->max_team) {
+    // cap reached (max_team 1 closes instantly)           aggregator.py:310
+    if (p.forming == id) {
+      p.forming = -1;
+      unwatch(r, p.executor, id);
+    }
+    close_team(r, id, t, CAP);
+    out->closed = CAP;
+  } else if (p.forming < 0) {
+    out->queried = 1;
+    const int is_busy = busy ? busy(ctx, p.executor) : 1;
+    if (!is_busy) {
+      // device is starving: run alone rather than wait     aggregator.py:317
+      r->solo_fast_path += 1;
+      close_team(r, id, t, SOLO);
+      out->closed = SOLO;
+    } else {
+      p.forming = id;  // watch the stream for its drain  aggregator.py:321
+      r->watchers[p.executor].push_back(id);
+    }
+  }
+  return 0;
+}
+
+int tf_region_stream_idle(tf_region* r, int32_t executor, int64_t* out_teams,
+                          int32_t cap) {
+  if (!r || executor < 0 || executor >= r->executors) return -TF_E_INVALID;
+  std::vector<int64_t> fire;
+  fire.swap(r->watchers[executor]);
+  int32_t n = 0;
+  for (int64_t id : fire) {
+    auto it = r->teams.find(id);
+    if (it == r->teams.end() || it->second.state != FORMING) continue;
+    Parent& p = r->parents[it->second.parent];
+    if (p.forming == id) p.forming = -1;  // aggregator.py:328-332
+    close_team(r, id, it->second, DRAIN);
+    if (out_teams && n < cap) out_teams[n] = id;
+    ++n;
+  }
+  return n;
+}
+
+int tf_region_team_size(const tf_region* r, int64_t team) {
+  if (!r) return -TF_E_INVALID;
+  auto it = r->teams.find(team);
+  if (it == r->teams.end()) return -TF_E_INVALID;
+  return (int)it->second.tags.size();
+}
+
+int tf_region_team_members(const tf_region* r, int64_t team, int64_t* tags,
+                           int32_t cap) {
+  if (!r || !tags) return -TF_E_INVALID;
+  auto it = r->teams.find(team);
+  if (it == r->teams.end()) return -TF_E_INVALID;
+  const auto& v = it->second.tags;
+  const int32_t n = std::min<int32_t>(cap, (int32_t)v.size());
+  std::copy(v.begin(), v.begin() + n, tags);
+  return (int)v.size();
+}
+
+int tf_region_team_parent(const tf_region* r, int64_t team) {
+  if (!r) return -TF_E_INVALID;
+  auto it = r->teams.find(team);
+  if (it == r->teams.end()) return -TF_E_INVALID;
+  return it->second.parent;
+}
+
+int tf_region_stats(const tf_region* r, int64_t* teams_formed,
+                    int64_t* solo_fast_path, int64_t* histogram129) {
+  if (!r) return TF_E_INVALID;
+  if (teams_formed) *teams_formed = r->teams_formed;
+  if (solo_fast_path) *solo_fast_path = r->solo_fast_path;
+  if (histogram129)
+    for (int i = 0; i <= TF_MAX_TEAM; ++i) histogram129[i] = r->histogram[i];
+  return 0;
+}
+
+// Frees the bookkeeping of a closed team (the executor does this after the
+// launch; the Python facade after every member left).
+int tf_region_release_team(tf_region* r, int64_t team) {
+  if (!r) return TF_E_INVALID;
+  auto it = r->teams.find(team);
+  if (it == r->teams.end() || it->second.state == FORMING) return TF_E_INVALID;
+  r->teams.erase(it);
+  return 0;
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------ executor
+struct tf_executor {
+  tf_region* region = nullptr;
+  std::vector<cudaStream_t> streams;
+  std::vector<cudaEvent_t> last;
+  std::vector<char> recorded;
+};
+
+namespace {
+
+int rt_busy(void* ctx, int32_t e) {
+  tf_executor* ex = static_cast<tf_executor*>(ctx);
+  if (!ex->recorded[e]) return 0;
+  return cudaEventQuery(ex->last[e]) == cudaErrorNotReady;
+}
+
+struct ReconArgs {
+  const double* pool;
+  int64_t slices;
+  int32_t n;
+  double ax, ay, az;
+  double *um, *up, *F, *amax;
+  int32_t flux_form;
+};
+
+int launch_team(tf_executor* ex, int64_t team, const ReconArgs& a,
+                int64_t* launches) {
+  tf_region* r = ex->region;
+  auto it = r->teams.find(team);
+  if (it == r->teams.end()) return TF_E_INVALID;
+  const Team& t = it->second;
+  int32_t ids[TF_MAX_TEAM];
+  const int T = (int)t.tags.size();
+  for (int i = 0; i < T; ++i) ids[i] = (int32_t)t.tags[i];
+  const int32_t e = r->parents[t.parent].executor;
+  int rc = tf_recon_flux_team_f64(a.pool, a.slices, ids, T, a.n, a.ax, a.ay,
+                                  a.az, a.um, a.up, a.F, /*out_mode=*/1,
+                                  a.amax, a.flux_form,
+                                  (tf_stream_t)ex->streams[e]);
+  if (rc) return rc;
+  cudaError_t ce = cudaEventRecord(ex->last[e], ex->streams[e]);
+  if (ce != cudaSuccess) return ce;
+  ex->recorded[e] = 1;
+  r->teams.erase(it);
+  *launches += 1;
+  return 0;
+}
+
+int drain_executor(tf_executor* ex, int32_t e, const ReconArgs& a,
+                   int64_t* launches) {
+  std::vector<int64_t> closed(ex->region->watchers[e].size());
+  if (closed.empty()) return 0;
+  const int n = tf_region_stream_idle(ex->region, e, closed.data(),
+                                      (int32_t)closed.size());
+  if (n < 0) return -n;
+  for (int i = 0; i < n; ++i) {
+    int rc = launch_team(ex, closed[i], a, launches);
+    if (rc) return rc;
+  }
+  return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+int tf_executor_create(tf_region* region, int32_t count, tf_executor** out) {
+  if (!region || !out || count < 1 || count != region->executors)
+    return TF_E_INVALID;
+  tf_executor* ex = new tf_executor();
+  ex->region = region;
+  ex->streams.resize(count);
+  ex->last.resize(count);
+  ex->recorded.assign(count, 0);
+  for (int i = 0; i < count; ++i) {
+    cudaError_t e = cudaStreamCreateWithFlags(&ex->streams[i], cudaStreamNonBlocking);
+    if (e == cudaSuccess)
+      e = cudaEventCreateWithFlags(&ex->last[i], cudaEventDisableTiming);
+    if (e != cudaSuccess) {
+      delete ex;
+      return e;
+    }
+  }
+  *out = ex;
+  return 0;
+}
+
+void tf_executor_destroy(tf_executor* ex) {
+  if (!ex) return;
+  for (auto s : ex->streams) cudaStreamDestroy(s);
+  for (auto e : ex->last) cudaEventDestroy(e);
+  delete ex;
+}
+
+tf_stream_t tf_executor_stream(const tf_executor* ex, int32_t executor) {
+  if (!ex || executor < 0 || executor >= (int32_t)ex->streams.size())
+    return nullptr;
+  return (tf_stream_t)ex->streams[executor];
+}
+
+int tf_executor_run_recon_flux(tf_executor* ex, const double* pool_ext,
+                               int64_t pool_slices, const int32_t* ids,
+                               int64_t count, int32_t n, double ax, double ay,
+                               double az, double* um, double* up, double* F,
+                               double* amax, int32_t flux_form,
+                               int64_t* launches) {
+  if (!ex || !ids || count < 0 || !launches) return TF_E_INVALID;
+  ReconArgs a{pool_ext, pool_slices, n, ax, ay, az, um, up, F, amax, flux_form};
+  tf_region* r = ex->region;
+  const int32_t E = (int32_t)ex->streams.size();
+  *launches = 0;
+  for (int64_t i = 0; i < count; ++i) {
+    // real-time drain signal: before the arrival joins its parent's forming
+    // team, observe whether that parent's stream has gone idle meanwhile
+    const int32_t pi = (int32_t)(r->arrivals % (int64_t)r->parents.size());
+    const int32_t pe = r->parents[pi].executor;
+    if (!r->watchers[pe].empty() && !rt_busy(ex, pe)) {
+      int rc = drain_executor(ex, pe, a, launches);
+      if (rc) return rc;
+    }
+    if ((i & 31) == 31) {
+      for (int32_t e = 0; e < E; ++e)
+        if (e != pe && !r->watchers[e].empty() && !rt_busy(ex, e)) {
+          int rc = drain_executor(ex, e, a, launches);
+          if (rc) return rc;
+        }
+    }
+    tf_enter_result res;
+    int rc = tf_region_enter(r, ids[i], rt_busy, ex, &res);
+    if (rc) return rc;
+    if (res.closed != FORMING) {
+      rc = launch_team(ex, res.team, a, launches);
+      if (rc) return rc;
+    }
+  }
+  // no more arrivals: every stream eventually drains, closing what is left
+  for (int32_t e = 0; e < E; ++e) {
+    int rc = drain_executor(ex, e, a, launches);
+    if (rc) return rc;
+  }
+  return 0;
+}
+
+int tf_executor_join(tf_executor* ex, tf_stream_t stream) {
+  if (!ex) return TF_E_INVALID;
+  for (size_t e = 0; e < ex->streams.size(); ++e) {
+    cudaError_t ce = cudaEventRecord(ex->last[e], ex->streams[e]);
+    if (ce == cudaSuccess)
+      ce = cudaStreamWaitEvent((cudaStream_t)stream, ex->last[e], 0);
+    if (ce != cudaSuccess) return ce;
+    ex->recorded[e] = 1;
+  }
+  return 0;
+}
+
+int tf_executor_sync(tf_executor* ex) {
+  if (!ex) return TF_E_INVALID;
+  for (auto s : ex->streams) {
+    cudaError_t ce = cudaStreamSynchronize(s);
+    if (ce != cudaSuccess) return ce;
+  }
+  return 0;
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------- captured plans
+// A formed team plan (the teams the formation core closed for one
+// iteration's arrival sequence) captured once into a CUDA graph: one kernel
+// node per team, each team on its parent's executor branch, so replaying an
+// iteration costs one graph launch instead of one host launch per team.
+struct tf_plan {
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  int64_t kernels = 0;
+};
+
+extern "C" {
+
+int tf_plan_capture_recon_flux(const int32_t* ids, const int64_t* team_offsets,
+                               const int32_t* team_executor, int64_t nteams,
+                               int32_t executors, const double* pool_ext,
+                               int64_t pool_slices, int32_t n, double ax,
+                               double ay, double az, double* um, double* up,
+                               double* F, double* amax, int32_t flux_form,
+                               tf_plan** out) {
+  if (!ids || !team_offsets || !team_executor || nteams < 0 || executors < 1 ||
+      !out)
+    return TF_E_INVALID;
+  for (int64_t t = 0; t < nteams; ++t) {
+    const int64_t sz = team_offsets[t + 1] - team_offsets[t];
+    if (sz < 1 || sz > TF_MAX_TEAM || team_executor[t] < 0 ||
+        team_executor[t] >= executors)
+      return TF_E_INVALID;
+  }
+  std::vector<cudaStream_t> br(executors + 1);
+  std::vector<cudaEvent_t> ev(executors + 1);
+  int rc = 0;
+  for (int i = 0; i <= executors && !rc; ++i) {
+    rc = cudaStreamCreateWithFlags(&br[i], cudaStreamNonBlocking);
+    if (!rc) rc = cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming);
+  }
+  tf_plan* plan = new tf_plan();
+  cudaStream_t origin = br[executors];
+  if (!rc) rc = cudaStreamBeginCapture(origin, cudaStreamCaptureModeThreadLocal);
+  if (!rc) {
+    int crc = cudaEventRecord(ev[executors], origin);
+    for (int e = 0; e < executors && !crc; ++e)
+      crc = cudaStreamWaitEvent(br[e], ev[executors], 0);
+    for (int64_t t = 0; t < nteams && !crc; ++t) {
+      const int64_t lo = team_offsets[t];
+      const int T = (int)(team_offsets[t + 1] - lo);
+      crc = tf_recon_flux_team_f64(pool_ext, pool_slices, ids + lo, T, n, ax,
+                                   ay, az, um, up, F, 1, amax, flux_form,
+                                   (tf_stream_t)br[team_executor[t]]);
+      plan->kernels += 1;
+    }
+    for (int e = 0; e < executors && !crc; ++e) {
+      crc = cudaEventRecord(ev[e], br[e]);
+      if (!crc) crc = cudaStreamWaitEvent(origin, ev[e], 0);
+    }
+    int erc = cudaStreamEndCapture(origin, &plan->graph);
+    rc = crc ? crc : erc;
+  }
+  if (!rc) rc = cudaGraphInstantiate(&plan->exec, plan->graph, 0);
+  for (int i = 0; i <= executors; ++i) {
+    if (br[i]) cudaStreamDestroy(br[i]);
+    if (ev[i]) cudaEventDestroy(ev[i]);
+  }
+  if (rc) {
+    if (plan->exec) cudaGraphExecDestroy(plan->exec);
+    if (plan->graph) cudaGraphDestroy(plan->graph);
+    delete plan;
+    return rc;
+  }
+  *out = plan;
+  return 0;
+}
+
+int tf_plan_launch(tf_plan* plan, tf_stream_t stream) {
+  if (!plan || !plan->exec) return TF_E_INVALID;
+  return cudaGraphLaunch(plan->exec, (cudaStream_t)stream);
+}
+
+int64_t tf_plan_kernels(const tf_plan* plan) { return plan ? plan->kernels : -1; }
+
+void tf_plan_destroy(tf_plan* plan) {
+  if (!plan) return;
+  if (plan->exec) cudaGraphExecDestroy(plan->exec);
+  if (plan->graph) cudaGraphDestroy(plan->graph);
+  delete plan;
+}
+
+}  // extern "C"

@@ -1,0 +1,542 @@
+// hydro_kernels.cu — sm_100a kernels for the strategy-3 hydro hot path.
+//
+// Batched re-statements of the reference per-sub-grid numpy bodies
+// (/root/reference/pkg/src/taskfuse/hydro/kernels.py), indexed by
+// (aggregated slice, cell).  The arithmetic is the reference's, operation
+// for operation, with FMA contraction forbidden (explicit __d*_rn
+// intrinsics), so every output is bit-identical to the CPU path:
+//   minmod      kernels.py:58-60   where(a*b<=0, 0, where(|a|<|b|, a, b))
+//   reconstruct kernels.py:73-81   um = base - 0.5*s ; up = base + 0.5*s
+//   flux        kernels.py:84-93   F = a*up  |  a*roll(um, -1, axis)
+//   update      kernels.py:100-111 u - dt_dx*((dFx) + (dFy)) + (dFz)
+//   ghosts      scenario.py:124-142 periodic 26-neighbour fill
+//
+// Data movement (B200): the fused reconstruct+flux kernel stages each
+// slice's (n+4)^3 stencil box — the smallest box covering the 6-point star
+// the stencil reads — from HBM into shared memory with ONE TMA
+// tensor load (cp.async.bulk.tensor.4d, mbarrier completion), so a gather
+// of strided team members costs nothing extra: the slice's
+// sub-grid id is just the 4th TMA coordinate.  Outputs (um, up, F: 90% of
+// the bytes) leave through coalesced streaming stores.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+#include <stdint.h>
+
+#include <mutex>
+#include <unordered_map>
+
+#include "../../include/taskfuse_b200.h"
+
+namespace {
+
+template <int N>
+struct Geo {
+  static constexpr int C = N + 2;      // face / flux cube edge
+  static constexpr int E = N + 6;      // ghosted edge (GHOST = 3)
+  static constexpr int B = N + 4;      // stencil box edge, ext index 1..N+4
+  static constexpr int CELLS = C * C * C;
+  static constexpr int BOX = B * B * B;
+  static constexpr int EXT3 = E * E * E;
+  static constexpr int OWN = N * N * N;
+};
+
+struct TeamIds {
+  int32_t id[TF_MAX_TEAM];
+};
+
+// ---------------------------------------------------------------- PTX glue
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(count)
+               : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile(
+      "mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "r"(bytes)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "LAB_WAIT:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@P1 bra DONE;\n"
+      "bra LAB_WAIT;\n"
+      "DONE:\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_box(void* dst, const CUtensorMap* map,
+                                             int c0, int c1, int c2, int c3,
+                                             uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::"
+      "complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3),
+      "r"(smem_u32(bar))
+      : "memory");
+}
+
+// --------------------------------------------------------------- numerics
+// kernels.py:58-60 — product test first, then strict |a|<|b|.  NaN in the
+// product fails `<= 0` and NaN in |a| fails `<`, both yielding b, as numpy.
+__device__ __forceinline__ double minmod(double a, double b) {
+  return (__dmul_rn(a, b) <= 0.0) ? 0.0 : ((fabs(a) < fabs(b)) ? a : b);
+}
+
+// Slope at stencil-box index b along stride st (kernels.py:76-79):
+// sigma = minmod(w[+e] - base, base - w[-e]).
+__device__ __forceinline__ double slope(const double* __restrict__ s, int b,
+                                        int st) {
+  const double base = s[b];
+  return minmod(__dsub_rn(s[b + st], base), __dsub_rn(base, s[b - st]));
+}
+
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// Fused reconstruct + flux.  MODE 0: um, up and F; MODE 1: um, up only
+// (reconstruct_body alone).  One CTA per aggregated slice.
+template <int N, int THREADS, int MODE, bool DEV_IDS>
+__global__ void __launch_bounds__(THREADS)
+    k_recon_flux(const __grid_constant__ CUtensorMap tmap,
+                 const int32_t* __restrict__ dev_ids,
+                 const __grid_constant__ TeamIds team, int out_mode, double ax,
+                 double ay, double az, double* __restrict__ um,
+                 double* __restrict__ up, double* __restrict__ F,
+                 double* __restrict__ amax, int flux_form) {
+  using G = Geo<N>;
+  constexpr int C = G::C, B = G::B, CELLS = G::CELLS;
+  extern __shared__ __align__(128) double sbox[];
+  __shared__ __align__(8) uint64_t bar;
+  __shared__ double red[THREADS / 32];
+
+  const int s = blockIdx.x;
+  const int g = DEV_IDS ? (dev_ids ? dev_ids[s] : s) : team.id[s];
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    mbar_expect_tx(&bar, G::BOX * (uint32_t)sizeof(double));
+    // box origin = extended index (1,1,1) of sub-grid g; coords innermost first
+    tma_load_box(sbox, &tmap, 1, 1, 1, g, &bar);
+  }
+  __syncthreads();  // barrier initialised before anyone polls it
+  mbar_wait(&bar, 0);
+
+  const int64_t slot = out_mode ? (int64_t)g : (int64_t)s;
+  double* __restrict__ um_s = um + slot * 3 * CELLS;
+  double* __restrict__ up_s = up + slot * 3 * CELLS;
+  double* __restrict__ F_s = MODE == 0 ? F + slot * 3 * CELLS : nullptr;
+  const double av[3] = {ax, ay, az};
+  const int stv[3] = {B * B, B, 1};
+  double speed = 0.0;
+
+  for (int c = threadIdx.x; c < CELLS; c += THREADS) {
+    const int ci = c / (C * C);
+    const int cj = (c / C) % C;
+    const int ck = c % C;
+    const int cv[3] = {ci, cj, ck};
+    const int b = ((ci + 1) * B + (cj + 1)) * B + (ck + 1);
+    const double base = sbox[b];
+#pragma unroll
+    for (int axis = 0; axis < 3; ++axis) {
+      const int st = stv[axis];
+      const double half = __dmul_rn(0.5, slope(sbox, b, st));
+      const double vm = __dsub_rn(base, half);
+      const double vp = __dadd_rn(base, half);
+      __stcs(um_s + axis * CELLS + c, vm);
+      __stcs(up_s + axis * CELLS + c, vp);
+      if (MODE == 0) {
+        const double a = av[axis];
+        double f;
+        // minus state of the next cell along the axis; np.roll(.., -1)
+        // wraps the last layer onto layer 0 (kernels.py:90-93)
+        const bool need_next = (a < 0.0) || flux_form == 1;
+        double next_m = 0.0;
+        if (need_next) {
+          const int bn = (cv[axis] == C - 1) ? b - (C - 1) * st : b + st;
+          const double hn = __dmul_rn(0.5, slope(sbox, bn, st));
+          next_m = __dsub_rn(sbox[bn], hn);
+        }
+        if (flux_form == 0) {
+          f = (a >= 0.0) ? __dmul_rn(a, vp) : __dmul_rn(a, next_m);
+        } else {
+          // Kurganov-Tadmor central-upwind: 1/2(f_L+f_R) - 1/2 a_max (u_R-u_L)
+          const double amx = fabs(a);
+          const double fl = __dmul_rn(a, vp), fr = __dmul_rn(a, next_m);
+          f = __dsub_rn(__dmul_rn(0.5, __dadd_rn(fl, fr)),
+                        __dmul_rn(__dmul_rn(0.5, amx), __dsub_rn(next_m, vp)));
+        }
+        __stcs(F_s + axis * CELLS + c, f);
+        speed = fmax(speed, fabs(a));  // local signal speed of this face
+      }
+    }
+  }
+  if (MODE == 0 && amax != nullptr) {
+    speed = warp_max(speed);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = speed;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      double v = threadIdx.x < THREADS / 32 ? red[threadIdx.x] : 0.0;
+      v = warp_max(v);
+      if (threadIdx.x == 0) amax[slot] = v;
+    }
+  }
+}
+
+// flux_body alone (kernels.py:84-93), elementwise over (slot, axis, cell).
+template <int N>
+__global__ void __launch_bounds__(256)
+    k_flux(const int32_t* __restrict__ ids, int T, int out_mode, double ax,
+           double ay, double az, const double* __restrict__ um,
+           const double* __restrict__ up, double* __restrict__ F) {
+  using G = Geo<N>;
+  constexpr int C = G::C, CELLS = G::CELLS;
+  const int64_t total = (int64_t)T * 3 * CELLS;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int s = (int)(i / (3 * CELLS));
+    const int r = (int)(i % (3 * CELLS));
+    const int axis = r / CELLS;
+    const int c = r % CELLS;
+    const int64_t slot = out_mode ? (int64_t)(ids ? ids[s] : s) : (int64_t)s;
+    const double a = axis == 0 ? ax : (axis == 1 ? ay : az);
+    const int64_t off = slot * 3 * CELLS + (int64_t)axis * CELLS;
+    double f;
+    if (a >= 0.0) {
+      f = __dmul_rn(a, up[off + c]);
+    } else {
+      const int st = axis == 0 ? C * C : (axis == 1 ? C : 1);
+      const int pos = (c / st) % C;
+      const int cn = pos == C - 1 ? c - (C - 1) * st : c + st;
+      f = __dmul_rn(a, um[off + cn]);
+    }
+    F[off + c] = f;
+  }
+}
+
+// update_body (kernels.py:100-111): no FMA anywhere, x,y,z accumulation order.
+template <int N>
+__global__ void __launch_bounds__(256)
+    k_update(const double* __restrict__ pool, const int32_t* __restrict__ ids,
+             int out_mode, const double* __restrict__ F, double dt_dx,
+             double* __restrict__ next) {
+  using G = Geo<N>;
+  constexpr int C = G::C, E = G::E, CELLS = G::CELLS;
+  const int s = blockIdx.x;
+  const int g = ids ? ids[s] : s;
+  const int64_t slot = out_mode ? (int64_t)g : (int64_t)s;
+  const double* __restrict__ Fs = F + slot * 3 * CELLS;
+  const double* __restrict__ u = pool + (int64_t)g * G::EXT3;
+  double* __restrict__ o = next + (int64_t)g * G::EXT3;
+  for (int c = threadIdx.x; c < G::OWN; c += blockDim.x) {
+    const int i = c / (N * N), j = (c / N) % N, k = c % N;
+    const int own = ((i + 1) * C + (j + 1)) * C + (k + 1);
+    double div = __dsub_rn(Fs[own], Fs[own - C * C]);
+    div = __dadd_rn(div, __dsub_rn(Fs[CELLS + own], Fs[CELLS + own - C]));
+    div = __dadd_rn(div, __dsub_rn(Fs[2 * CELLS + own], Fs[2 * CELLS + own - 1]));
+    const int e = ((i + 3) * E + (j + 3)) * E + (k + 3);
+    o[e] = __dsub_rn(u[e], __dmul_rn(dt_dx, div));
+  }
+}
+
+// exchange_ghosts (scenario.py:124-142): every ghost cell of sub-grid g is
+// the periodic global cell it overlays, i.e. a neighbour's owned cell.
+template <int N>
+__global__ void __launch_bounds__(256)
+    k_ghost_fill(double* __restrict__ pool, const int32_t* __restrict__ ids,
+                 int per_axis) {
+  using G = Geo<N>;
+  constexpr int E = G::E;
+  const int s = blockIdx.x;
+  const int g = ids ? ids[s] : s;
+  const int m = per_axis, grid = per_axis * N;
+  const int bx = g / (m * m), by = (g / m) % m, bz = g % m;
+  double* __restrict__ dst = pool + (int64_t)g * G::EXT3;
+  for (int c = threadIdx.x; c < G::EXT3; c += blockDim.x) {
+    const int i = c / (E * E), j = (c / E) % E, k = c % E;
+    const bool owned = i >= 3 && i < N + 3 && j >= 3 && j < N + 3 && k >= 3 &&
+                       k < N + 3;
+    if (owned) continue;
+    const int gi = (bx * N + i - 3 + grid) % grid;
+    const int gj = (by * N + j - 3 + grid) % grid;
+    const int gk = (bz * N + k - 3 + grid) % grid;
+    const int src = ((gi / N) * m + (gj / N)) * m + (gk / N);
+    const int e = ((gi % N + 3) * E + (gj % N + 3)) * E + (gk % N + 3);
+    dst[c] = pool[(int64_t)src * G::EXT3 + e];
+  }
+}
+
+// prep_body (kernels.py:69-70): whole-extended-array copy, 16 B vectors.
+template <int N>
+__global__ void __launch_bounds__(256)
+    k_prep(const double* __restrict__ pool, const int32_t* __restrict__ ids,
+           int out_mode, double* __restrict__ w) {
+  using G = Geo<N>;
+  const int s = blockIdx.x;
+  const int g = ids ? ids[s] : s;
+  const int64_t slot = out_mode ? (int64_t)g : (int64_t)s;
+  const double2* __restrict__ src =
+      reinterpret_cast<const double2*>(pool + (int64_t)g * G::EXT3);
+  double2* __restrict__ dst = reinterpret_cast<double2*>(w + slot * G::EXT3);
+  for (int c = threadIdx.x; c < G::EXT3 / 2; c += blockDim.x) dst[c] = src[c];
+}
+
+__global__ void k_reduce(const int32_t* __restrict__ ids, int T, int out_mode,
+                         double v, double* __restrict__ out) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= T) return;
+  const int64_t slot = out_mode ? (int64_t)(ids ? ids[s] : s) : (int64_t)s;
+  out[slot] = v;
+}
+
+// ------------------------------------------------------------ host side
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault,
+                                &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+struct MapKey {
+  const void* ptr;
+  int64_t slices;
+  int n;
+  bool operator==(const MapKey& o) const {
+    return ptr == o.ptr && slices == o.slices && n == o.n;
+  }
+};
+struct MapKeyHash {
+  size_t operator()(const MapKey& k) const {
+    return std::hash<const void*>()(k.ptr) ^ (size_t)(k.slices * 131 + k.n);
+  }
+};
+
+// 4-D view (slice, x, y, z) of the pool; box = the (n+4)^3 stencil box.
+int pool_map(const double* pool, int64_t slices, int n, CUtensorMap* out) {
+  static std::mutex mu;
+  static std::unordered_map<MapKey, CUtensorMap, MapKeyHash> cache;
+  const MapKey key{pool, slices, n};
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = cache.find(key);
+  if (it != cache.end()) {
+    *out = it->second;
+    return 0;
+  }
+  auto fn = encode_fn();
+  if (!fn) return TF_E_NO_TMA;
+  const cuuint64_t E = (cuuint64_t)(n + 6);
+  const cuuint32_t Bx = (cuuint32_t)(n + 4);
+  cuuint64_t dims[4] = {E, E, E, (cuuint64_t)slices};
+  cuuint64_t strides[3] = {E * 8, E * E * 8, E * E * E * 8};
+  cuuint32_t box[4] = {Bx, Bx, Bx, 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUtensorMap m;
+  CUresult r = fn(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4,
+                  const_cast<double*>(pool), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return TF_E_INVALID;
+  if (cache.size() > 256) cache.clear();
+  cache.emplace(key, m);
+  *out = m;
+  return 0;
+}
+
+template <int N>
+constexpr int recon_threads() {
+  return N == 8 ? 256 : 512;
+}
+
+template <int N, int MODE, bool DEV_IDS>
+int launch_recon(const CUtensorMap& map, const int32_t* dev_ids,
+                 const TeamIds& team, int T, int out_mode, double ax, double ay,
+                 double az, double* um, double* up, double* F, double* amax,
+                 int flux_form, cudaStream_t st) {
+  constexpr int TH = recon_threads<N>();
+  constexpr size_t smem = Geo<N>::BOX * sizeof(double);
+  auto kern = k_recon_flux<N, TH, MODE, DEV_IDS>;
+  static bool attr_done = false;  // benign race: idempotent attribute set
+  if (!attr_done) {
+    cudaError_t e = cudaFuncSetAttribute(
+        kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr_done = true;
+  }
+  kern<<<T, TH, smem, st>>>(map, dev_ids, team, out_mode, ax, ay, az, um, up,
+                            F, amax, flux_form);
+  return cudaGetLastError();
+}
+
+template <int MODE, bool DEV_IDS>
+int dispatch_recon(const double* pool, int64_t slices, const int32_t* dev_ids,
+                   const TeamIds& team, int T, int n, int out_mode, double ax,
+                   double ay, double az, double* um, double* up, double* F,
+                   double* amax, int flux_form, cudaStream_t st) {
+  if (T == 0) return 0;
+  CUtensorMap map;
+  int rc = pool_map(pool, slices, n, &map);
+  if (rc) return rc;
+  if (n == 8)
+    return launch_recon<8, MODE, DEV_IDS>(map, dev_ids, team, T, out_mode, ax,
+                                          ay, az, um, up, F, amax, flux_form,
+                                          st);
+  return launch_recon<16, MODE, DEV_IDS>(map, dev_ids, team, T, out_mode, ax,
+                                         ay, az, um, up, F, amax, flux_form,
+                                         st);
+}
+
+bool valid_n(int n) { return n == 8 || n == 16; }
+
+}  // namespace
+
+extern "C" {
+
+int tf_recon_flux_f64(const double* pool_ext, int64_t pool_slices,
+                      const int32_t* ids, int32_t T, int32_t n, double ax,
+                      double ay, double az, double* um, double* up, double* F,
+                      int32_t out_mode, double* amax, int32_t flux_form,
+                      tf_stream_t stream) {
+  if (!valid_n(n) || T < 0 || !pool_ext || !um || !up || !F ||
+      (flux_form != 0 && flux_form != 1) || pool_slices < 1 ||
+      (ids == nullptr && T > pool_slices))
+    return TF_E_INVALID;
+  static const TeamIds none{};
+  return dispatch_recon<0, true>(pool_ext, pool_slices, ids, none, T, n,
+                                 out_mode, ax, ay, az, um, up, F, amax,
+                                 flux_form, (cudaStream_t)stream);
+}
+
+int tf_recon_flux_team_f64(const double* pool_ext, int64_t pool_slices,
+                           const int32_t* host_ids, int32_t T, int32_t n,
+                           double ax, double ay, double az, double* um,
+                           double* up, double* F, int32_t out_mode,
+                           double* amax, int32_t flux_form,
+                           tf_stream_t stream) {
+  if (!valid_n(n) || T < 1 || T > TF_MAX_TEAM || !host_ids || !pool_ext ||
+      !um || !up || !F || (flux_form != 0 && flux_form != 1))
+    return TF_E_INVALID;
+  TeamIds team;
+  for (int i = 0; i < T; ++i) {
+    if (host_ids[i] < 0 || host_ids[i] >= pool_slices) return TF_E_INVALID;
+    team.id[i] = host_ids[i];
+  }
+  return dispatch_recon<0, false>(pool_ext, pool_slices, nullptr, team, T, n,
+                                  out_mode, ax, ay, az, um, up, F, amax,
+                                  flux_form, (cudaStream_t)stream);
+}
+
+int tf_reconstruct_f64(const double* pool_ext, int64_t pool_slices,
+                       const int32_t* ids, int32_t T, int32_t n, double* um,
+                       double* up, int32_t out_mode, tf_stream_t stream) {
+  if (!valid_n(n) || T < 0 || !pool_ext || !um || !up || pool_slices < 1 ||
+      (ids == nullptr && T > pool_slices))
+    return TF_E_INVALID;
+  static const TeamIds none{};
+  return dispatch_recon<1, true>(pool_ext, pool_slices, ids, none, T, n,
+                                 out_mode, 0, 0, 0, um, up, nullptr, nullptr,
+                                 0, (cudaStream_t)stream);
+}
+
+int tf_flux_f64(const int32_t* ids, int32_t T, int32_t n, double ax, double ay,
+                double az, const double* um, const double* up, double* F,
+                int32_t out_mode, tf_stream_t stream) {
+  if (!valid_n(n) || T < 0 || !um || !up || !F) return TF_E_INVALID;
+  if (T == 0) return 0;
+  const int64_t total = (int64_t)T * 3 * (n + 2) * (n + 2) * (n + 2);
+  const int blocks = (int)((total + 255) / 256 < 148 * 16 ? (total + 255) / 256
+                                                          : 148 * 16);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (n == 8)
+    k_flux<8><<<blocks, 256, 0, st>>>(ids, T, out_mode, ax, ay, az, um, up, F);
+  else
+    k_flux<16><<<blocks, 256, 0, st>>>(ids, T, out_mode, ax, ay, az, um, up, F);
+  return cudaGetLastError();
+}
+
+int tf_update_f64(const double* pool_ext, const int32_t* ids, int32_t T,
+                  int32_t n, const double* F, int32_t out_mode, double dt_dx,
+                  double* next_ext, tf_stream_t stream) {
+  if (!valid_n(n) || T < 0 || !pool_ext || !F || !next_ext)
+    return TF_E_INVALID;
+  if (T == 0) return 0;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (n == 8)
+    k_update<8><<<T, 256, 0, st>>>(pool_ext, ids, out_mode, F, dt_dx, next_ext);
+  else
+    k_update<16><<<T, 256, 0, st>>>(pool_ext, ids, out_mode, F, dt_dx,
+                                    next_ext);
+  return cudaGetLastError();
+}
+
+int tf_ghost_fill_f64(double* pool_ext, const int32_t* ids, int32_t T,
+                      int32_t n, int32_t per_axis, tf_stream_t stream) {
+  if (!valid_n(n) || per_axis < 1 || !pool_ext) return TF_E_INVALID;
+  const int64_t S = (int64_t)per_axis * per_axis * per_axis;
+  if (ids == nullptr) T = (int32_t)S;
+  if (T < 0 || (ids == nullptr && T != S)) return TF_E_INVALID;
+  if (T == 0) return 0;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (n == 8)
+    k_ghost_fill<8><<<T, 256, 0, st>>>(pool_ext, ids, per_axis);
+  else
+    k_ghost_fill<16><<<T, 256, 0, st>>>(pool_ext, ids, per_axis);
+  return cudaGetLastError();
+}
+
+int tf_prep_f64(const double* pool_ext, const int32_t* ids, int32_t T,
+                int32_t n, double* w, int32_t out_mode, tf_stream_t stream) {
+  if (!valid_n(n) || T < 0 || !pool_ext || !w) return TF_E_INVALID;
+  if (T == 0) return 0;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (n == 8)
+    k_prep<8><<<T, 256, 0, st>>>(pool_ext, ids, out_mode, w);
+  else
+    k_prep<16><<<T, 256, 0, st>>>(pool_ext, ids, out_mode, w);
+  return cudaGetLastError();
+}
+
+int tf_reduce_f64(const int32_t* ids, int32_t T, double ax, double ay,
+                  double az, double* reduce_out, int32_t out_mode,
+                  tf_stream_t stream) {
+  if (T < 0 || !reduce_out) return TF_E_INVALID;
+  if (T == 0) return 0;
+  // max_speed (scenario.py:40-41): max(|v|) over the velocity components
+  double v = fabs(ax);
+  v = fabs(ay) > v ? fabs(ay) : v;
+  v = fabs(az) > v ? fabs(az) : v;
+  k_reduce<<<(T + 127) / 128, 128, 0, (cudaStream_t)stream>>>(
+      ids, T, out_mode, v, reduce_out);
+  return cudaGetLastError();
+}
+
+const char* tf_version(void) { return "taskfuse_b200 0.1 sm_100a"; }
+
+int tf_check_device(int32_t dev) {
+  cudaDeviceProp p;
+  cudaError_t e = cudaGetDeviceProperties(&p, dev);
+  if (e != cudaSuccess) return e;
+  return (p.major == 10 && p.minor == 0) ? 0 : TF_E_INVALID;
+}
+
+}  // extern "C"
