@@ -1,0 +1,452 @@
+#!/usr/bin/env python
+"""Benchmark: strategy-3 aggregated FP64 hydro reconstruct+flux on B200.
+
+Metric (BASELINE.json): sub-grid cell-updates/s of the hydro
+reconstruct+flux hot path vs aggregation level, and % of HBM peak.
+
+Workload (BASELINE.json configs[1]): Sod shock tube, 4096 8^3 sub-grids
+(grid 128^3), velocity (1,1,1).  One STEP = one iteration of the aggregated
+reconstruct+flux region over all sub-grids: the 4096 task arrivals are
+formed into teams by the strategy-3 formation core (max_team = 128 by
+default, parents = S/max_team as HydroSim does, step.py:61), each team is one
+launch of the batched TMA kernel, and the iteration's team launches replay as
+one CUDA graph over the executor streams.  Inputs are device-resident; two
+input pools alternate between steps (per-step working set 385 MB, 3x L2).
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+
+Multi-GPU (torchrun): weak scaling, each rank owns its own 4096 sub-grids;
+the step has no data-path collective (the recon+flux region is
+embarrassingly parallel), value = all ranks' cell-updates / max-rank time.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = ("sub-grid cell-updates/sec (hydro reconstruct+flux) vs "
+          "aggregation; % HBM peak")
+UNIT = "cell-updates/s"
+GRID, N_SUB, FIELD = 128, 8, "sod"
+VELOCITY = (1.0, 1.0, 1.0)
+
+
+def b_alg(n: int) -> int:
+    """Algorithmic bytes per sub-grid-iteration (SURVEY §8 d): the distinct
+    stencil cells read ((n+2)^3 + 6(n+2)^2) plus um, up, F written
+    (9 (n+2)^3), FP64."""
+    c = n + 2
+    return 8 * (c ** 3 + 6 * c ** 2 + 9 * c ** 3)
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            p = json.load(fh)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# --------------------------------------------------------------- clocks
+class ClockSampler:
+    """NVML SM clock + throttle reasons while the GPU is under load."""
+
+    BITS = {0x4: "sw_power_cap", 0x8: "hw_slowdown",
+            0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+            0x80: "hw_power_brake_slowdown", 0x2: "applications_clocks",
+            0x1: "gpu_idle"}
+
+    def __init__(self, index: int):
+        self.samples, self.reasons = [], set()
+        self._stop = threading.Event()
+        self.max_mhz = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(
+                self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(
+                    self.h, self.nv.NVML_CLOCK_SM))
+                mask = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.BITS.items():
+                    if mask & bit and bit != 0x1:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.01)
+
+    def __enter__(self):
+        if self.nv is not None:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *exc):
+        if self.nv is not None:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz,
+                    "reasons": sorted(self.reasons), "samples": 0}
+        return {"sm_mhz": statistics.median(self.samples),
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------- dist plumbing
+def dist_setup(gpus: int):
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    elif torch.cuda.is_available():
+        torch.cuda.set_device(0)
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(world, x: float) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def timed(fn, steps, warmup, world, stream):
+    """W untimed steps, then EXACTLY `steps` steps between barrier+sync on
+    both sides, CUDA events on the launching stream; ms/step (max ranks)."""
+    import torch
+    for k in range(warmup):
+        fn(k)
+    torch.cuda.synchronize()
+    barrier(world)
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for k in range(steps):
+        fn(k)
+    t1.record(stream)
+    torch.cuda.synchronize()
+    barrier(world)
+    return max_over_ranks(world, t0.elapsed_time(t1) / steps)
+
+
+# ------------------------------------------------------------- workload
+class Workload:
+    def __init__(self, n=N_SUB, grid=GRID, field=FIELD, pools=2):
+        import torch
+        from paper_2210_06438_b200 import ops
+        from paper_2210_06438_b200.hydro import (initial_field,
+                                                 pool_from_field, sod_field)
+        self.n, self.grid = n, grid
+        self.m = grid // n
+        self.S = self.m ** 3
+        f = (sod_field if field == "sod" else initial_field)(grid, "cuda")
+        self.pools = []
+        for _ in range(pools):
+            p = pool_from_field(f, n)
+            ops.ghost_fill(p, n, self.m)
+            self.pools.append(p)
+        c = n + 2
+        shape = (self.S, 3, c, c, c)
+        self.um = torch.empty(shape, dtype=torch.float64, device="cuda")
+        self.up = torch.empty_like(self.um)
+        self.F = torch.empty_like(self.um)
+        self.amax = torch.empty(self.S, dtype=torch.float64, device="cuda")
+        torch.cuda.synchronize()
+
+
+def plan_runner(wl, max_team, executors, parents=None):
+    from paper_2210_06438_b200.strategy3 import TeamPlan, form_teams
+    teams = form_teams(range(wl.S), max_team, executors, parents)
+    plans = [TeamPlan(teams, p, wl.n, VELOCITY, wl.um, wl.up, wl.F,
+                      executors, amax=wl.amax) for p in wl.pools]
+    hist = {}
+    for t in teams:
+        hist[len(t.ids)] = hist.get(len(t.ids), 0) + 1
+
+    def step(k):
+        plans[k % len(plans)].launch()
+    return step, len(teams), hist, plans
+
+
+def realtime_runner(wl, max_team, executors, parents=None):
+    from paper_2210_06438_b200.strategy3 import (RealtimeExecutor,
+                                                 default_parents)
+    parents = parents or default_parents(wl.S, max_team)
+    ex = RealtimeExecutor("reconstruct", max_team, executors, parents)
+    arrivals = list(range(wl.S))
+    launches = []
+
+    def step(k):
+        launches.append(ex.run(wl.pools[k % len(wl.pools)], wl.n, VELOCITY,
+                               arrivals, wl.um, wl.up, wl.F, amax=wl.amax))
+    return step, launches, ex
+
+
+def single_runner(wl):
+    from paper_2210_06438_b200 import ops
+
+    def step(k):
+        ops.recon_flux(wl.pools[k % len(wl.pools)], wl.n, VELOCITY, wl.um,
+                       wl.up, wl.F, out_mode=1, amax=wl.amax)
+    return step
+
+
+def rate(S, n, ms):
+    return S * n ** 3 / (ms * 1e-3)
+
+
+def run_sweep(wl, args, world, stream, peak):
+    """Aggregation sweep 1..128 (plan-graph and real-time executor),
+    strategy 2 (A=1 over many streams), strategy 1 (16^3, A=1)."""
+    out = {"aggregation": {}, "realtime": {}, "strategy2": {},
+           "strategy1": {}}
+    ks, kw = max(5, args.steps // 2), 3
+    for A in (1, 4, 16, 64, 128):
+        step, nk, hist, _ = plan_runner(wl, A, args.executors)
+        ms = timed(step, ks, kw, world, stream)
+        out["aggregation"][A] = {
+            "cell_updates_per_s": rate(wl.S, wl.n, ms), "ms_per_iter": ms,
+            "launches": nk, "hbm_frac": wl.S * b_alg(wl.n) / (ms * 1e-3)
+            / (peak * 1e9)}
+        rstep, launches, ex = realtime_runner(wl, A, args.executors)
+        ms = timed(rstep, ks, kw, world, stream)
+        st = ex.stats()
+        out["realtime"][A] = {
+            "cell_updates_per_s": rate(wl.S, wl.n, ms), "ms_per_iter": ms,
+            "launches_per_iter": launches[-1],
+            "mean_team": wl.S * len(launches) / max(1, st["teams_formed"]),
+            "solo_fast_path": st["solo_fast_path"]}
+    for E in (1, 8, 32, 128):
+        # strategy 2: per-task launches (A = 1) spread over E streams
+        step, nk, _, _ = plan_runner(wl, 1, E, parents=E)
+        ms = timed(step, ks, kw, world, stream)
+        out["strategy2"][E] = {"cell_updates_per_s": rate(wl.S, wl.n, ms),
+                               "ms_per_iter": ms, "launches": nk}
+    wl16 = Workload(n=16, grid=wl.grid, field=FIELD)
+    for A in (1,):
+        step, nk, _, _ = plan_runner(wl16, A, args.executors)
+        ms = timed(step, ks, kw, world, stream)
+        out["strategy1"][f"16^3_A{A}"] = {
+            "cell_updates_per_s": rate(wl16.S, 16, ms), "ms_per_iter": ms,
+            "launches": nk, "hbm_frac": wl16.S * b_alg(16) / (ms * 1e-3)
+            / (peak * 1e9)}
+    del wl16
+    return out
+
+
+def cpu_baseline_leg(S, n, grid, steps=2, min_seconds=10.0):
+    from oracle.cpu_baseline import CpuBaseline, cpu_model
+    cb = CpuBaseline(FIELD, grid, n, VELOCITY, range(S))
+    try:
+        times = []
+        t_start = time.perf_counter()
+        while len(times) < steps or (time.perf_counter() - t_start
+                                     < min_seconds / cb.workers
+                                     and len(times) < 20):
+            times.append(cb.step())
+        best = min(times)
+    finally:
+        cb.close()
+    return {"value": rate(S, n, best * 1e3), "unit": UNIT,
+            "cores": cb.workers, "kind": "port",
+            "sample": (f"all {S} 8^3 sub-grids of config 2 per pass "
+                       f"(prep+reconstruct+flux bodies, oracle port of "
+                       f"hydro/kernels.py), spawn pool of {cb.workers} "
+                       f"workers, slowest worker, best of {len(times)} "
+                       f"passes; CPU {cpu_model()}")}
+
+
+def reference_arm(args, world, rank):
+    """--impl reference: the reference's CPU path (oracle port; the
+    reference is pure Python and is not present on GPU boxes) on all host
+    cores, same metric/config/unit."""
+    if rank != 0:
+        return
+    from oracle.cpu_baseline import CpuBaseline, cpu_model
+    S = (GRID // N_SUB) ** 3
+    cb = CpuBaseline(FIELD, GRID, N_SUB, VELOCITY, range(S))
+    try:
+        for _ in range(args.warmup):
+            cb.step()
+        times = [cb.step() for _ in range(args.steps)]
+    finally:
+        cb.close()
+    ms = 1e3 * sum(times) / len(times)
+    value = rate(S, N_SUB, ms)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "config 2: Sod shock tube, 4096 8^3 "
+                   "sub-grids, one reconstruct+flux iteration per step",
+                   "subgrids": S, "subgrid_n": N_SUB},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cb.workers,
+                         "kind": "port",
+                         "sample": f"all {S} sub-grids per step, spawn pool "
+                                   f"of {cb.workers}, CPU {cpu_model()}"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def e2e_leg(wl, step_fn, steps, warmup, world, stream):
+    """Same metric through the public API with HOST buffers: every step
+    copies the ghosted pool host->device (pinned), runs the aggregated
+    iteration, and reads um, up, F back device->host."""
+    import torch
+    host_in = wl.pools[0].cpu().pin_memory()
+    outs = [torch.empty_like(t, device="cpu").pin_memory()
+            for t in (wl.um, wl.up, wl.F)]
+    dev_in = wl.pools[0]
+
+    def step(k):
+        dev_in.copy_(host_in, non_blocking=True)
+        step_fn(0)
+        for h, d in zip(outs, (wl.um, wl.up, wl.F)):
+            h.copy_(d, non_blocking=True)
+    ms = timed(step, steps, warmup, world, stream)
+    torch.cuda.synchronize()
+    return ms, host_in.numel() * 8, sum(o.numel() * 8 for o in outs)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--max-team", type=int, default=128)
+    ap.add_argument("--executors", type=int, default=8)
+    ap.add_argument("--mode", choices=("plan", "realtime", "single"),
+                    default="plan")
+    ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile-only", action="store_true",
+                    help="just warm-up+timed hot-path steps (for ncu)")
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+
+    world, rank, local = dist_setup(args.gpus)
+    if args.impl == "reference":
+        reference_arm(args, world, rank)
+        return
+    import torch
+    from paper_2210_06438_b200 import _lib
+    lib = _lib.load(build_if_missing=False)
+    assert lib.tf_check_device(local) == 0, "not an sm_100 device"
+    peak, peak_src = peaks()
+    stream = torch.cuda.current_stream()
+    wl = Workload()
+    if args.mode == "plan":
+        step, nk, hist, _ = plan_runner(wl, args.max_team, args.executors)
+        launches_per_step = nk
+    elif args.mode == "realtime":
+        step, launches, _ = realtime_runner(wl, args.max_team, args.executors)
+        launches_per_step = None
+        hist = None
+    else:
+        step = single_runner(wl)
+        launches_per_step, hist = 1, {wl.S: 1}
+    if args.profile_only:
+        timed(step, args.steps, args.warmup, world, stream)
+        return
+    # settle clocks under load before the timed region (untimed)
+    with ClockSampler(local) as clk:
+        t_end = time.time() + 0.5
+        k = 0
+        while time.time() < t_end:
+            step(k)
+            k += 1
+        ms = timed(step, args.steps, args.warmup, world, stream)
+    if launches_per_step is None:
+        launches_per_step = launches[-1]
+    total_S = wl.S * world
+    value = rate(total_S, wl.n, ms)
+    bytes_step = wl.S * b_alg(wl.n)
+    achieved = bytes_step / (ms * 1e-3) / 1e9
+    # the kernel timed alone: one launch over all slices (aggregation limit)
+    ms_single = timed(single_runner(wl), args.steps, args.warmup, world,
+                      stream)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": {
+            "workload": "config 2: Sod shock tube, 4096 8^3 FP64 sub-grids "
+                        "per GPU, one aggregated reconstruct+flux iteration "
+                        "per step",
+            "subgrids_per_gpu": wl.S, "subgrid_n": wl.n, "grid": GRID,
+            "max_team": args.max_team, "executors": args.executors,
+            "mode": args.mode, "team_histogram": hist,
+            "parallelism": f"sub-grid partition x{world} (no collective)",
+            "l2": "two input pools alternate; per-step working set "
+                  f"{(bytes_step + wl.S * 8 * 2744) / 1e6:.0f} MB vs 126 MB L2"},
+        "gpu_launches": launches_per_step * args.steps,
+        "roofline": {
+            "bound": "hbm", "achieved": achieved, "peak": peak,
+            "unit": "GB/s", "frac": achieved / peak, "peak_source": peak_src,
+            "traffic": None,
+            "per_subgrid_alg_bytes": b_alg(wl.n),
+            "note": "achieved = algorithmic bytes of the whole step / step "
+                    "time (all launches are the recon+flux kernel)",
+            "kernel_alone": {
+                "ms": ms_single,
+                "achieved": bytes_step / (ms_single * 1e-3) / 1e9,
+                "frac": bytes_step / (ms_single * 1e-3) / 1e9 / peak}},
+        "clocks": clk.summary(),
+    }
+    e_ms, bi, bo = e2e_leg(wl, step, max(5, args.steps // 5), 3, world,
+                           stream)
+    line["e2e"] = {"value": rate(total_S, wl.n, e_ms), "unit": UNIT,
+                   "h2d_bytes_per_step": bi, "d2h_bytes_per_step": bo,
+                   "ms_per_step": e_ms}
+    if not args.no_sweep:
+        line["sweep"] = run_sweep(wl, args, world, stream, peak)
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline_leg(wl.S, wl.n, GRID)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -12,8 +12,9 @@
 //   ghosts      scenario.py:124-142 periodic 26-neighbour fill
 //
 // Data movement (B200): the fused reconstruct+flux kernel stages each
-// slice's (n+4)^3 stencil box — the smallest box covering the 6-point star
-// the stencil reads — from HBM into shared memory with ONE TMA
+// slice's (n+4)^2 x (n+6) stencil box — the smallest TMA-legal box covering
+// the 6-point star the stencil reads (the inner z extent is the
+// full 16-byte-aligned row) — from HBM into shared memory with ONE TMA
 // tensor load (cp.async.bulk.tensor.4d, mbarrier completion), so a gather
 // of strided team members costs nothing extra: the slice's
 // sub-grid id is just the 4th TMA coordinate.  Outputs (um, up, F: 90% of
@@ -34,9 +35,12 @@ template <int N>
 struct Geo {
   static constexpr int C = N + 2;      // face / flux cube edge
   static constexpr int E = N + 6;      // ghosted edge (GHOST = 3)
-  static constexpr int B = N + 4;      // stencil box edge, ext index 1..N+4
+  static constexpr int B = N + 4;      // stencil box x/y edge, ext 1..N+4
+  // TMA needs the box's inner (z) start 16-byte aligned, so the box spans
+  // the full z row (ext 0..E-1) — the same DRAM sectors as z 1..N+4.
+  static constexpr int BZ = E;
   static constexpr int CELLS = C * C * C;
-  static constexpr int BOX = B * B * B;
+  static constexpr int BOX = B * B * BZ;
   static constexpr int EXT3 = E * E * E;
   static constexpr int OWN = N * N * N;
 };
@@ -119,7 +123,7 @@ __global__ void __launch_bounds__(THREADS)
                  double* __restrict__ up, double* __restrict__ F,
                  double* __restrict__ amax, int flux_form) {
   using G = Geo<N>;
-  constexpr int C = G::C, B = G::B, CELLS = G::CELLS;
+  constexpr int C = G::C, B = G::B, BZ = G::BZ, CELLS = G::CELLS;
   extern __shared__ __align__(128) double sbox[];
   __shared__ __align__(8) uint64_t bar;
   __shared__ double red[THREADS / 32];
@@ -129,8 +133,9 @@ __global__ void __launch_bounds__(THREADS)
   if (threadIdx.x == 0) {
     mbar_init(&bar, 1);
     mbar_expect_tx(&bar, G::BOX * (uint32_t)sizeof(double));
-    // box origin = extended index (1,1,1) of sub-grid g; coords innermost first
-    tma_load_box(sbox, &tmap, 1, 1, 1, g, &bar);
+    // box origin = extended index (x,y,z) = (1,1,0) of sub-grid g;
+    // coordinates innermost first
+    tma_load_box(sbox, &tmap, 0, 1, 1, g, &bar);
   }
   __syncthreads();  // barrier initialised before anyone polls it
   mbar_wait(&bar, 0);
@@ -140,7 +145,7 @@ __global__ void __launch_bounds__(THREADS)
   double* __restrict__ up_s = up + slot * 3 * CELLS;
   double* __restrict__ F_s = MODE == 0 ? F + slot * 3 * CELLS : nullptr;
   const double av[3] = {ax, ay, az};
-  const int stv[3] = {B * B, B, 1};
+  const int stv[3] = {B * BZ, BZ, 1};
   double speed = 0.0;
 
   for (int c = threadIdx.x; c < CELLS; c += THREADS) {
@@ -148,7 +153,8 @@ __global__ void __launch_bounds__(THREADS)
     const int cj = (c / C) % C;
     const int ck = c % C;
     const int cv[3] = {ci, cj, ck};
-    const int b = ((ci + 1) * B + (cj + 1)) * B + (ck + 1);
+    // cube (ci,cj,ck) = ext (ci+2,cj+2,ck+2) = box (ci+1, cj+1, ck+2)
+    const int b = ((ci + 1) * B + (cj + 1)) * BZ + (ck + 2);
     const double base = sbox[b];
 #pragma unroll
     for (int axis = 0; axis < 3; ++axis) {
@@ -348,7 +354,7 @@ int pool_map(const double* pool, int64_t slices, int n, CUtensorMap* out) {
   const cuuint32_t Bx = (cuuint32_t)(n + 4);
   cuuint64_t dims[4] = {E, E, E, (cuuint64_t)slices};
   cuuint64_t strides[3] = {E * 8, E * E * 8, E * E * E * 8};
-  cuuint32_t box[4] = {Bx, Bx, Bx, 1};
+  cuuint32_t box[4] = {(cuuint32_t)E, Bx, Bx, 1};
   cuuint32_t estr[4] = {1, 1, 1, 1};
   CUtensorMap m;
   CUresult r = fn(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4,

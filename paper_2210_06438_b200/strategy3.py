@@ -1,0 +1,243 @@
+"""Strategy-3 work aggregation on real CUDA streams — the bulk (throughput)
+interface to the C++ formation core and the batched sm_100a kernels.
+
+Three ways to run one iteration of the aggregated reconstruct+flux region
+over a set of sub-grid task arrivals:
+
+* `RealtimeExecutor.run` — the reference's demand-driven policy
+  (aggregator.py:284-345) in real time: an arrival finding its parent's
+  stream idle runs alone; otherwise it joins the forming team, which closes
+  at `max_team` or when the stream drains (observed with cudaEventQuery).
+  One kernel launch per closed team, team ids inside the launch parameters.
+* `form_teams` + `TeamPlan` — the teams a saturated device forms (every
+  busy query answers "busy", so teams close at the cap; the arrival stream's
+  end closes the rest) captured once into a CUDA graph with one kernel node
+  per team on its parent's executor branch.  An iterative solver re-forms the
+  same teams every iteration, so replaying the graph is the steady state.
+* `recon_flux_all` — the limit of aggregation: one launch over all slices.
+
+Arrival order follows HydroSim.driver (step.py:133-137): sub-grids in
+lexicographic order, parents = max(1, S // max_team) (step.py:61), parent of
+arrival i = i % parents (aggregator.py:298), parent p on executor
+(crc32(region) % E + p) % E (aggregator.py:273-277).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from .errors import ValidationError
+
+_CLOSE = {1: "cap", 2: "solo", 3: "drain"}
+
+
+def default_parents(subgrids: int, max_team: int) -> int:
+    """step.py:61 — one parent per expected team."""
+    return max(1, subgrids // max_team)
+
+
+class FormationCore:
+    """Owns one C++ tf_region (AggregationRegion formation state)."""
+
+    def __init__(self, name: str, max_team: int, parents: int,
+                 executors: int):
+        self.lib = _lib.load()
+        if not 1 <= max_team <= _lib.MAX_TEAM:
+            raise ValidationError(
+                f"max_team must be in 1..{_lib.MAX_TEAM}, got {max_team}")
+        if parents < 1 or executors < 1:
+            raise ValidationError("parents and executors must be >= 1")
+        h = C.c_void_p()
+        _lib.check(self.lib.tf_region_create(name.encode(), max_team, parents,
+                                             executors, C.byref(h)),
+                   "tf_region_create")
+        self.handle = h
+        self.name = name
+        self.max_team = max_team
+        self.parents = parents
+        self.executors = executors
+
+    def parent_executor(self, parent: int) -> int:
+        return self.lib.tf_region_parent_executor(self.handle, parent)
+
+    def enter(self, tag: int, busy) -> _lib.EnterResult:
+        res = _lib.EnterResult()
+        cb = _lib.BUSY_FN(lambda ctx, e: int(bool(busy(e))))
+        _lib.check(self.lib.tf_region_enter(self.handle, int(tag), cb, None,
+                                            C.byref(res)), "tf_region_enter")
+        return res
+
+    def stream_idle(self, executor: int) -> list[int]:
+        buf = (C.c_int64 * 8192)()
+        n = self.lib.tf_region_stream_idle(self.handle, executor, buf, 8192)
+        if n < 0:
+            _lib.check(-n, "tf_region_stream_idle")
+        return list(buf[:n])
+
+    def members(self, team: int) -> list[int]:
+        size = self.lib.tf_region_team_size(self.handle, team)
+        buf = (C.c_int64 * max(size, 1))()
+        self.lib.tf_region_team_members(self.handle, team, buf, size)
+        return list(buf[:size])
+
+    def team_parent(self, team: int) -> int:
+        return self.lib.tf_region_team_parent(self.handle, team)
+
+    def release(self, team: int) -> None:
+        _lib.check(self.lib.tf_region_release_team(self.handle, team),
+                   "tf_region_release_team")
+
+    def stats(self) -> dict:
+        tf, solo = C.c_int64(), C.c_int64()
+        hist = (C.c_int64 * 129)()
+        self.lib.tf_region_stats(self.handle, C.byref(tf), C.byref(solo), hist)
+        return {"teams_formed": tf.value, "solo_fast_path": solo.value,
+                "size_histogram": {k: hist[k] for k in range(129) if hist[k]}}
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h:
+            self.lib.tf_region_destroy(h)
+            self.handle = None
+
+
+@dataclass
+class Team:
+    executor: int
+    parent: int
+    ids: list
+    reason: str
+
+
+def form_teams(arrivals, max_team: int, executors: int = 1,
+               parents: int | None = None, name: str = "reconstruct",
+               busy=lambda executor: True) -> list[Team]:
+    """Run the formation core over an arrival sequence and return the closed
+    teams in closure order.  `busy(executor)` answers the starvation query;
+    the default models a saturated device.  Teams still forming when the
+    arrivals end close as their streams drain (in executor order)."""
+    arrivals = [int(a) for a in arrivals]
+    if parents is None:
+        parents = default_parents(len(arrivals), max_team)
+    core = FormationCore(name, max_team, parents, executors)
+    teams = []
+
+    def take(team_id, reason):
+        teams.append(Team(core.parent_executor(core.team_parent(team_id)),
+                          core.team_parent(team_id), core.members(team_id),
+                          reason))
+        core.release(team_id)
+
+    for tag in arrivals:
+        res = core.enter(tag, busy)
+        if res.closed:
+            take(res.team, _CLOSE[res.closed])
+    for e in range(executors):
+        for team_id in core.stream_idle(e):
+            take(team_id, "drain")
+    return teams
+
+
+class TeamPlan:
+    """One iteration's teams captured as a CUDA graph (tf_plan)."""
+
+    def __init__(self, teams, pool, n, velocity, um, up, F, executors,
+                 amax=None, flux_form=0):
+        self.lib = _lib.load()
+        ids = np.concatenate([np.asarray(t.ids, dtype=np.int32)
+                              for t in teams]) if teams else \
+            np.zeros(0, np.int32)
+        offs = np.zeros(len(teams) + 1, dtype=np.int64)
+        offs[1:] = np.cumsum([len(t.ids) for t in teams])
+        exe = np.asarray([t.executor for t in teams], dtype=np.int32)
+        self._keep = (ids, offs, exe, pool, um, up, F, amax)
+        S = pool.shape[0]
+        if ids.size and (ids.min() < 0 or ids.max() >= S):
+            raise ValidationError("team id outside the pool")
+        for t, nm in ((um, "um"), (up, "up"), (F, "F")):
+            if t.shape[0] < S:
+                raise ValidationError(f"{nm} must hold one slot per sub-grid")
+        ax, ay, az = (float(v) for v in velocity)
+        h = C.c_void_p()
+        rc = self.lib.tf_plan_capture_recon_flux(
+            ids.ctypes.data_as(C.POINTER(C.c_int32)),
+            offs.ctypes.data_as(C.POINTER(C.c_int64)),
+            exe.ctypes.data_as(C.POINTER(C.c_int32)), len(teams), executors,
+            pool.data_ptr(), S, n, ax, ay, az, um.data_ptr(), up.data_ptr(),
+            F.data_ptr(), None if amax is None else amax.data_ptr(),
+            int(flux_form), C.byref(h))
+        _lib.check(rc, "tf_plan_capture_recon_flux")
+        self.handle = h
+        self.kernels = self.lib.tf_plan_kernels(h)
+        self.slices = int(ids.size)
+
+    def launch(self, stream=None) -> None:
+        s = stream if stream is not None else torch.cuda.current_stream()
+        _lib.check(self.lib.tf_plan_launch(self.handle, s.cuda_stream),
+                   "tf_plan_launch")
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h:
+            self.lib.tf_plan_destroy(h)
+            self.handle = None
+
+
+class RealtimeExecutor:
+    """tf_executor: real-time strategy-3 formation over `executors` streams."""
+
+    def __init__(self, name: str, max_team: int, executors: int,
+                 parents: int):
+        self.core = FormationCore(name, max_team, parents, executors)
+        self.lib = self.core.lib
+        h = C.c_void_p()
+        _lib.check(self.lib.tf_executor_create(self.core.handle, executors,
+                                               C.byref(h)),
+                   "tf_executor_create")
+        self.handle = h
+        self.executors = executors
+
+    def run(self, pool, n, velocity, ids, um, up, F, amax=None,
+            flux_form=0, join_stream=None) -> int:
+        """Submit the arrivals; returns the number of team launches.  The
+        current torch stream (or join_stream) is made to wait for them."""
+        arr = np.ascontiguousarray(np.asarray(ids, dtype=np.int32))
+        S = pool.shape[0]
+        if arr.size and (arr.min() < 0 or arr.max() >= S):
+            raise ValidationError("arrival id outside the pool")
+        launches = C.c_int64()
+        ax, ay, az = (float(v) for v in velocity)
+        rc = self.lib.tf_executor_run_recon_flux(
+            self.handle, pool.data_ptr(), S,
+            arr.ctypes.data_as(C.POINTER(C.c_int32)), arr.size, n, ax, ay, az,
+            um.data_ptr(), up.data_ptr(), F.data_ptr(),
+            None if amax is None else amax.data_ptr(), int(flux_form),
+            C.byref(launches))
+        _lib.check(rc, "tf_executor_run_recon_flux")
+        s = join_stream if join_stream is not None else \
+            torch.cuda.current_stream()
+        _lib.check(self.lib.tf_executor_join(self.handle, s.cuda_stream),
+                   "tf_executor_join")
+        return launches.value
+
+    def stats(self) -> dict:
+        return self.core.stats()
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h:
+            self.lib.tf_executor_destroy(h)
+            self.handle = None
+
+
+def recon_flux_all(pool, n, velocity, um, up, F, amax=None, flux_form=0,
+                   stream=None) -> None:
+    """Aggregation limit: every slice of the pool in one launch."""
+    from . import ops
+    ops.recon_flux(pool, n, velocity, um, up, F, out_mode=1, amax=amax,
+                   flux_form=flux_form, stream=stream)
