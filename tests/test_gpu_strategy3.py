@@ -1,0 +1,84 @@
+"""Strategy-3 bulk paths on the GPU: the formed team plan (CUDA graph) and
+the real-time executor must give results independent of team composition —
+bit-identical to the oracle (test_hydro.py:195-199 'profile choice does not
+change results') — and every arrival must land in exactly one team."""
+
+import numpy as np
+import pytest
+
+from oracle import hydro_oracle as HO
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def cfg2(cuda):
+    import torch
+    n, grid = 8, 128
+    f = HO.sod_field(grid)
+    hp = HO.make_pool(f, n)
+    HO.exchange_ghosts_pool(hp, n, grid // n)
+    vel = (1.0, 1.0, 1.0)
+    oum, oup, oF = HO.recon_flux_batch(hp, n, vel)
+    pool = torch.from_numpy(hp).to(cuda)
+    return pool, n, vel, oum, oup, oF
+
+
+def _outs(S, n, dev):
+    import torch
+    c = n + 2
+    return [torch.full((S, 3, c, c, c), float("nan"), dtype=torch.float64,
+                       device=dev) for _ in range(3)]
+
+
+def test_form_teams_partitions_arrivals():
+    from paper_2210_06438_b200.strategy3 import form_teams
+    for A in (1, 4, 16, 64, 128):
+        teams = form_teams(range(4096), A, executors=8)
+        ids = sorted(i for t in teams for i in t.ids)
+        assert ids == list(range(4096))
+        assert all(1 <= len(t.ids) <= A for t in teams)
+        # saturated device: every team closes at the cap, strided members
+        assert all(len(t.ids) == A for t in teams)
+        P = max(1, 4096 // A)
+        assert all(np.all(np.diff(t.ids) == P) for t in teams if len(t.ids) > 1)
+
+
+@pytest.mark.parametrize("A,E", [(1, 4), (16, 8), (128, 8), (128, 1)])
+def test_team_plan_bit_exact(cuda, cfg2, A, E):
+    import torch
+    from paper_2210_06438_b200.strategy3 import TeamPlan, form_teams
+    pool, n, vel, oum, oup, oF = cfg2
+    S = pool.shape[0]
+    um, up, F = _outs(S, n, cuda)
+    amax = torch.full((S,), float("nan"), dtype=torch.float64, device=cuda)
+    plan = TeamPlan(form_teams(range(S), A, E), pool, n, vel, um, up, F, E,
+                    amax=amax)
+    plan.launch()
+    plan.launch()   # replay is idempotent
+    torch.cuda.synchronize()
+    assert plan.kernels == S // A
+    assert np.array_equal(F.cpu().numpy(), oF)
+    assert np.array_equal(um.cpu().numpy(), oum)
+    assert np.array_equal(up.cpu().numpy(), oup)
+    assert bool((amax == 1.0).all())
+
+
+@pytest.mark.parametrize("A,E", [(1, 1), (16, 4), (128, 8)])
+def test_realtime_executor_bit_exact(cuda, cfg2, A, E):
+    import torch
+    from paper_2210_06438_b200.strategy3 import (RealtimeExecutor,
+                                                 default_parents)
+    pool, n, vel, oum, oup, oF = cfg2
+    S = pool.shape[0]
+    um, up, F = _outs(S, n, cuda)
+    ex = RealtimeExecutor("reconstruct", A, E, default_parents(S, A))
+    order = np.random.default_rng(A).permutation(S)
+    launches = ex.run(pool, n, vel, order, um, up, F)
+    torch.cuda.synchronize()
+    st = ex.stats()
+    assert st["teams_formed"] == launches
+    assert sum(k * v for k, v in st["size_histogram"].items()) == S
+    assert max(st["size_histogram"]) <= A
+    assert np.array_equal(F.cpu().numpy(), oF)
+    assert np.array_equal(um.cpu().numpy(), oum)
