@@ -188,11 +188,12 @@ class Workload:
         torch.cuda.synchronize()
 
 
-def plan_runner(wl, max_team, executors, parents=None):
+def plan_runner(wl, max_team, executors, parents=None, overlap=True):
     from paper_2210_06438_b200.strategy3 import TeamPlan, form_teams
     teams = form_teams(range(wl.S), max_team, executors, parents)
     plans = [TeamPlan(teams, p, wl.n, VELOCITY, wl.um, wl.up, wl.F,
-                      executors, amax=wl.amax) for p in wl.pools]
+                      executors, amax=wl.amax, overlap=overlap)
+             for p in wl.pools]
     hist = {}
     for t in teams:
         hist[len(t.ids)] = hist.get(len(t.ids), 0) + 1
@@ -202,11 +203,12 @@ def plan_runner(wl, max_team, executors, parents=None):
     return step, len(teams), hist, plans
 
 
-def realtime_runner(wl, max_team, executors, parents=None):
+def realtime_runner(wl, max_team, executors, parents=None, overlap=False):
     from paper_2210_06438_b200.strategy3 import (RealtimeExecutor,
                                                  default_parents)
     parents = parents or default_parents(wl.S, max_team)
-    ex = RealtimeExecutor("reconstruct", max_team, executors, parents)
+    ex = RealtimeExecutor("reconstruct", max_team, executors, parents,
+                          overlap=overlap)
     arrivals = list(range(wl.S))
     launches = []
 
@@ -352,10 +354,12 @@ def main():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--max-team", type=int, default=128)
-    ap.add_argument("--executors", type=int, default=8)
+    ap.add_argument("--executors", type=int, default=4)
     ap.add_argument("--mode", choices=("plan", "realtime", "single"),
                     default="plan")
     ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--no-overlap", action="store_true",
+                    help="disable PDL overlap of consecutive team launches")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-only", action="store_true",
                     help="just warm-up+timed hot-path steps (for ncu)")
@@ -374,7 +378,8 @@ def main():
     stream = torch.cuda.current_stream()
     wl = Workload()
     if args.mode == "plan":
-        step, nk, hist, _ = plan_runner(wl, args.max_team, args.executors)
+        step, nk, hist, _ = plan_runner(wl, args.max_team, args.executors,
+                                        overlap=not args.no_overlap)
         launches_per_step = nk
     elif args.mode == "realtime":
         step, launches, _ = realtime_runner(wl, args.max_team, args.executors)

@@ -69,6 +69,21 @@ int tf_recon_flux_team_f64(const double* pool_ext, int64_t pool_slices,
                            int32_t out_mode, double* amax, int32_t flux_form,
                            tf_stream_t stream);
 
+/* Launch flags for tf_recon_flux_team_ex_f64.
+ * TF_LAUNCH_OVERLAP_PREV: programmatic dependent launch — the team kernel may
+ * start while the previous kernel on the stream still runs.  Only valid when
+ * that kernel does not produce this team's inputs (e.g. it is another team
+ * of the same region); the executor and the captured plans use it between
+ * consecutive teams of one executor stream.                                */
+#define TF_LAUNCH_OVERLAP_PREV 1
+int tf_recon_flux_team_ex_f64(const double* pool_ext, int64_t pool_slices,
+                              const int32_t* host_ids, int32_t T, int32_t n,
+                              double ax, double ay, double az,
+                              double* um, double* up, double* F,
+                              int32_t out_mode, double* amax,
+                              int32_t flux_form, int32_t flags,
+                              tf_stream_t stream);
+
 /* reconstruct_body alone (kernels.py:73-81): w = pool_ext[ids[s]].          */
 int tf_reconstruct_f64(const double* pool_ext, int64_t pool_slices,
                        const int32_t* ids, int32_t T, int32_t n,
@@ -165,6 +180,12 @@ int tf_executor_run_recon_flux(tf_executor* ex, const double* pool_ext,
                                double az, double* um, double* up, double* F,
                                double* amax, int32_t flux_form,
                                int64_t* launches);
+/* Every executor stream waits for the work issued so far on `stream` (call
+ * before run when the pool was produced on `stream`).                      */
+int tf_executor_fork(tf_executor* ex, tf_stream_t stream);
+/* TF_LAUNCH_OVERLAP_PREV: consecutive teams on one executor stream overlap
+ * (programmatic dependent launch).                                         */
+int tf_executor_set_flags(tf_executor* ex, int32_t flags);
 /* Make `stream` wait for all work issued so far on every executor stream.  */
 int tf_executor_join(tf_executor* ex, tf_stream_t stream);
 int tf_executor_sync(tf_executor* ex);
@@ -182,7 +203,7 @@ int tf_plan_capture_recon_flux(const int32_t* ids, const int64_t* team_offsets,
                                int64_t pool_slices, int32_t n, double ax,
                                double ay, double az, double* um, double* up,
                                double* F, double* amax, int32_t flux_form,
-                               tf_plan** out);
+                               int32_t flags, tf_plan** out);
 int tf_plan_launch(tf_plan* plan, tf_stream_t stream);
 int64_t tf_plan_kernels(const tf_plan* plan);
 void tf_plan_destroy(tf_plan* plan);

@@ -24,6 +24,7 @@ _pi64 = C.POINTER(C.c_int64)
 TF_E_INVALID = 1001
 TF_E_NO_TMA = 1002
 MAX_TEAM = 128
+TF_LAUNCH_OVERLAP_PREV = 1
 
 
 class EnterResult(C.Structure):
@@ -40,6 +41,9 @@ SIGNATURES = {
     "tf_recon_flux_team_f64": (C.c_int, [_p, _i64, _pi32, _i32, _i32, _f64,
                                          _f64, _f64, _p, _p, _p, _i32, _p,
                                          _i32, _p]),
+    "tf_recon_flux_team_ex_f64": (C.c_int, [_p, _i64, _pi32, _i32, _i32, _f64,
+                                            _f64, _f64, _p, _p, _p, _i32, _p,
+                                            _i32, _i32, _p]),
     "tf_reconstruct_f64": (C.c_int, [_p, _i64, _p, _i32, _i32, _p, _p, _i32,
                                      _p]),
     "tf_flux_f64": (C.c_int, [_p, _i32, _i32, _f64, _f64, _f64, _p, _p, _p,
@@ -67,10 +71,12 @@ SIGNATURES = {
                                              _f64, _f64, _f64, _p, _p, _p, _p,
                                              _i32, _pi64]),
     "tf_executor_join": (C.c_int, [_p, _p]),
+    "tf_executor_fork": (C.c_int, [_p, _p]),
+    "tf_executor_set_flags": (C.c_int, [_p, _i32]),
     "tf_executor_sync": (C.c_int, [_p]),
     "tf_plan_capture_recon_flux": (C.c_int, [_pi32, _pi64, _pi32, _i64, _i32,
                                              _p, _i64, _i32, _f64, _f64, _f64,
-                                             _p, _p, _p, _p, _i32,
+                                             _p, _p, _p, _p, _i32, _i32,
                                              C.POINTER(_p)]),
     "tf_plan_launch": (C.c_int, [_p, _p]),
     "tf_plan_kernels": (_i64, [_p]),

@@ -14,6 +14,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <chrono>
 #include <string>
 #include <unordered_map>
 #include <vector>
@@ -231,14 +232,35 @@ struct tf_executor {
   std::vector<cudaStream_t> streams;
   std::vector<cudaEvent_t> last;
   std::vector<char> recorded;
+  std::vector<char> overlap_ok;  // previous op on the stream is a team kernel
+  cudaEvent_t fork = nullptr;
+  int32_t flags = 0;
+  std::vector<int64_t> busy_until;  // steady-clock ns; see rt_busy
 };
 
 namespace {
 
+int64_t now_ns() {
+  return std::chrono::duration_cast<std::chrono::nanoseconds>(
+             std::chrono::steady_clock::now().time_since_epoch())
+      .count();
+}
+
+// A stream observed busy is not re-queried for kRecheckNs: no kernel
+// finishes faster than that, and cudaEventQuery (~0.3-1 us) would otherwise
+// dominate the arrival loop.
+constexpr int64_t kRecheckNs = 2000;
+
 int rt_busy(void* ctx, int32_t e) {
   tf_executor* ex = static_cast<tf_executor*>(ctx);
   if (!ex->recorded[e]) return 0;
-  return cudaEventQuery(ex->last[e]) == cudaErrorNotReady;
+  const int64_t t = now_ns();
+  if (t < ex->busy_until[e]) return 1;
+  if (cudaEventQuery(ex->last[e]) == cudaErrorNotReady) {
+    ex->busy_until[e] = t + kRecheckNs;
+    return 1;
+  }
+  return 0;
 }
 
 struct ReconArgs {
@@ -260,14 +282,17 @@ int launch_team(tf_executor* ex, int64_t team, const ReconArgs& a,
   const int T = (int)t.tags.size();
   for (int i = 0; i < T; ++i) ids[i] = (int32_t)t.tags[i];
   const int32_t e = r->parents[t.parent].executor;
-  int rc = tf_recon_flux_team_f64(a.pool, a.slices, ids, T, a.n, a.ax, a.ay,
-                                  a.az, a.um, a.up, a.F, /*out_mode=*/1,
-                                  a.amax, a.flux_form,
-                                  (tf_stream_t)ex->streams[e]);
+  const int f = ex->overlap_ok[e] ? (ex->flags & TF_LAUNCH_OVERLAP_PREV) : 0;
+  int rc = tf_recon_flux_team_ex_f64(a.pool, a.slices, ids, T, a.n, a.ax,
+                                     a.ay, a.az, a.um, a.up, a.F,
+                                     /*out_mode=*/1, a.amax, a.flux_form, f,
+                                     (tf_stream_t)ex->streams[e]);
   if (rc) return rc;
+  ex->overlap_ok[e] = 1;
   cudaError_t ce = cudaEventRecord(ex->last[e], ex->streams[e]);
   if (ce != cudaSuccess) return ce;
   ex->recorded[e] = 1;
+  ex->busy_until[e] = now_ns() + kRecheckNs;  // just launched: busy
   r->teams.erase(it);
   *launches += 1;
   return 0;
@@ -299,6 +324,13 @@ int tf_executor_create(tf_region* region, int32_t count, tf_executor** out) {
   ex->streams.resize(count);
   ex->last.resize(count);
   ex->recorded.assign(count, 0);
+  ex->overlap_ok.assign(count, 0);
+  ex->busy_until.assign(count, 0);
+  if (cudaEventCreateWithFlags(&ex->fork, cudaEventDisableTiming) !=
+      cudaSuccess) {
+    delete ex;
+    return TF_E_INVALID;
+  }
   for (int i = 0; i < count; ++i) {
     cudaError_t e = cudaStreamCreateWithFlags(&ex->streams[i], cudaStreamNonBlocking);
     if (e == cudaSuccess)
@@ -316,6 +348,7 @@ void tf_executor_destroy(tf_executor* ex) {
   if (!ex) return;
   for (auto s : ex->streams) cudaStreamDestroy(s);
   for (auto e : ex->last) cudaEventDestroy(e);
+  if (ex->fork) cudaEventDestroy(ex->fork);
   delete ex;
 }
 
@@ -368,6 +401,22 @@ int tf_executor_run_recon_flux(tf_executor* ex, const double* pool_ext,
   return 0;
 }
 
+int tf_executor_set_flags(tf_executor* ex, int32_t flags) {
+  if (!ex) return TF_E_INVALID;
+  ex->flags = flags;
+  return 0;
+}
+
+int tf_executor_fork(tf_executor* ex, tf_stream_t stream) {
+  if (!ex) return TF_E_INVALID;
+  cudaError_t ce = cudaEventRecord(ex->fork, (cudaStream_t)stream);
+  for (size_t e = 0; e < ex->streams.size() && ce == cudaSuccess; ++e) {
+    ce = cudaStreamWaitEvent(ex->streams[e], ex->fork, 0);
+    ex->overlap_ok[e] = 0;  // next team follows a full dependency
+  }
+  return ce;
+}
+
 int tf_executor_join(tf_executor* ex, tf_stream_t stream) {
   if (!ex) return TF_E_INVALID;
   for (size_t e = 0; e < ex->streams.size(); ++e) {
@@ -410,7 +459,7 @@ int tf_plan_capture_recon_flux(const int32_t* ids, const int64_t* team_offsets,
                                int64_t pool_slices, int32_t n, double ax,
                                double ay, double az, double* um, double* up,
                                double* F, double* amax, int32_t flux_form,
-                               tf_plan** out) {
+                               int32_t flags, tf_plan** out) {
   if (!ids || !team_offsets || !team_executor || nteams < 0 || executors < 1 ||
       !out)
     return TF_E_INVALID;
@@ -434,12 +483,18 @@ int tf_plan_capture_recon_flux(const int32_t* ids, const int64_t* team_offsets,
     int crc = cudaEventRecord(ev[executors], origin);
     for (int e = 0; e < executors && !crc; ++e)
       crc = cudaStreamWaitEvent(br[e], ev[executors], 0);
+    // the first team on a branch follows the fork (a full dependency);
+    // later teams on the branch may overlap their predecessor (PDL)
+    std::vector<char> started(executors, 0);
     for (int64_t t = 0; t < nteams && !crc; ++t) {
       const int64_t lo = team_offsets[t];
       const int T = (int)(team_offsets[t + 1] - lo);
-      crc = tf_recon_flux_team_f64(pool_ext, pool_slices, ids + lo, T, n, ax,
-                                   ay, az, um, up, F, 1, amax, flux_form,
-                                   (tf_stream_t)br[team_executor[t]]);
+      const int e = team_executor[t];
+      const int f = started[e] ? (flags & TF_LAUNCH_OVERLAP_PREV) : 0;
+      crc = tf_recon_flux_team_ex_f64(pool_ext, pool_slices, ids + lo, T, n,
+                                      ax, ay, az, um, up, F, 1, amax,
+                                      flux_form, f, (tf_stream_t)br[e]);
+      started[e] = 1;
       plan->kernels += 1;
     }
     for (int e = 0; e < executors && !crc; ++e) {

@@ -128,6 +128,9 @@ __global__ void __launch_bounds__(THREADS)
   __shared__ __align__(8) uint64_t bar;
   __shared__ double red[THREADS / 32];
 
+  // let a programmatically-dependent next team launch as soon as every CTA
+  // of this one is resident (no-op unless the next launch opted in)
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int s = blockIdx.x;
   const int g = DEV_IDS ? (dev_ids ? dev_ids[s] : s) : team.id[s];
   if (threadIdx.x == 0) {
@@ -378,7 +381,7 @@ template <int N, int MODE, bool DEV_IDS>
 int launch_recon(const CUtensorMap& map, const int32_t* dev_ids,
                  const TeamIds& team, int T, int out_mode, double ax, double ay,
                  double az, double* um, double* up, double* F, double* amax,
-                 int flux_form, cudaStream_t st) {
+                 int flux_form, cudaStream_t st, int flags) {
   constexpr int TH = recon_threads<N>();
   constexpr size_t smem = Geo<N>::BOX * sizeof(double);
   auto kern = k_recon_flux<N, TH, MODE, DEV_IDS>;
@@ -389,16 +392,29 @@ int launch_recon(const CUtensorMap& map, const int32_t* dev_ids,
     if (e != cudaSuccess) return e;
     attr_done = true;
   }
-  kern<<<T, TH, smem, st>>>(map, dev_ids, team, out_mode, ax, ay, az, um, up,
-                            F, amax, flux_form);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)T);
+  cfg.blockDim = dim3(TH);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  // TF_LAUNCH_OVERLAP_PREV: programmatic dependent launch — this team may
+  // start while the previous (independent) team kernel on the stream is
+  // still running; the kernel never calls griddepcontrol.wait.
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = (flags & TF_LAUNCH_OVERLAP_PREV) ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, map, dev_ids, team, out_mode, ax, ay,
+                            az, um, up, F, amax, flux_form);
 }
 
 template <int MODE, bool DEV_IDS>
 int dispatch_recon(const double* pool, int64_t slices, const int32_t* dev_ids,
                    const TeamIds& team, int T, int n, int out_mode, double ax,
                    double ay, double az, double* um, double* up, double* F,
-                   double* amax, int flux_form, cudaStream_t st) {
+                   double* amax, int flux_form, cudaStream_t st,
+                   int flags = 0) {
   if (T == 0) return 0;
   CUtensorMap map;
   int rc = pool_map(pool, slices, n, &map);
@@ -406,10 +422,10 @@ int dispatch_recon(const double* pool, int64_t slices, const int32_t* dev_ids,
   if (n == 8)
     return launch_recon<8, MODE, DEV_IDS>(map, dev_ids, team, T, out_mode, ax,
                                           ay, az, um, up, F, amax, flux_form,
-                                          st);
+                                          st, flags);
   return launch_recon<16, MODE, DEV_IDS>(map, dev_ids, team, T, out_mode, ax,
                                          ay, az, um, up, F, amax, flux_form,
-                                         st);
+                                         st, flags);
 }
 
 bool valid_n(int n) { return n == 8 || n == 16; }
@@ -439,6 +455,17 @@ int tf_recon_flux_team_f64(const double* pool_ext, int64_t pool_slices,
                            double* up, double* F, int32_t out_mode,
                            double* amax, int32_t flux_form,
                            tf_stream_t stream) {
+  return tf_recon_flux_team_ex_f64(pool_ext, pool_slices, host_ids, T, n, ax,
+                                   ay, az, um, up, F, out_mode, amax,
+                                   flux_form, 0, stream);
+}
+
+int tf_recon_flux_team_ex_f64(const double* pool_ext, int64_t pool_slices,
+                              const int32_t* host_ids, int32_t T, int32_t n,
+                              double ax, double ay, double az, double* um,
+                              double* up, double* F, int32_t out_mode,
+                              double* amax, int32_t flux_form, int32_t flags,
+                              tf_stream_t stream) {
   if (!valid_n(n) || T < 1 || T > TF_MAX_TEAM || !host_ids || !pool_ext ||
       !um || !up || !F || (flux_form != 0 && flux_form != 1))
     return TF_E_INVALID;
@@ -449,7 +476,7 @@ int tf_recon_flux_team_f64(const double* pool_ext, int64_t pool_slices,
   }
   return dispatch_recon<0, false>(pool_ext, pool_slices, nullptr, team, T, n,
                                   out_mode, ax, ay, az, um, up, F, amax,
-                                  flux_form, (cudaStream_t)stream);
+                                  flux_form, (cudaStream_t)stream, flags);
 }
 
 int tf_reconstruct_f64(const double* pool_ext, int64_t pool_slices,

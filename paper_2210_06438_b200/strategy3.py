@@ -147,7 +147,7 @@ class TeamPlan:
     """One iteration's teams captured as a CUDA graph (tf_plan)."""
 
     def __init__(self, teams, pool, n, velocity, um, up, F, executors,
-                 amax=None, flux_form=0):
+                 amax=None, flux_form=0, overlap=True):
         self.lib = _lib.load()
         ids = np.concatenate([np.asarray(t.ids, dtype=np.int32)
                               for t in teams]) if teams else \
@@ -170,7 +170,8 @@ class TeamPlan:
             exe.ctypes.data_as(C.POINTER(C.c_int32)), len(teams), executors,
             pool.data_ptr(), S, n, ax, ay, az, um.data_ptr(), up.data_ptr(),
             F.data_ptr(), None if amax is None else amax.data_ptr(),
-            int(flux_form), C.byref(h))
+            int(flux_form), _lib.TF_LAUNCH_OVERLAP_PREV if overlap else 0,
+            C.byref(h))
         _lib.check(rc, "tf_plan_capture_recon_flux")
         self.handle = h
         self.kernels = self.lib.tf_plan_kernels(h)
@@ -192,7 +193,7 @@ class RealtimeExecutor:
     """tf_executor: real-time strategy-3 formation over `executors` streams."""
 
     def __init__(self, name: str, max_team: int, executors: int,
-                 parents: int):
+                 parents: int, overlap: bool = False):
         self.core = FormationCore(name, max_team, parents, executors)
         self.lib = self.core.lib
         h = C.c_void_p()
@@ -200,6 +201,9 @@ class RealtimeExecutor:
                                                C.byref(h)),
                    "tf_executor_create")
         self.handle = h
+        _lib.check(self.lib.tf_executor_set_flags(
+            h, _lib.TF_LAUNCH_OVERLAP_PREV if overlap else 0),
+            "tf_executor_set_flags")
         self.executors = executors
 
     def run(self, pool, n, velocity, ids, um, up, F, amax=None,
@@ -212,6 +216,10 @@ class RealtimeExecutor:
             raise ValidationError("arrival id outside the pool")
         launches = C.c_int64()
         ax, ay, az = (float(v) for v in velocity)
+        s = join_stream if join_stream is not None else \
+            torch.cuda.current_stream()
+        _lib.check(self.lib.tf_executor_fork(self.handle, s.cuda_stream),
+                   "tf_executor_fork")
         rc = self.lib.tf_executor_run_recon_flux(
             self.handle, pool.data_ptr(), S,
             arr.ctypes.data_as(C.POINTER(C.c_int32)), arr.size, n, ax, ay, az,
@@ -219,8 +227,6 @@ class RealtimeExecutor:
             None if amax is None else amax.data_ptr(), int(flux_form),
             C.byref(launches))
         _lib.check(rc, "tf_executor_run_recon_flux")
-        s = join_stream if join_stream is not None else \
-            torch.cuda.current_stream()
         _lib.check(self.lib.tf_executor_join(self.handle, s.cuda_stream),
                    "tf_executor_join")
         return launches.value
