@@ -208,6 +208,22 @@ int tf_plan_launch(tf_plan* plan, tf_stream_t stream);
 int64_t tf_plan_kernels(const tf_plan* plan);
 void tf_plan_destroy(tf_plan* plan);
 
+/* ---- multi-GPU slab halo (exchange_ghosts across a partition) ----------- */
+/* The local pool holds an x-slab of mx sub-grid layers of an m^3 periodic
+ * lattice: (mx*m*m, E, E, E), local id = (bx*m + by)*m + bz.  Planes are
+ * (3, m*n, m*n) FP64.  pack: lo = the slab's first 3 owned x layers, hi =
+ * its last 3.  fill: every ghost cell from the local pool or, in x beyond
+ * the slab, from halo_lo (the left neighbour's hi) / halo_hi (the right
+ * neighbour's lo).  One rank: halo_lo = own hi, halo_hi = own lo gives
+ * exactly exchange_ghosts (scenario.py:124-142).  fill covers local ids
+ * [first, first+count) so interior sub-grids can be filled (and computed)
+ * while the halo planes are still in flight.                               */
+int tf_halo_pack_f64(const double* pool_ext, int32_t n, int32_t mx, int32_t m,
+                     double* lo_plane, double* hi_plane, tf_stream_t stream);
+int tf_ghost_fill_slab_f64(double* pool_ext, int32_t n, int32_t mx, int32_t m,
+                           const double* halo_lo, const double* halo_hi,
+                           int32_t first, int32_t count, tf_stream_t stream);
+
 /* ---- misc ----------------------------------------------------------------*/
 const char* tf_version(void);
 /* sm_100a device check: 0 iff device `dev` is compute capability 10.0.    */

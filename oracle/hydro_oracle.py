@@ -338,6 +338,31 @@ def staged_iteration(pool: np.ndarray, n: int, per_axis: int,
     return nxt
 
 
+def slab_pack(pool: np.ndarray, n: int, mx: int, m: int):
+    """exchange_ghosts (scenario.py:124-142) split across an x-slab
+    partition: the slab's 3 lowest / highest owned x layers, (3, G, G)."""
+    own = pool[:, GHOST:GHOST + n, GHOST:GHOST + n, GHOST:GHOST + n]
+    slab = own.reshape(mx, m, m, n, n, n).transpose(0, 3, 1, 4, 2, 5) \
+        .reshape(mx * n, m * n, m * n)
+    return slab[:GHOST].copy(), slab[-GHOST:].copy()
+
+
+def slab_fill(pool: np.ndarray, n: int, mx: int, m: int, halo_lo, halo_hi):
+    """Ghost fill of a slab pool from its own owned cells plus the x halo
+    planes: the periodic window of the global field the slab overlays."""
+    own = pool[:, GHOST:GHOST + n, GHOST:GHOST + n, GHOST:GHOST + n]
+    slab = own.reshape(mx, m, m, n, n, n).transpose(0, 3, 1, 4, 2, 5) \
+        .reshape(mx * n, m * n, m * n)
+    ext = np.concatenate([halo_lo, slab, halo_hi], axis=0)  # x: -3..X+3
+    G = m * n
+    for g in range(mx * m * m):
+        bx, by, bz = g // (m * m), (g // m) % m, g % m
+        xi = np.arange(bx * n - GHOST, bx * n + n + GHOST) + GHOST
+        yi = np.arange(by * n - GHOST, by * n + n + GHOST) % G
+        zi = np.arange(bz * n - GHOST, bz * n + n + GHOST) % G
+        pool[g] = ext[np.ix_(xi, yi, zi)]
+
+
 def digest(a: np.ndarray) -> str:
     """sha256 of the C-contiguous little-endian float64 bytes."""
     import hashlib

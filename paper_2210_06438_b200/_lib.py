@@ -81,6 +81,9 @@ SIGNATURES = {
     "tf_plan_launch": (C.c_int, [_p, _p]),
     "tf_plan_kernels": (_i64, [_p]),
     "tf_plan_destroy": (None, [_p]),
+    "tf_halo_pack_f64": (C.c_int, [_p, _i32, _i32, _i32, _p, _p, _p]),
+    "tf_ghost_fill_slab_f64": (C.c_int, [_p, _i32, _i32, _i32, _p, _p, _i32,
+                                         _i32, _p]),
     "tf_version": (C.c_char_p, []),
     "tf_check_device": (C.c_int, [_i32]),
 }
