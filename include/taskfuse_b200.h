@@ -108,6 +108,13 @@ int tf_update_f64(const double* pool_ext, const int32_t* ids, int32_t T,
 int tf_ghost_fill_f64(double* pool_ext, const int32_t* ids, int32_t T,
                       int32_t n, int32_t per_axis, tf_stream_t stream);
 
+/* make_state / assemble (scenario.py:83-106) on the device: the global
+ * (grid_n^3) field <-> the owned cells of the pool (ghosts untouched).      */
+int tf_field_to_pool_f64(const double* field, int32_t grid_n, int32_t n,
+                         double* pool_ext, tf_stream_t stream);
+int tf_pool_to_field_f64(const double* pool_ext, int32_t grid_n, int32_t n,
+                         double* field, tf_stream_t stream);
+
 /* prep_body (kernels.py:69-70): w[slot] = pool_ext[ids[s]].                */
 int tf_prep_f64(const double* pool_ext, const int32_t* ids, int32_t T,
                 int32_t n, double* w, int32_t out_mode, tf_stream_t stream);

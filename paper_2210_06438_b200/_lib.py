@@ -51,6 +51,8 @@ SIGNATURES = {
     "tf_update_f64": (C.c_int, [_p, _p, _i32, _i32, _p, _i32, _f64, _p, _p]),
     "tf_ghost_fill_f64": (C.c_int, [_p, _p, _i32, _i32, _i32, _p]),
     "tf_prep_f64": (C.c_int, [_p, _p, _i32, _i32, _p, _i32, _p]),
+    "tf_field_to_pool_f64": (C.c_int, [_p, _i32, _i32, _p, _p]),
+    "tf_pool_to_field_f64": (C.c_int, [_p, _i32, _i32, _p, _p]),
     "tf_reduce_f64": (C.c_int, [_p, _i32, _f64, _f64, _f64, _p, _i32, _p]),
     "tf_region_create": (C.c_int, [C.c_char_p, _i32, _i32, _i32,
                                    C.POINTER(_p)]),

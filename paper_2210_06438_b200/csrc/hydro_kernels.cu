@@ -303,6 +303,32 @@ __global__ void __launch_bounds__(256)
   for (int c = threadIdx.x; c < G::EXT3 / 2; c += blockDim.x) dst[c] = src[c];
 }
 
+// make_state / assemble (scenario.py:83-106) on the device: the global
+// (G,G,G) field <-> the owned cells of the (S,E,E,E) pool.  DIR 0: field ->
+// pool (ghosts untouched), DIR 1: pool -> field.  One thread per owned cell,
+// consecutive threads along z in both layouts.
+template <int N, int DIR>
+__global__ void __launch_bounds__(256)
+    k_field_pool(double* __restrict__ field, double* __restrict__ pool,
+                 int per_axis) {
+  using G = Geo<N>;
+  constexpr int E = G::E;
+  const int m = per_axis, Gn = per_axis * N;
+  const int64_t total = (int64_t)Gn * Gn * Gn;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int x = (int)(t / ((int64_t)Gn * Gn));
+    const int y = (int)((t / Gn) % Gn), z = (int)(t % Gn);
+    const int64_t id = ((int64_t)(x / N) * m + y / N) * m + z / N;
+    const int64_t e = id * G::EXT3 +
+                      ((int64_t)(x % N + 3) * E + (y % N + 3)) * E + (z % N + 3);
+    if (DIR == 0)
+      pool[e] = field[t];
+    else
+      field[t] = pool[e];
+  }
+}
+
 __global__ void k_reduce(const int32_t* __restrict__ ids, int T, int out_mode,
                          double v, double* __restrict__ out) {
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
@@ -561,6 +587,41 @@ int tf_reduce_f64(const int32_t* ids, int32_t T, double ax, double ay,
   k_reduce<<<(T + 127) / 128, 128, 0, (cudaStream_t)stream>>>(
       ids, T, out_mode, v, reduce_out);
   return cudaGetLastError();
+}
+
+static int field_pool(double* field, double* pool, int32_t grid_n, int32_t n,
+                      int dir, tf_stream_t stream) {
+  if (!valid_n(n) || grid_n < n || grid_n % n || !field || !pool)
+    return TF_E_INVALID;
+  const int m = grid_n / n;
+  const int64_t total = (int64_t)grid_n * grid_n * grid_n;
+  const int blocks =
+      (int)((total + 255) / 256 < 148 * 32 ? (total + 255) / 256 : 148 * 32);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (n == 8) {
+    if (dir == 0)
+      k_field_pool<8, 0><<<blocks, 256, 0, st>>>(field, pool, m);
+    else
+      k_field_pool<8, 1><<<blocks, 256, 0, st>>>(field, pool, m);
+  } else {
+    if (dir == 0)
+      k_field_pool<16, 0><<<blocks, 256, 0, st>>>(field, pool, m);
+    else
+      k_field_pool<16, 1><<<blocks, 256, 0, st>>>(field, pool, m);
+  }
+  return cudaGetLastError();
+}
+
+int tf_field_to_pool_f64(const double* field, int32_t grid_n, int32_t n,
+                         double* pool_ext, tf_stream_t stream) {
+  return field_pool(const_cast<double*>(field), pool_ext, grid_n, n, 0,
+                    stream);
+}
+
+int tf_pool_to_field_f64(const double* pool_ext, int32_t grid_n, int32_t n,
+                         double* field, tf_stream_t stream) {
+  return field_pool(field, const_cast<double*>(pool_ext), grid_n, n, 1,
+                    stream);
 }
 
 const char* tf_version(void) { return "taskfuse_b200 0.1 sm_100a"; }

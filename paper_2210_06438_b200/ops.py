@@ -183,6 +183,34 @@ def ghost_fill(pool, n, per_axis, ids=None, stream=None) -> None:
     _lib.check(rc, "tf_ghost_fill_f64")
 
 
+def field_to_pool(field, n, pool, stream=None) -> None:
+    """make_state's owned-cell scatter (scenario.py:83-96) on the device."""
+    lib = _lib.load()
+    _check_n(n)
+    _need_cuda_f64(field, "field")
+    g = field.shape[0]
+    if field.dim() != 3 or g % n or pool.shape[0] != (g // n) ** 3:
+        raise ValidationError("field/pool shapes do not match")
+    _check_pool(pool, n)
+    _lib.check(lib.tf_field_to_pool_f64(field.data_ptr(), g, n,
+                                        pool.data_ptr(), _stream(stream)),
+               "tf_field_to_pool_f64")
+
+
+def pool_to_field(pool, n, field, stream=None) -> None:
+    """assemble (scenario.py:99-106) on the device."""
+    lib = _lib.load()
+    _check_n(n)
+    _need_cuda_f64(field, "field")
+    g = field.shape[0]
+    if field.dim() != 3 or g % n or pool.shape[0] != (g // n) ** 3:
+        raise ValidationError("field/pool shapes do not match")
+    _check_pool(pool, n)
+    _lib.check(lib.tf_pool_to_field_f64(pool.data_ptr(), g, n,
+                                        field.data_ptr(), _stream(stream)),
+               "tf_pool_to_field_f64")
+
+
 def prep(pool, n, w, ids=None, T=None, out_mode=1, stream=None) -> None:
     """prep_body batched: w[slot] = pool[id]."""
     lib = _lib.load()

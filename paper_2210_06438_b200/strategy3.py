@@ -241,6 +241,79 @@ class RealtimeExecutor:
             self.handle = None
 
 
+class AggregatedIteration:
+    """One device-resident hydro iteration with strategy-3 team launches:
+    ghost fill -> reconstruct+flux (captured team plan) -> update -> swap.
+
+    `run_host(field_in, field_out)` is the end-to-end call with HOST
+    buffers: the global field (grid^3, the reference's `assemble` layout)
+    goes host->device, one iteration runs, the updated field comes back —
+    exactly what `reference_step(u, iterations=1)` computes on the CPU
+    (reference.py:42-48), bit for bit.
+    """
+
+    def __init__(self, grid_n: int, n: int, velocity=(1.0, 1.0, 1.0),
+                 max_team: int = 128, executors: int = 4, device=None,
+                 overlap: bool = True):
+        from . import ops
+        from .hydro.scenario import dt_over_dx
+        self.ops = ops
+        dev = torch.device(device) if device is not None else \
+            torch.device("cuda", torch.cuda.current_device())
+        self.n, self.grid_n = n, grid_n
+        self.m = grid_n // n
+        S = self.m ** 3
+        self.S = S
+        self.velocity = tuple(float(v) for v in velocity)
+        self.dt_dx = dt_over_dx(velocity)
+        e, c = n + 6, n + 2
+        f64 = dict(dtype=torch.float64, device=dev)
+        self.pools = [torch.full((S, e, e, e), float("nan"), **f64)
+                      for _ in range(2)]
+        self.um = torch.empty((S, 3, c, c, c), **f64)
+        self.up = torch.empty_like(self.um)
+        self.F = torch.empty_like(self.um)
+        self.field_dev = torch.empty((grid_n,) * 3, **f64)
+        self.teams = form_teams(range(S), max_team, executors)
+        # one captured plan per pool (the pools swap every iteration)
+        self.plans = [TeamPlan(self.teams, p, n, self.velocity, self.um,
+                               self.up, self.F, executors, overlap=overlap)
+                      for p in self.pools]
+        self.cur = 0
+
+    @property
+    def pool(self):
+        return self.pools[self.cur]
+
+    def load(self, field_dev) -> None:
+        self.ops.field_to_pool(field_dev, self.n, self.pool)
+
+    def step(self) -> None:
+        """One iteration on the device-resident current pool."""
+        ops, n = self.ops, self.n
+        cur, nxt = self.pools[self.cur], self.pools[1 - self.cur]
+        ops.ghost_fill(cur, n, self.m)
+        self.plans[self.cur].launch()
+        ops.update(cur, n, self.F, self.dt_dx, nxt)
+        self.cur = 1 - self.cur
+
+    def store(self, field_dev) -> None:
+        self.ops.pool_to_field(self.pool, self.n, field_dev)
+
+    def run_host(self, field_in, field_out, iterations: int = 1) -> None:
+        """Host (pinned) field in -> `iterations` iterations -> host out."""
+        self.field_dev.copy_(field_in, non_blocking=True)
+        self.load(self.field_dev)
+        for _ in range(iterations):
+            self.step()
+        self.store(self.field_dev)
+        field_out.copy_(self.field_dev, non_blocking=True)
+
+    @property
+    def launches_per_step(self) -> int:
+        return 2 + len(self.teams)
+
+
 def recon_flux_all(pool, n, velocity, um, up, F, amax=None, flux_form=0,
                    stream=None) -> None:
     """Aggregation limit: every slice of the pool in one launch."""

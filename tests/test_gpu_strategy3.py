@@ -64,6 +64,41 @@ def test_team_plan_bit_exact(cuda, cfg2, A, E):
     assert bool((amax == 1.0).all())
 
 
+@pytest.mark.parametrize("grid,n,vel", [(32, 8, (1.0, 1.0, 1.0)),
+                                        (64, 8, (-1.0, 0.5, -0.25)),
+                                        (64, 16, (0.7, -1.3, 0.0))])
+def test_aggregated_iteration_host_roundtrip(cuda, grid, n, vel):
+    """run_host: host field in -> one device iteration -> host field out ==
+    reference_step(u, iterations=1); three chained == one reference step."""
+    import torch
+    from paper_2210_06438_b200.strategy3 import AggregatedIteration
+    f = HO.stress_field(grid)
+    it = AggregatedIteration(grid, n, vel, max_team=16, executors=2)
+    host_in = torch.from_numpy(f).pin_memory()
+    host_out = torch.empty_like(host_in).pin_memory()
+    it.run_host(host_in, host_out)
+    torch.cuda.synchronize()
+    assert np.array_equal(host_out.numpy(), HO.advect_once(f, vel))
+    it.run_host(host_in, host_out, iterations=3)
+    torch.cuda.synchronize()
+    assert np.array_equal(host_out.numpy(), HO.reference_step(f, vel))
+
+
+def test_field_pool_kernels_roundtrip(cuda):
+    import torch
+    from paper_2210_06438_b200 import ops
+    f = HO.initial_field(32)
+    field = torch.from_numpy(f).to(cuda)
+    pool = torch.full((64, 14, 14, 14), float("nan"), dtype=torch.float64,
+                      device=cuda)
+    ops.field_to_pool(field, 8, pool)
+    assert np.array_equal(pool.cpu().numpy(), HO.make_pool(f, 8),
+                          equal_nan=True)
+    out = torch.empty_like(field)
+    ops.pool_to_field(pool, 8, out)
+    assert torch.equal(out, field)
+
+
 @pytest.mark.parametrize("A,E", [(1, 1), (16, 4), (128, 8)])
 def test_realtime_executor_bit_exact(cuda, cfg2, A, E):
     import torch
