@@ -370,6 +370,51 @@ def e2e_faces_leg(wl, step_fn, steps, warmup, world, stream):
     return ms, host_in.numel() * 8, sum(o.numel() * 8 for o in outs)
 
 
+def cfg5_leg(args, world, rank, local, peak):
+    """BASELINE config 5: 262 144 8^3 sub-grids (grid 512^3, blast field)
+    slab-partitioned over the ranks (strong scaling: fixed total).  One step
+    = one full device iteration per rank: pack halo planes, ring exchange
+    (NCCL P2P), ghost fill (interior layers overlapped with the exchange),
+    aggregated reconstruct+flux, update."""
+    import numpy as np
+    import torch
+    from paper_2210_06438_b200.hydro import initial_field
+    from paper_2210_06438_b200.parallel_halo import SlabHydro, SlabPartition
+    grid, n = args.cfg5_grid, N_SUB
+    part = SlabPartition(grid, n, world, rank)
+    a = part.x0 * n
+    x = (np.arange(grid) + 0.5) / grid
+    # the slab of initial_field (scenario.py:30-37), evaluated per slab
+    xs = x[a:a + part.mx * n]
+    r2 = ((xs - 0.5) ** 2)[:, None, None] + ((x - 0.5) ** 2)[None, :, None] \
+        + ((x - 0.5) ** 2)[None, None, :]
+    slab = 1.0 + 1.0 * np.exp(-r2 / (2.0 * 0.1 ** 2))
+    sim = SlabHydro(part, slab, VELOCITY, device=torch.device("cuda", local))
+    del slab
+    stream = torch.cuda.current_stream()
+    ms = timed(lambda k: sim.iteration(overlap=True), args.steps,
+               args.warmup, world, stream)
+    S_total = (grid // n) ** 3
+    value = rate(S_total, n, ms)
+    bytes_alg = part.subgrids * b_alg(n)
+    return {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"config 5: blast wave, {S_total} 8^3 "
+                   f"sub-grids (grid {grid}^3) slab-partitioned over "
+                   f"{world} GPU(s); one full iteration per step (halo "
+                   "exchange, ghost fill, recon+flux, update)",
+                   "subgrids_per_gpu": part.subgrids,
+                   "halo_bytes_per_rank_per_step": 2 * part.plane_bytes,
+                   "parallelism": f"x-slab partition x{world}, NCCL P2P "
+                                  "ring halo"},
+        "recon_flux_hbm_frac_lower_bound": bytes_alg / (ms * 1e-3) / 1e9
+        / peak,
+    }
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -384,6 +429,8 @@ def main():
     ap.add_argument("--no-overlap", action="store_true",
                     help="disable PDL overlap of consecutive team launches")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--workload", choices=("cfg2", "cfg5"), default="cfg2")
+    ap.add_argument("--cfg5-grid", type=int, default=512)
     ap.add_argument("--profile-only", action="store_true",
                     help="just warm-up+timed hot-path steps (for ncu)")
     args = ap.parse_args()
@@ -399,6 +446,14 @@ def main():
     assert lib.tf_check_device(local) == 0, "not an sm_100 device"
     peak, peak_src = peaks()
     stream = torch.cuda.current_stream()
+    if args.workload == "cfg5":
+        line = cfg5_leg(args, world, rank, local, peak)
+        if rank == 0:
+            print(json.dumps(line), flush=True)
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+        return
     wl = Workload()
     if args.mode == "plan":
         step, nk, hist, _ = plan_runner(wl, args.max_team, args.executors,

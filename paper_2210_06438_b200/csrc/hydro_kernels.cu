@@ -231,14 +231,24 @@ __device__ __forceinline__ void block_max_store(double v, double* red,
 // CTAs/SM; VAR 2 z-pairs, register-unconstrained.
 template <int N, int VAR>
 struct ReconShape {
-  static constexpr bool pair = VAR != 0;
-  static constexpr int min_blocks = VAR == 2 ? (N == 8 ? 4 : 1) : (N == 8 ? 6 : 2);
+  // VAR: 0 scalar/1536, 1 pair/1536, 2 pair/2048, 4 pair/1024, 5 scalar/2048
+  static constexpr bool pair = VAR != 0 && VAR != 5;
+  // resident threads per SM the register budget must allow (2048 -> <= 32
+  // registers/thread, full occupancy; 1536 -> 42; 1024 -> 64)
+  static constexpr int sm_threads =
+      (VAR == 2 || VAR == 5) ? 2048 : (VAR == 4 ? 1024 : 1536);
 };
+template <int THREADS, int VAR>
+constexpr int recon_min_blocks() {
+  return ReconShape<8, VAR>::sm_threads / THREADS > 0
+             ? ReconShape<8, VAR>::sm_threads / THREADS
+             : 1;
+}
 
 // Fused reconstruct + flux.  MODE 0: um, up and F; MODE 1: um, up only
 // (reconstruct_body alone).  One CTA per aggregated slice.
 template <int N, int THREADS, int MODE, bool DEV_IDS, int VAR = 0>
-__global__ void __launch_bounds__(THREADS, ReconShape<N, VAR>::min_blocks)
+__global__ void __launch_bounds__(THREADS, recon_min_blocks<THREADS, VAR>())
     k_recon_flux(const __grid_constant__ CUtensorMap tmap,
                  const int32_t* __restrict__ dev_ids,
                  const __grid_constant__ TeamIds team, int out_mode, double ax,
@@ -274,13 +284,105 @@ __global__ void __launch_bounds__(THREADS, ReconShape<N, VAR>::min_blocks)
   if (MODE == 0 && amax != nullptr) block_max_store<THREADS>(speed, red, amax + slot);
 }
 
+__device__ __forceinline__ void bulk_store(void* gdst, const void* ssrc,
+                                           uint32_t bytes) {
+  asm volatile(
+      "cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(
+          reinterpret_cast<uint64_t>(gdst)),
+      "r"(smem_u32(ssrc)), "r"(bytes)
+      : "memory");
+}
+
+// VAR 3 (n = 8, MODE 0): outputs staged in shared memory one axis at a time
+// and written by TMA bulk stores (cp.async.bulk.global.shared::cta, 8000 B
+// per array), double-buffered across axes; the threads never issue a global
+// store.
+template <bool DEV_IDS>
+__global__ void __launch_bounds__(256, 3)
+    k_recon_flux_bulkstore(const __grid_constant__ CUtensorMap tmap,
+                           const int32_t* __restrict__ dev_ids,
+                           const __grid_constant__ TeamIds team, int out_mode,
+                           double ax, double ay, double az,
+                           double* __restrict__ um, double* __restrict__ up,
+                           double* __restrict__ F, double* __restrict__ amax,
+                           int flux_form) {
+  constexpr int N = 8, THREADS = 256;
+  using G = Geo<N>;
+  constexpr int C = G::C, B = G::B, BZ = G::BZ, CELLS = G::CELLS;
+  constexpr int HP = C / 2, PAIRS = C * C * HP;
+  extern __shared__ __align__(128) double smem[];
+  double* sbox = smem;                       // G::BOX doubles
+  double* stage = smem + G::BOX;             // [2][3][CELLS]
+  __shared__ __align__(8) uint64_t bar;
+  __shared__ double red[THREADS / 32];
+
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  const int s = blockIdx.x;
+  const int g = DEV_IDS ? (dev_ids ? dev_ids[s] : s) : team.id[s];
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    mbar_expect_tx(&bar, G::BOX * (uint32_t)sizeof(double));
+    tma_load_box(sbox, &tmap, 0, 1, 1, g, &bar);
+  }
+  __syncthreads();
+  mbar_wait(&bar, 0);
+  const int64_t slot = out_mode ? (int64_t)g : (int64_t)s;
+  double* outs[3] = {um + slot * 3 * CELLS, up + slot * 3 * CELLS,
+                     F + slot * 3 * CELLS};
+  const double av[3] = {ax, ay, az};
+  const int stv[3] = {B * BZ, BZ, 1};
+  double speed = 0.0;
+#pragma unroll 1
+  for (int axis = 0; axis < 3; ++axis) {
+    double* st_buf = stage + (axis & 1) * 3 * CELLS;
+    if (axis == 2) {
+      // buffer 0 is reused: its bulk stores (axis 0) must have read it
+      if (threadIdx.x == 0)
+        asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+      __syncthreads();
+    }
+    const int st = stv[axis];
+    const double a = av[axis];
+    for (int p = threadIdx.x; p < PAIRS; p += THREADS) {
+      const int ci = p / (C * HP);
+      const int cj = (p / HP) % C;
+      const int ck = 2 * (p % HP);
+      const int c = (ci * C + cj) * C + ck;
+      const int b = ((ci + 1) * B + (cj + 1)) * BZ + (ck + 2);
+      const int pos0 = axis == 0 ? ci : (axis == 1 ? cj : ck);
+      const int pos1 = axis == 2 ? ck + 1 : pos0;
+      const Faces r0 = cell_axis(sbox, b, st, pos0, C, a, 0, flux_form);
+      const Faces r1 = cell_axis(sbox, b + 1, st, pos1, C, a, 0, flux_form);
+      *reinterpret_cast<double2*>(st_buf + c) = make_double2(r0.vm, r1.vm);
+      *reinterpret_cast<double2*>(st_buf + CELLS + c) =
+          make_double2(r0.vp, r1.vp);
+      *reinterpret_cast<double2*>(st_buf + 2 * CELLS + c) =
+          make_double2(r0.f, r1.f);
+      speed = fmax(speed, fabs(a));
+    }
+    // make the generic-proxy smem writes visible to the bulk-copy engine
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int k = 0; k < 3; ++k)
+        bulk_store(outs[k] + axis * CELLS, st_buf + k * CELLS,
+                   CELLS * (uint32_t)sizeof(double));
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    }
+  }
+  if (amax != nullptr) block_max_store<THREADS>(speed, red, amax + slot);
+  // shared memory must outlive the bulk stores' reads
+  if (threadIdx.x == 0)
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+
 // Persistent variant for large aggregated launches (T >> #SMs): a grid of
 // resident CTAs walks the slices with a static stride (the host sizes the
 // grid so every CTA gets the same count, +-1) and double-buffers the TMA
 // stencil boxes: slice j+2's load is in flight while slice j is computed
 // and stored.  One block barrier per slice.
 template <int N, int THREADS, int MODE, int VAR>
-__global__ void __launch_bounds__(THREADS, ReconShape<N, VAR>::min_blocks)
+__global__ void __launch_bounds__(THREADS, recon_min_blocks<THREADS, VAR>())
     k_recon_flux_persistent(const __grid_constant__ CUtensorMap tmap,
                             const int32_t* __restrict__ dev_ids, int T,
                             int out_mode, double ax, double ay, double az,
@@ -523,7 +625,9 @@ int pool_map(const double* pool, int64_t slices, int n, CUtensorMap* out) {
 
 template <int N>
 constexpr int recon_threads() {
-  return N == 8 ? 256 : 512;
+  // 512 threads: every z-pair of an 8^3 slice (500) in flight at once;
+  // measured best of 128/256/512 on B200
+  return 512;
 }
 
 template <int N, int MODE, bool DEV_IDS>
@@ -532,12 +636,11 @@ int launch_recon(const CUtensorMap& map, const int32_t* dev_ids,
                  double az, double* um, double* up, double* F, double* amax,
                  int flux_form, cudaStream_t st, int flags);
 
-template <int N, int MODE, bool DEV_IDS, int VAR>
+template <int N, int MODE, bool DEV_IDS, int VAR, int TH = recon_threads<N>()>
 int launch_recon_var(const CUtensorMap& map, const int32_t* dev_ids,
                      const TeamIds& team, int T, int out_mode, double ax,
                      double ay, double az, double* um, double* up, double* F,
                      double* amax, int flux_form, cudaStream_t st, int flags) {
-  constexpr int TH = recon_threads<N>();
   constexpr size_t smem = Geo<N>::BOX * sizeof(double);
   auto kern = k_recon_flux<N, TH, MODE, DEV_IDS, VAR>;
   static bool attr_done = false;  // benign race: idempotent attribute set
@@ -574,6 +677,46 @@ int launch_recon(const CUtensorMap& map, const int32_t* dev_ids,
     const char* v = getenv("TASKFUSE_RECON_VARIANT");
     return v ? atoi(v) : 2;
   }();
+  static const int threads = [] {
+    const char* v = getenv("TASKFUSE_RECON_THREADS");
+    return v ? atoi(v) : 0;
+  }();
+#define TF_RECON_CASE(V, TH_)                                               \
+  if (N == 8 && var == V && threads == TH_)                                 \
+    return launch_recon_var<N, MODE, DEV_IDS, V, TH_>(                      \
+        map, dev_ids, team, T, out_mode, ax, ay, az, um, up, F, amax,       \
+        flux_form, st, flags);
+  TF_RECON_CASE(0, 256)
+  TF_RECON_CASE(2, 256)
+  TF_RECON_CASE(4, 256)
+  TF_RECON_CASE(5, 256)
+  TF_RECON_CASE(4, 512)
+  TF_RECON_CASE(5, 512)
+  TF_RECON_CASE(0, 512)
+#undef TF_RECON_CASE
+  if (var == 3 && N == 8 && MODE == 0) {
+    constexpr size_t smem = (Geo<8>::BOX + 6 * Geo<8>::CELLS) * sizeof(double);
+    auto kern = k_recon_flux_bulkstore<DEV_IDS>;
+    static bool attr_done = false;
+    if (!attr_done) {
+      cudaError_t e = cudaFuncSetAttribute(
+          kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+      attr_done = true;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)T);
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = (flags & TF_LAUNCH_OVERLAP_PREV) ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kern, map, dev_ids, team, out_mode, ax,
+                              ay, az, um, up, F, amax, flux_form);
+  }
   if (var == 1)
     return launch_recon_var<N, MODE, DEV_IDS, 1>(map, dev_ids, team, T,
                                                  out_mode, ax, ay, az, um, up,
