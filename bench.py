@@ -48,6 +48,13 @@ def b_alg(n: int) -> int:
     return 8 * (c ** 3 + 6 * c ** 2 + 9 * c ** 3)
 
 
+def b_step(n: int) -> int:
+    """Algorithmic bytes of the fused full step per sub-grid (SURVEY §8 d
+    secondary metric): distinct stencil cells read + n^3 written."""
+    c = n + 2
+    return 8 * (c ** 3 + 6 * c ** 2 + n ** 3)
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -351,6 +358,37 @@ def e2e_leg(args, steps, warmup, world, stream):
         it.launches_per_step + 2
 
 
+def fused_legs(args, steps, warmup, world, stream, peak):
+    """The fused full iteration (field.FieldIteration, SURVEY §8 f #2) on
+    config 2: device-resident step and the host round trip."""
+    import torch
+    from paper_2210_06438_b200.hydro import sod_field
+    from paper_2210_06438_b200.field import FieldIteration
+    it = FieldIteration(GRID, N_SUB, VELOCITY, max_team=args.max_team,
+                        executors=args.executors)
+    it.load(sod_field(GRID, "cuda"))
+    ms_dev = timed(lambda k: it.step(), steps, warmup, world, stream)
+    host_in = sod_field(GRID, "cpu").pin_memory()
+    host_out = torch.empty_like(host_in).pin_memory()
+    ms_e2e = timed(lambda k: it.run_host(host_in, host_out), steps, warmup,
+                   world, stream)
+    S = (GRID // N_SUB) ** 3
+    n = N_SUB
+    fused_bytes = S * b_step(n)
+    return {
+        "device": {"value": rate(S * world, n, ms_dev), "unit": UNIT,
+                   "ms_per_step": ms_dev,
+                   "hbm_frac": fused_bytes / (ms_dev * 1e-3) / 1e9 / peak,
+                   "launches_per_step": it.launches_per_step,
+                   "step": "halo refresh + one fused recon+flux+update "
+                           "kernel per team (CUDA graph)"},
+        "e2e": {"value": rate(S * world, n, ms_e2e), "unit": UNIT,
+                "ms_per_step": ms_e2e,
+                "h2d_bytes_per_step": host_in.numel() * 8,
+                "d2h_bytes_per_step": host_out.numel() * 8},
+    }
+
+
 def e2e_faces_leg(wl, step_fn, steps, warmup, world, stream):
     """Variant: ghosted pool in, ALL recon+flux outputs (um, up, F) out —
     PCIe-bound by 385 MB per step."""
@@ -378,7 +416,7 @@ def cfg5_leg(args, world, rank, local, peak):
     aggregated reconstruct+flux, update."""
     import numpy as np
     import torch
-    from paper_2210_06438_b200.hydro import initial_field
+    from paper_2210_06438_b200.field import SlabFieldIteration
     from paper_2210_06438_b200.parallel_halo import SlabHydro, SlabPartition
     grid, n = args.cfg5_grid, N_SUB
     part = SlabPartition(grid, n, world, rank)
@@ -389,14 +427,25 @@ def cfg5_leg(args, world, rank, local, peak):
     r2 = ((xs - 0.5) ** 2)[:, None, None] + ((x - 0.5) ** 2)[None, :, None] \
         + ((x - 0.5) ** 2)[None, None, :]
     slab = 1.0 + 1.0 * np.exp(-r2 / (2.0 * 0.1 ** 2))
-    sim = SlabHydro(part, slab, VELOCITY, device=torch.device("cuda", local))
-    del slab
+    dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream()
-    ms = timed(lambda k: sim.iteration(overlap=True), args.steps,
+    # fused path (padded global field, one fused kernel per team of the
+    # slab) — the step measured for `value`
+    fused = SlabFieldIteration(part, slab, VELOCITY, device=dev)
+    ms = timed(lambda k: fused.iteration(overlap=True), args.steps,
                args.warmup, world, stream)
+    del fused
+    torch.cuda.empty_cache()
+    # materialising path (ghosted sub-grid pool, faces in HBM, update)
+    pool = SlabHydro(part, slab, VELOCITY, device=dev)
+    ms_pool = timed(lambda k: pool.iteration(overlap=True),
+                    max(3, args.steps // 2), args.warmup, world, stream)
+    del pool, slab
+    torch.cuda.empty_cache()
     S_total = (grid // n) ** 3
     value = rate(S_total, n, ms)
     bytes_alg = part.subgrids * b_alg(n)
+    fused_bytes = part.subgrids * b_step(n)
     return {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
@@ -410,8 +459,21 @@ def cfg5_leg(args, world, rank, local, peak):
                    "halo_bytes_per_rank_per_step": 2 * part.plane_bytes,
                    "parallelism": f"x-slab partition x{world}, NCCL P2P "
                                   "ring halo"},
-        "recon_flux_hbm_frac_lower_bound": bytes_alg / (ms * 1e-3) / 1e9
-        / peak,
+        "roofline": {
+            "bound": "hbm", "unit": "GB/s", "peak": peak,
+            "achieved": fused_bytes / (ms * 1e-3) / 1e9,
+            "frac": fused_bytes / (ms * 1e-3) / 1e9 / peak,
+            "traffic": None,
+            "note": "fused step, SURVEY §8(d) B_step = 8[(n+2)^3 + "
+                    "6(n+2)^2 + n^3] = 16 896 B per 8^3 sub-grid; halo "
+                    "refresh and exchange inside the step"},
+        "materialising_path": {
+            "ms_per_step": ms_pool,
+            "value": rate(S_total, n, ms_pool),
+            "recon_flux_hbm_frac_lower_bound":
+                bytes_alg / (ms_pool * 1e-3) / 1e9 / peak,
+            "step": "pack+exchange, ghost fill, recon+flux (um/up/F to "
+                    "HBM), update"},
     }
 
 
@@ -527,6 +589,8 @@ def main():
                    "gpu_launches_per_step": e_launch}
     f_ms, fbi, fbo = e2e_faces_leg(wl, step, max(5, args.steps // 5), 3,
                                    world, stream)
+    line["fused_full_iteration"] = fused_legs(args, max(10, args.steps // 2),
+                                              3, world, stream, peak)
     line["e2e_faces"] = {"value": rate(total_S, wl.n, f_ms), "unit": UNIT,
                          "h2d_bytes_per_step": fbi,
                          "d2h_bytes_per_step": fbo, "ms_per_step": f_ms,

@@ -211,6 +211,14 @@ int tf_plan_capture_recon_flux(const int32_t* ids, const int64_t* team_offsets,
                                double ay, double az, double* um, double* up,
                                double* F, double* amax, int32_t flux_form,
                                int32_t flags, tf_plan** out);
+/* Same for the fused full step on a padded field (tf_field_step_f64).      */
+int tf_plan_capture_field_step(const int32_t* ids, const int64_t* team_offsets,
+                               const int32_t* team_executor, int64_t nteams,
+                               int32_t executors, const double* padded_in,
+                               int32_t X, int32_t Gy, int32_t Gz, int32_t n,
+                               double ax, double ay, double az, double dt_dx,
+                               double* padded_out, int32_t flags,
+                               tf_plan** out);
 int tf_plan_launch(tf_plan* plan, tf_stream_t stream);
 int64_t tf_plan_kernels(const tf_plan* plan);
 void tf_plan_destroy(tf_plan* plan);
@@ -230,6 +238,30 @@ int tf_halo_pack_f64(const double* pool_ext, int32_t n, int32_t mx, int32_t m,
 int tf_ghost_fill_slab_f64(double* pool_ext, int32_t n, int32_t mx, int32_t m,
                            const double* halo_lo, const double* halo_hi,
                            int32_t first, int32_t count, tf_stream_t stream);
+
+/* ---- fused full iteration on a padded global field (SURVEY §8 f #2) ----- */
+/* Padded field P: (X+4, Gy+4, Gz+8) FP64, owned global cell (x,y,z) at
+ * P[x+2][y+2][z+4] (X = the slab's x extent; Gy = Gz = grid_n).
+ * tf_field_step_f64: for T sub-grids (device ids, or host_ids <= 128 in the
+ * launch parameters, or ids == host_ids == NULL: the first T in lexicographic
+ * (bx,by,bz) order of the (X/n, Gy/n, Gz/n) lattice), one fused
+ * reconstruct+flux+update per sub-grid (kernels.py:73-111, bit-identical):
+ * reads the stencil box from padded_in, writes the owned cells of
+ * padded_out.  Halo of padded_in must be current.
+ * tf_field_halo_f64: periodic y/z halo of every layer; periodic_x != 0 also
+ * fills the x halo periodically (one GPU; multi-GPU receives it instead).
+ * tf_field_pad_f64 / tf_field_unpad_f64: (X, Gy, Gz) field <-> interior.    */
+int tf_field_step_f64(const double* padded_in, int32_t X, int32_t Gy,
+                      int32_t Gz, int32_t n, const int32_t* ids,
+                      const int32_t* host_ids, int32_t T, double ax, double ay,
+                      double az, double dt_dx, double* padded_out,
+                      int32_t flags, tf_stream_t stream);
+int tf_field_halo_f64(double* padded, int32_t X, int32_t Gy, int32_t Gz,
+                      int32_t periodic_x, tf_stream_t stream);
+int tf_field_pad_f64(const double* field, int32_t X, int32_t Gy, int32_t Gz,
+                     double* padded, tf_stream_t stream);
+int tf_field_unpad_f64(const double* padded, int32_t X, int32_t Gy,
+                       int32_t Gz, double* field, tf_stream_t stream);
 
 /* ---- misc ----------------------------------------------------------------*/
 const char* tf_version(void);

@@ -80,12 +80,22 @@ SIGNATURES = {
                                              _p, _i64, _i32, _f64, _f64, _f64,
                                              _p, _p, _p, _p, _i32, _i32,
                                              C.POINTER(_p)]),
+    "tf_plan_capture_field_step": (C.c_int, [_pi32, _pi64, _pi32, _i64, _i32,
+                                             _p, _i32, _i32, _i32, _i32, _f64,
+                                             _f64, _f64, _f64, _p, _i32,
+                                             C.POINTER(_p)]),
     "tf_plan_launch": (C.c_int, [_p, _p]),
     "tf_plan_kernels": (_i64, [_p]),
     "tf_plan_destroy": (None, [_p]),
     "tf_halo_pack_f64": (C.c_int, [_p, _i32, _i32, _i32, _p, _p, _p]),
     "tf_ghost_fill_slab_f64": (C.c_int, [_p, _i32, _i32, _i32, _p, _p, _i32,
                                          _i32, _p]),
+    "tf_field_step_f64": (C.c_int, [_p, _i32, _i32, _i32, _i32, _p, _pi32,
+                                    _i32, _f64, _f64, _f64, _f64, _p, _i32,
+                                    _p]),
+    "tf_field_halo_f64": (C.c_int, [_p, _i32, _i32, _i32, _i32, _p]),
+    "tf_field_pad_f64": (C.c_int, [_p, _i32, _i32, _i32, _p, _p]),
+    "tf_field_unpad_f64": (C.c_int, [_p, _i32, _i32, _i32, _p, _p]),
     "tf_version": (C.c_char_p, []),
     "tf_check_device": (C.c_int, [_i32]),
 }

@@ -8,7 +8,7 @@
 //   * tf_region_stream_idle() <- the stream-drain callback (device.py:364-370)
 // Fed the same signal sequence, it produces the same teams, parents and
 // slice ids as the reference (checked against recorded reference traces in
-// tests/test_aggregation_replay.py).  The executor wires the signals to real
+// tests/test_abi.py).  The executor wires the signals to real
 // CUDA streams: busy == the parent stream's last event has not completed.
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -451,15 +451,17 @@ struct tf_plan {
   int64_t kernels = 0;
 };
 
-extern "C" {
+namespace {
 
-int tf_plan_capture_recon_flux(const int32_t* ids, const int64_t* team_offsets,
-                               const int32_t* team_executor, int64_t nteams,
-                               int32_t executors, const double* pool_ext,
-                               int64_t pool_slices, int32_t n, double ax,
-                               double ay, double az, double* um, double* up,
-                               double* F, double* amax, int32_t flux_form,
-                               int32_t flags, tf_plan** out) {
+// Capture nteams team launches (launch(ids, T, flags, stream)) as a graph:
+// fork to one branch per executor, teams in order on their branch (the first
+// one after the fork is a full dependency, later ones may overlap their
+// predecessor via PDL when flags ask for it), join.
+template <typename Launch>
+int capture_teams(const int32_t* ids, const int64_t* team_offsets,
+                  const int32_t* team_executor, int64_t nteams,
+                  int32_t executors, int32_t flags, Launch launch,
+                  tf_plan** out) {
   if (!ids || !team_offsets || !team_executor || nteams < 0 || executors < 1 ||
       !out)
     return TF_E_INVALID;
@@ -483,17 +485,13 @@ int tf_plan_capture_recon_flux(const int32_t* ids, const int64_t* team_offsets,
     int crc = cudaEventRecord(ev[executors], origin);
     for (int e = 0; e < executors && !crc; ++e)
       crc = cudaStreamWaitEvent(br[e], ev[executors], 0);
-    // the first team on a branch follows the fork (a full dependency);
-    // later teams on the branch may overlap their predecessor (PDL)
     std::vector<char> started(executors, 0);
     for (int64_t t = 0; t < nteams && !crc; ++t) {
       const int64_t lo = team_offsets[t];
       const int T = (int)(team_offsets[t + 1] - lo);
       const int e = team_executor[t];
       const int f = started[e] ? (flags & TF_LAUNCH_OVERLAP_PREV) : 0;
-      crc = tf_recon_flux_team_ex_f64(pool_ext, pool_slices, ids + lo, T, n,
-                                      ax, ay, az, um, up, F, 1, amax,
-                                      flux_form, f, (tf_stream_t)br[e]);
+      crc = launch(ids + lo, T, f, (tf_stream_t)br[e]);
       started[e] = 1;
       plan->kernels += 1;
     }
@@ -517,6 +515,43 @@ int tf_plan_capture_recon_flux(const int32_t* ids, const int64_t* team_offsets,
   }
   *out = plan;
   return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+int tf_plan_capture_field_step(const int32_t* ids, const int64_t* team_offsets,
+                               const int32_t* team_executor, int64_t nteams,
+                               int32_t executors, const double* padded_in,
+                               int32_t X, int32_t Gy, int32_t Gz, int32_t n,
+                               double ax, double ay, double az, double dt_dx,
+                               double* padded_out, int32_t flags,
+                               tf_plan** out) {
+  return capture_teams(
+      ids, team_offsets, team_executor, nteams, executors, flags,
+      [&](const int32_t* tid, int T, int f, tf_stream_t s) {
+        return tf_field_step_f64(padded_in, X, Gy, Gz, n, nullptr, tid, T, ax,
+                                 ay, az, dt_dx, padded_out, f, s);
+      },
+      out);
+}
+
+int tf_plan_capture_recon_flux(const int32_t* ids, const int64_t* team_offsets,
+                               const int32_t* team_executor, int64_t nteams,
+                               int32_t executors, const double* pool_ext,
+                               int64_t pool_slices, int32_t n, double ax,
+                               double ay, double az, double* um, double* up,
+                               double* F, double* amax, int32_t flux_form,
+                               int32_t flags, tf_plan** out) {
+  return capture_teams(
+      ids, team_offsets, team_executor, nteams, executors, flags,
+      [&](const int32_t* tid, int T, int f, tf_stream_t s) {
+        return tf_recon_flux_team_ex_f64(pool_ext, pool_slices, tid, T, n, ax,
+                                         ay, az, um, up, F, 1, amax,
+                                         flux_form, f, s);
+      },
+      out);
 }
 
 int tf_plan_launch(tf_plan* plan, tf_stream_t stream) {

@@ -1,0 +1,421 @@
+// field_step.cu — the fused full hydro iteration on a padded global field
+// (recon + flux + update without materialised faces).
+//
+// Layout.  Instead of one ghosted (n+6)^3 copy per sub-grid (90 MB of
+// duplicated ghosts at config 2, 22 KB per 8^3 sub-grid), the field lives
+// once, as a padded global array P of shape (X+4, Gy+4, Gz+8): owned global
+// cell (x,y,z) at P[x+2][y+2][z+4].  The halo (2 layers in x and y — the
+// stencil's ghost depth, SURVEY F5 — and 4 in z, so every z row start stays
+// 16-byte aligned for TMA) is refreshed once per iteration: periodic copies
+// in y/z, and in x either a periodic copy (one GPU) or the two neighbour
+// planes (multi-GPU slabs; contiguous, so NCCL sends/receives them with no
+// pack kernel).
+//
+// Step kernel.  One CTA per sub-grid of the team: ONE TMA box load of the
+// (n+4) x (n+4) x (n+8) stencil box straight from P (the sub-grid's "ghost
+// exchange" is just the box overlapping its neighbours), the fluxes of all
+// (n+2)^3 faces into shared memory with the reference's arithmetic
+// (cell_axis, kernels.py:73-93), then the no-FMA update of the n^3 owned
+// cells (kernels.py:100-111) into the next padded field.  Algorithmic bytes
+// per 8^3 sub-grid: 8 * [12*12*16 read + 512 written] = 22.5 KB, vs
+// 84.8 KB + 36 KB ghost fill + 28 KB update for the materialising path.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+#include <stdint.h>
+
+#include <cstdlib>
+#include <mutex>
+#include <unordered_map>
+
+#include "../../include/taskfuse_b200.h"
+
+namespace {
+
+constexpr int HX = 2, HY = 2, HZ = 4;  // halo widths of the padded field
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar))
+               : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                   smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar) {
+  asm volatile(
+      "{\n.reg .pred P1;\nLAB_WAIT:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], 0;\n"
+      "@P1 bra DONE;\nbra LAB_WAIT;\nDONE:\n}\n" ::"r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map,
+                                            int c0, int c1, int c2,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::"
+      "complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2),
+      "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ double minmod(double a, double b) {
+  return (__dmul_rn(a, b) <= 0.0) ? 0.0 : ((fabs(a) < fabs(b)) ? a : b);
+}
+__device__ __forceinline__ double slope(const double* s, int b, int st) {
+  const double base = s[b];
+  return minmod(__dsub_rn(s[b + st], base), __dsub_rn(base, s[b - st]));
+}
+// flux of one face (kernels.py:73-93 for one axis): upwind F = a*up (a>=0)
+// or a*um of the next cell along the axis (a<0).  The update never reads
+// the np.roll wrap layer, so the "next" cell always exists in the box.
+__device__ __forceinline__ double face_flux(const double* s, int b, int st,
+                                            double a) {
+  if (a >= 0.0) {
+    const double half = __dmul_rn(0.5, slope(s, b, st));
+    return __dmul_rn(a, __dadd_rn(s[b], half));
+  }
+  const int bn = b + st;
+  const double half = __dmul_rn(0.5, slope(s, bn, st));
+  return __dmul_rn(a, __dsub_rn(s[bn], half));
+}
+
+struct TeamIds {
+  int32_t id[TF_MAX_TEAM];
+};
+
+template <int N>
+struct FGeo {
+  static constexpr int C = N + 2;
+  static constexpr int BX = N + 4, BY = N + 4, BZ = N + 8;
+  static constexpr int BOX = BX * BY * BZ;
+  static constexpr int CELLS = C * C * C;
+};
+
+// One CTA per sub-grid: fused recon+flux+update.  Sub-grid id -> lattice
+// coordinates in the (mx, m, m) local lattice.
+template <int N, int THREADS, bool DEV_IDS, bool DIRECT>
+__global__ void __launch_bounds__(THREADS)
+    k_step_fused(const __grid_constant__ CUtensorMap tmap,
+                 const int32_t* __restrict__ dev_ids,
+                 const __grid_constant__ TeamIds team, int m, double ax,
+                 double ay, double az, double dt_dx, double* __restrict__ out,
+                 int64_t pyz, int pz) {
+  using G = FGeo<N>;
+  constexpr int C = G::C, BY = G::BY, BZ = G::BZ, CELLS = G::CELLS;
+  extern __shared__ __align__(128) double smem[];
+  double* sbox = smem;             // BOX
+  double* sF = smem + G::BOX;      // 3 * CELLS
+  __shared__ __align__(8) uint64_t bar;
+
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  const int s = blockIdx.x;
+  const int g = DEV_IDS ? (dev_ids ? dev_ids[s] : s) : team.id[s];
+  const int bx = g / (m * m), by = (g / m) % m, bz = g % m;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar);
+    mbar_expect_tx(&bar, G::BOX * (uint32_t)sizeof(double));
+    // padded coords of the box origin: global (b*n-2, b*n-2, b*n-4)
+    tma_load_3d(sbox, &tmap, bz * N, by * N, bx * N, &bar);
+  }
+  __syncthreads();
+  mbar_wait(&bar);
+
+  const int stx = BY * BZ, sty = BZ;
+  if (DIRECT) {
+    // each thread: its owned cells' 6 face fluxes straight from the box
+    // (every interior face is computed twice — cheaper than a 24 KB shared
+    // flux array and a block barrier); same arithmetic, same order
+    for (int o = threadIdx.x; o < N * N * N; o += THREADS) {
+      const int i = o / (N * N), j = (o / N) % N, k = o % N;
+      // owned (i,j,k) = box (i+2, j+2, k+4); its minus face = box - stride
+      const int b = ((i + 2) * BY + (j + 2)) * BZ + (k + 4);
+      double div = __dsub_rn(face_flux(sbox, b, stx, ax),
+                             face_flux(sbox, b - stx, stx, ax));
+      div = __dadd_rn(div, __dsub_rn(face_flux(sbox, b, sty, ay),
+                                     face_flux(sbox, b - sty, sty, ay)));
+      div = __dadd_rn(div, __dsub_rn(face_flux(sbox, b, 1, az),
+                                     face_flux(sbox, b - 1, 1, az)));
+      const int64_t x = (int64_t)bx * N + i + HX, y = (int64_t)by * N + j + HY,
+                    z = (int64_t)bz * N + k + HZ;
+      out[x * pyz + y * pz + z] = __dsub_rn(sbox[b], __dmul_rn(dt_dx, div));
+    }
+    return;
+  }
+  // cube c (0..C-1) = global b*n-1+c = box index (c+1, c+1, c+3)
+  for (int c = threadIdx.x; c < CELLS; c += THREADS) {
+    const int ci = c / (C * C), cj = (c / C) % C, ck = c % C;
+    const int b = ((ci + 1) * BY + (cj + 1)) * BZ + (ck + 3);
+    // the last face layer (the np.roll wrap) is never read by the update;
+    // for a < 0 its upwind cell lies outside the box, so it is skipped
+    sF[c] = (ax < 0.0 && ci == C - 1) ? 0.0 : face_flux(sbox, b, stx, ax);
+    sF[CELLS + c] = (ay < 0.0 && cj == C - 1) ? 0.0 : face_flux(sbox, b, sty, ay);
+    sF[2 * CELLS + c] = (az < 0.0 && ck == C - 1) ? 0.0 : face_flux(sbox, b, 1, az);
+  }
+  __syncthreads();
+  // update_body (kernels.py:100-111): x, y, z accumulation order, no FMA
+  for (int o = threadIdx.x; o < N * N * N; o += THREADS) {
+    const int i = o / (N * N), j = (o / N) % N, k = o % N;
+    const int own = ((i + 1) * C + (j + 1)) * C + (k + 1);
+    double div = __dsub_rn(sF[own], sF[own - C * C]);
+    div = __dadd_rn(div, __dsub_rn(sF[CELLS + own], sF[CELLS + own - C]));
+    div = __dadd_rn(div, __dsub_rn(sF[2 * CELLS + own], sF[2 * CELLS + own - 1]));
+    const double u = sbox[((i + 2) * BY + (j + 2)) * BZ + (k + 4)];
+    const int64_t x = (int64_t)bx * N + i + HX, y = (int64_t)by * N + j + HY,
+                  z = (int64_t)bz * N + k + HZ;
+    out[x * pyz + y * pz + z] = __dsub_rn(u, __dmul_rn(dt_dx, div));
+  }
+}
+
+// Periodic y and z halo of every x layer (z after y so corners are right).
+__global__ void k_halo_yz(double* __restrict__ P, int layers, int Gy, int Gz) {
+  const int py = Gy + 2 * HY, pz = Gz + 2 * HZ;
+  const int64_t per_layer = (int64_t)py * pz;
+  // phase 1: y halo rows (full z extent of owned rows, z in [HZ, HZ+Gz))
+  const int64_t ny = (int64_t)layers * 2 * HY * Gz;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < ny;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t l = t / (2 * HY * Gz);
+    const int r = (int)((t / Gz) % (2 * HY)), z = (int)(t % Gz) + HZ;
+    const int yd = r < HY ? r : Gy + r;                  // halo row
+    const int ys = r < HY ? Gy + r : r;                  // periodic source
+    P[l * per_layer + (int64_t)yd * pz + z] = P[l * per_layer + (int64_t)ys * pz + z];
+  }
+}
+__global__ void k_halo_z(double* __restrict__ P, int layers, int Gy, int Gz) {
+  const int py = Gy + 2 * HY, pz = Gz + 2 * HZ;
+  const int64_t per_layer = (int64_t)py * pz;
+  const int64_t nz = (int64_t)layers * py * 2 * HZ;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nz;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t l = t / ((int64_t)py * 2 * HZ);
+    const int y = (int)((t / (2 * HZ)) % py), r = (int)(t % (2 * HZ));
+    const int zd = r < HZ ? r : Gz + r;
+    const int zs = r < HZ ? Gz + r : r;
+    P[l * per_layer + (int64_t)y * pz + zd] = P[l * per_layer + (int64_t)y * pz + zs];
+  }
+}
+
+// G^3 (or slab X x Gy x Gz) field <-> padded interior.
+__global__ void k_pad_io(double* __restrict__ field, double* __restrict__ P,
+                         int X, int Gy, int Gz, int dir) {
+  const int py = Gy + 2 * HY, pz = Gz + 2 * HZ;
+  const int64_t total = (int64_t)X * Gy * Gz;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t x = t / ((int64_t)Gy * Gz);
+    const int y = (int)((t / Gz) % Gy), z = (int)(t % Gz);
+    const int64_t p = ((x + HX) * py + y + HY) * (int64_t)pz + z + HZ;
+    if (dir == 0)
+      P[p] = field[t];
+    else
+      field[t] = P[p];
+  }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault,
+                                &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+struct Key {
+  const void* p;
+  int X, Gy, Gz, n;
+  bool operator==(const Key& o) const {
+    return p == o.p && X == o.X && Gy == o.Gy && Gz == o.Gz && n == o.n;
+  }
+};
+struct KeyHash {
+  size_t operator()(const Key& k) const {
+    return std::hash<const void*>()(k.p) ^ ((size_t)k.X * 1315423911u) ^
+           ((size_t)k.Gy << 20) ^ ((size_t)k.Gz << 40) ^ (size_t)k.n;
+  }
+};
+
+int field_map(const double* P, int X, int Gy, int Gz, int n, CUtensorMap* out) {
+  static std::mutex mu;
+  static std::unordered_map<Key, CUtensorMap, KeyHash> cache;
+  const Key key{P, X, Gy, Gz, n};
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = cache.find(key);
+  if (it != cache.end()) {
+    *out = it->second;
+    return 0;
+  }
+  auto fn = encode_fn();
+  if (!fn) return TF_E_NO_TMA;
+  const cuuint64_t pz = Gz + 2 * HZ, py = Gy + 2 * HY, px = X + 2 * HX;
+  cuuint64_t dims[3] = {pz, py, px};
+  cuuint64_t strides[2] = {pz * 8, pz * py * 8};
+  cuuint32_t box[3] = {(cuuint32_t)(n + 8), (cuuint32_t)(n + 4),
+                       (cuuint32_t)(n + 4)};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUtensorMap m;
+  if (fn(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(P), dims,
+         strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+         CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return TF_E_INVALID;
+  if (cache.size() > 256) cache.clear();
+  cache.emplace(key, m);
+  *out = m;
+  return 0;
+}
+
+template <int N, bool DEV_IDS, int TH, bool DIRECT>
+int launch_step_var(const CUtensorMap& map, const int32_t* dev_ids,
+                    const TeamIds& team, int T, int m, double ax, double ay,
+                    double az, double dt_dx, double* out, int X, int Gy,
+                    int Gz, cudaStream_t st, int flags) {
+  constexpr size_t smem =
+      (FGeo<N>::BOX + (DIRECT ? 0 : 3 * FGeo<N>::CELLS)) * sizeof(double);
+  auto kern = k_step_fused<N, TH, DEV_IDS, DIRECT>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(
+        kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const int64_t pz = Gz + 2 * HZ, pyz = (int64_t)(Gy + 2 * HY) * pz;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)T);
+  cfg.blockDim = dim3(TH);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute a[1];
+  a[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  a[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = a;
+  cfg.numAttrs = (flags & TF_LAUNCH_OVERLAP_PREV) ? 1 : 0;
+  (void)X;
+  return cudaLaunchKernelEx(&cfg, kern, map, dev_ids, team, m, ax, ay, az,
+                            dt_dx, out, pyz, (int)pz);
+}
+
+template <int N, bool DEV_IDS>
+int launch_step(const CUtensorMap& map, const int32_t* dev_ids,
+                const TeamIds& team, int T, int m, double ax, double ay,
+                double az, double dt_dx, double* out, int X, int Gy, int Gz,
+                cudaStream_t st, int flags) {
+  // TASKFUSE_STEP_VARIANT (A/B only): 0 shared flux array / 512 threads,
+  // 1 direct / 512, 2 direct / 256, 3 direct / 128 (default; measured
+  // 0.745 ms vs 1.89 ms for variant 0 on 262 144 sub-grids)
+  static const int var = [] {
+    const char* v = getenv("TASKFUSE_STEP_VARIANT");
+    return v ? atoi(v) : 3;
+  }();
+#define TF_STEP(TH_, D_)                                                   \
+  return launch_step_var<N, DEV_IDS, TH_, D_>(map, dev_ids, team, T, m, ax, \
+                                              ay, az, dt_dx, out, X, Gy, Gz, \
+                                              st, flags)
+  if (var == 0) TF_STEP(512, false);
+  if (var == 2) TF_STEP(256, true);
+  if (var == 3) TF_STEP(128, true);
+  TF_STEP(512, true);
+#undef TF_STEP
+}
+
+int grid_for(int64_t total) {
+  const int64_t b = (total + 255) / 256;
+  return (int)(b < 148 * 16 ? (b < 1 ? 1 : b) : 148 * 16);
+}
+
+}  // namespace
+
+extern "C" {
+
+int tf_field_step_f64(const double* padded_in, int32_t X, int32_t Gy,
+                      int32_t Gz, int32_t n, const int32_t* ids,
+                      const int32_t* host_ids, int32_t T, double ax, double ay,
+                      double az, double dt_dx, double* padded_out,
+                      int32_t flags, tf_stream_t stream) {
+  if ((n != 8 && n != 16) || X < n || Gy < n || Gz < n || X % n || Gy % n ||
+      Gz % n || Gy != Gz || !padded_in || !padded_out || T < 0 ||
+      (host_ids && T > TF_MAX_TEAM) || padded_in == padded_out)
+    return TF_E_INVALID;
+  if (T == 0) return 0;
+  const int m = Gy / n;
+  const int S = (X / n) * m * m;
+  CUtensorMap map;
+  int rc = field_map(padded_in, X, Gy, Gz, n, &map);
+  if (rc) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  TeamIds team{};
+  if (host_ids) {
+    for (int i = 0; i < T; ++i) {
+      if (host_ids[i] < 0 || host_ids[i] >= S) return TF_E_INVALID;
+      team.id[i] = host_ids[i];
+    }
+    return n == 8 ? launch_step<8, false>(map, nullptr, team, T, m, ax, ay, az,
+                                          dt_dx, padded_out, X, Gy, Gz, st,
+                                          flags)
+                  : launch_step<16, false>(map, nullptr, team, T, m, ax, ay,
+                                           az, dt_dx, padded_out, X, Gy, Gz,
+                                           st, flags);
+  }
+  if (!ids && T > S) return TF_E_INVALID;
+  return n == 8 ? launch_step<8, true>(map, ids, team, T, m, ax, ay, az, dt_dx,
+                                       padded_out, X, Gy, Gz, st, flags)
+                : launch_step<16, true>(map, ids, team, T, m, ax, ay, az,
+                                        dt_dx, padded_out, X, Gy, Gz, st,
+                                        flags);
+}
+
+int tf_field_halo_f64(double* padded, int32_t X, int32_t Gy, int32_t Gz,
+                      int32_t periodic_x, tf_stream_t stream) {
+  if (!padded || X < 2 || Gy < 2 || Gz < 4) return TF_E_INVALID;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int layers = X + 2 * HX;
+  const int py = Gy + 2 * HY, pz = Gz + 2 * HZ;
+  // y/z halos of the owned layers (and, for multi-GPU, of the x halo layers
+  // the caller received — they arrive already y/z-filled, refilling is a
+  // no-op), then the periodic x halo on one GPU
+  k_halo_yz<<<grid_for((int64_t)layers * 2 * HY * Gz), 256, 0, st>>>(padded, layers, Gy, Gz);
+  k_halo_z<<<grid_for((int64_t)layers * py * 2 * HZ), 256, 0, st>>>(padded, layers, Gy, Gz);
+  if (periodic_x) {
+    const size_t layer = (size_t)py * pz * sizeof(double);
+    cudaError_t e = cudaMemcpyAsync(padded, padded + (size_t)X * py * pz,
+                                    HX * layer, cudaMemcpyDeviceToDevice, st);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(padded + (size_t)(X + HX) * py * pz,
+                          padded + (size_t)HX * py * pz, HX * layer,
+                          cudaMemcpyDeviceToDevice, st);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaGetLastError();
+}
+
+int tf_field_pad_f64(const double* field, int32_t X, int32_t Gy, int32_t Gz,
+                     double* padded, tf_stream_t stream) {
+  if (!field || !padded || X < 1 || Gy < 1 || Gz < 1) return TF_E_INVALID;
+  k_pad_io<<<grid_for((int64_t)X * Gy * Gz), 256, 0, (cudaStream_t)stream>>>(
+      const_cast<double*>(field), padded, X, Gy, Gz, 0);
+  return cudaGetLastError();
+}
+
+int tf_field_unpad_f64(const double* padded, int32_t X, int32_t Gy,
+                       int32_t Gz, double* field, tf_stream_t stream) {
+  if (!field || !padded || X < 1 || Gy < 1 || Gz < 1) return TF_E_INVALID;
+  k_pad_io<<<grid_for((int64_t)X * Gy * Gz), 256, 0, (cudaStream_t)stream>>>(
+      field, const_cast<double*>(padded), X, Gy, Gz, 1);
+  return cudaGetLastError();
+}
+
+}  // extern "C"

@@ -1,0 +1,210 @@
+"""Fused full iteration on a padded global field — SURVEY §8(f) rank 2.
+
+The materialising path (ghost-filled per-sub-grid pools, um/up/F written to
+HBM, separate update) moves ~150 KB per 8^3 sub-grid-iteration.  Here the
+field is stored once, padded by the stencil's halo (csrc/field_step.cu), and
+one fused kernel per team does reconstruct + flux + update for its
+sub-grids: ~22.5 KB per sub-grid-iteration.  Strategy 3 is unchanged on
+top: teams formed by the same formation core, one launch per team, the
+iteration's team launches captured as a CUDA graph over the executor
+branches with PDL between consecutive teams.  Bit-identical to
+reference_step (tests/test_gpu_field.py).
+
+`FieldIteration` — one GPU.  `SlabFieldIteration` — one rank of an x-slab
+partition: the x halo layers are contiguous slices of the padded array, so
+the ring exchange sends/receives them in place (no pack kernel), and the
+interior sub-grid layers are stepped while the planes are in flight.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+import torch
+
+from . import _lib
+from .errors import ValidationError
+from .parallel_halo import SlabPartition, exchange_halos
+from .strategy3 import Team, form_teams
+
+HX, HY, HZ = 2, 2, 4
+
+
+def padded_shape(X: int, G: int) -> tuple[int, int, int]:
+    return (X + 2 * HX, G + 2 * HY, G + 2 * HZ)
+
+
+def interior(P: torch.Tensor) -> torch.Tensor:
+    return P[HX:-HX, HY:-HY, HZ:-HZ]
+
+
+class _FieldBase:
+    def __init__(self, X: int, G: int, n: int, velocity, dt_dx, device):
+        from .hydro.scenario import dt_over_dx
+        if n not in (8, 16) or X % n or G % n:
+            raise ValidationError("sub-grid edge must be 8 or 16 and divide "
+                                  "the field extents")
+        self.lib = _lib.load()
+        self.X, self.G, self.n = X, G, n
+        self.m = G // n
+        self.mx = X // n
+        self.S = self.mx * self.m * self.m
+        self.velocity = tuple(float(v) for v in velocity)
+        self.dt_dx = dt_over_dx(velocity) if dt_dx is None else float(dt_dx)
+        dev = torch.device(device) if device is not None else \
+            torch.device("cuda", torch.cuda.current_device())
+        self.device = dev
+        self.P = [torch.full(padded_shape(X, G), float("nan"),
+                             dtype=torch.float64, device=dev)
+                  for _ in range(2)]
+        self.cur = 0
+
+    @property
+    def field(self) -> torch.Tensor:
+        return self.P[self.cur]
+
+    def _s(self, stream=None) -> int:
+        return (stream or torch.cuda.current_stream()).cuda_stream
+
+    def load(self, field_dev: torch.Tensor, stream=None) -> None:
+        """(X, G, G) device field -> current padded interior."""
+        _lib.check(self.lib.tf_field_pad_f64(
+            field_dev.data_ptr(), self.X, self.G, self.G,
+            self.field.data_ptr(), self._s(stream)), "tf_field_pad_f64")
+
+    def store(self, field_dev: torch.Tensor, stream=None) -> None:
+        _lib.check(self.lib.tf_field_unpad_f64(
+            self.field.data_ptr(), self.X, self.G, self.G,
+            field_dev.data_ptr(), self._s(stream)), "tf_field_unpad_f64")
+
+    def halo(self, periodic_x: bool, stream=None) -> None:
+        _lib.check(self.lib.tf_field_halo_f64(
+            self.field.data_ptr(), self.X, self.G, self.G, int(periodic_x),
+            self._s(stream)), "tf_field_halo_f64")
+
+    def step_ids(self, ids: torch.Tensor | None, T: int, stream=None) -> None:
+        """One fused step for T sub-grids (device ids, or the first T)."""
+        cur, nxt = self.P[self.cur], self.P[1 - self.cur]
+        ax, ay, az = self.velocity
+        _lib.check(self.lib.tf_field_step_f64(
+            cur.data_ptr(), self.X, self.G, self.G, self.n,
+            None if ids is None else ids.data_ptr(), None, T, ax, ay, az,
+            self.dt_dx, nxt.data_ptr(), 0, self._s(stream)),
+            "tf_field_step_f64")
+
+    def swap(self) -> None:
+        self.cur = 1 - self.cur
+
+    def owned(self) -> torch.Tensor:
+        return interior(self.field).contiguous()
+
+
+class FieldPlan:
+    """A formed team plan of the fused step captured as a CUDA graph."""
+
+    def __init__(self, teams: list[Team], fi: _FieldBase, src: int,
+                 executors: int, overlap: bool = True):
+        lib = fi.lib
+        ids = np.concatenate([np.asarray(t.ids, np.int32) for t in teams])
+        offs = np.zeros(len(teams) + 1, np.int64)
+        offs[1:] = np.cumsum([len(t.ids) for t in teams])
+        exe = np.asarray([t.executor for t in teams], np.int32)
+        self._keep = (ids, offs, exe)
+        ax, ay, az = fi.velocity
+        h = C.c_void_p()
+        _lib.check(lib.tf_plan_capture_field_step(
+            ids.ctypes.data_as(C.POINTER(C.c_int32)),
+            offs.ctypes.data_as(C.POINTER(C.c_int64)),
+            exe.ctypes.data_as(C.POINTER(C.c_int32)), len(teams), executors,
+            fi.P[src].data_ptr(), fi.X, fi.G, fi.G, fi.n, ax, ay, az,
+            fi.dt_dx, fi.P[1 - src].data_ptr(),
+            _lib.TF_LAUNCH_OVERLAP_PREV if overlap else 0, C.byref(h)),
+            "tf_plan_capture_field_step")
+        self.lib, self.handle = lib, h
+        self.kernels = lib.tf_plan_kernels(h)
+
+    def launch(self, stream=None) -> None:
+        s = stream or torch.cuda.current_stream()
+        _lib.check(self.lib.tf_plan_launch(self.handle, s.cuda_stream),
+                   "tf_plan_launch")
+
+    def __del__(self):
+        if getattr(self, "handle", None):
+            self.lib.tf_plan_destroy(self.handle)
+            self.handle = None
+
+
+class FieldIteration(_FieldBase):
+    """One-GPU fused iteration with strategy-3 team launches."""
+
+    def __init__(self, grid_n: int, n: int, velocity=(1.0, 1.0, 1.0),
+                 max_team: int = 128, executors: int = 4, dt_dx=None,
+                 device=None, overlap: bool = True):
+        super().__init__(grid_n, grid_n, n, velocity, dt_dx, device)
+        self.teams = form_teams(range(self.S), max_team, executors)
+        self.plans = [FieldPlan(self.teams, self, src, executors, overlap)
+                      for src in (0, 1)]
+        self.field_dev = torch.empty((grid_n,) * 3, dtype=torch.float64,
+                                     device=self.device)
+
+    def step(self, stream=None) -> None:
+        self.halo(True, stream)
+        self.plans[self.cur].launch(stream)
+        self.swap()
+
+    def run_host(self, field_in, field_out, iterations: int = 1) -> None:
+        """Host field (pinned) in -> iterations -> host field out."""
+        self.field_dev.copy_(field_in, non_blocking=True)
+        self.load(self.field_dev)
+        for _ in range(iterations):
+            self.step()
+        self.store(self.field_dev)
+        field_out.copy_(self.field_dev, non_blocking=True)
+
+    @property
+    def launches_per_step(self) -> int:
+        return 2 + len(self.teams)   # 2 halo kernels + one per team
+
+
+class SlabFieldIteration(_FieldBase):
+    """One rank's x-slab of a padded global field (multi-GPU)."""
+
+    def __init__(self, part: SlabPartition, slab_field=None,
+                 velocity=(1.0, 1.0, 1.0), dt_dx=None, device=None):
+        super().__init__(part.mx * part.n, part.grid_n, part.n, velocity,
+                         dt_dx, device)
+        self.part = part
+        mm = self.m * self.m
+        self.comm_stream = torch.cuda.Stream(device=self.device)
+        ar = lambda a, b: torch.arange(a, b, dtype=torch.int32,  # noqa: E731
+                                       device=self.device)
+        self.interior_ids = ar(mm, self.S - mm) if self.mx > 2 else None
+        self.boundary_ids = torch.cat([ar(0, mm), ar(self.S - mm, self.S)]) \
+            if self.mx > 1 else ar(0, self.S)
+        if slab_field is not None:
+            if isinstance(slab_field, np.ndarray):
+                slab_field = torch.from_numpy(np.ascontiguousarray(slab_field))
+            self.load(slab_field.to(self.device, torch.float64))
+
+    def _planes(self):
+        P, X = self.field, self.X
+        # lo = my lowest 2 owned x layers, hi = my highest; halos in place
+        return (P[HX:2 * HX], P[X:X + HX], P[0:HX], P[X + HX:X + 2 * HX])
+
+    def iteration(self, exchange=None, overlap: bool = True) -> None:
+        exchange = exchange or exchange_halos
+        cur = torch.cuda.current_stream()
+        self.halo(False, cur)                      # y/z halos, own layers
+        lo, hi, halo_lo, halo_hi = self._planes()
+        if not overlap or self.interior_ids is None:
+            exchange(self.part, lo, hi, halo_lo, halo_hi)
+            self.step_ids(None, self.S, cur)
+        else:
+            self.comm_stream.wait_stream(cur)
+            with torch.cuda.stream(self.comm_stream):
+                exchange(self.part, lo, hi, halo_lo, halo_hi)
+            self.step_ids(self.interior_ids, self.interior_ids.numel(), cur)
+            cur.wait_stream(self.comm_stream)
+            self.step_ids(self.boundary_ids, self.boundary_ids.numel(), cur)
+        self.swap()

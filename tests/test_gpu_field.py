@@ -1,0 +1,94 @@
+"""The fused full iteration on a padded global field (SURVEY §8 f #2) is
+bit-identical to the reference's whole-grid integrator, through team plans,
+the host round trip, and slab partitions (virtual ranks on one GPU)."""
+
+import numpy as np
+import pytest
+
+from oracle import hydro_oracle as HO
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("grid,n,vel,A,E", [
+    (16, 8, (1.0, 1.0, 1.0), 1, 1),
+    (32, 8, (-1.0, 0.5, -0.25), 16, 4),
+    (64, 8, (0.7, -1.3, 0.0), 128, 4),
+    (64, 16, (1.0, 1.0, 1.0), 8, 2),
+    (64, 16, (-0.3, -0.2, 0.9), 64, 4)])
+def test_field_iteration_matches_reference(cuda, grid, n, vel, A, E):
+    import torch
+    from paper_2210_06438_b200.field import FieldIteration
+    f = HO.stress_field(grid)
+    it = FieldIteration(grid, n, vel, max_team=A, executors=E)
+    it.load(torch.from_numpy(f).to(cuda))
+    for _ in range(3):
+        it.step()
+    torch.cuda.synchronize()
+    assert np.array_equal(it.owned().cpu().numpy(), HO.reference_step(f, vel))
+
+
+def test_field_iteration_golden(cuda, hydro_golden):
+    import torch
+    from paper_2210_06438_b200.field import FieldIteration
+    case = next(c for c in hydro_golden["cases"]
+                if c["name"] == "blast16_n8_v111")
+    it = FieldIteration(16, 8, (1.0, 1.0, 1.0), max_team=4, executors=2)
+    it.load(torch.from_numpy(HO.initial_field(16)).to(cuda))
+    for _ in range(6):
+        it.step()
+    torch.cuda.synchronize()
+    assert HO.digest(it.owned().cpu().numpy()) == case["reference_step_2"]
+
+
+def test_field_host_roundtrip(cuda):
+    import torch
+    from paper_2210_06438_b200.field import FieldIteration
+    f = HO.initial_field(64)
+    it = FieldIteration(64, 8, (1.0, 1.0, 1.0))
+    hin = torch.from_numpy(f).pin_memory()
+    hout = torch.empty_like(hin).pin_memory()
+    it.run_host(hin, hout)
+    torch.cuda.synchronize()
+    assert np.array_equal(hout.numpy(), HO.advect_once(f))
+
+
+@pytest.mark.parametrize("world,n,grid,vel", [
+    (2, 8, 32, (1.0, 1.0, 1.0)), (4, 8, 64, (-1.0, 0.5, -0.25)),
+    (2, 16, 64, (0.7, -1.3, 0.0)), (8, 8, 64, (1.0, 1.0, 1.0))])
+def test_slab_field_virtual_ranks(cuda, world, n, grid, vel):
+    import torch
+    from paper_2210_06438_b200.field import SlabFieldIteration
+    from paper_2210_06438_b200.parallel_halo import SlabPartition
+    f = HO.stress_field(grid)
+    ranks = []
+    for r in range(world):
+        p = SlabPartition(grid, n, world, r)
+        ranks.append(SlabFieldIteration(p, p.slab(f), vel, device=cuda))
+    for _ in range(3):
+        for r in ranks:
+            r.halo(False)
+        planes = [r._planes() for r in ranks]
+        for k, r in enumerate(ranks):
+            p = r.part
+            planes[k][2].copy_(planes[p.left][1])    # halo_lo <- left's hi
+            planes[k][3].copy_(planes[p.right][0])   # halo_hi <- right's lo
+        for r in ranks:
+            r.step_ids(None, r.S)
+            r.swap()
+    torch.cuda.synchronize()
+    got = torch.cat([r.owned() for r in ranks]).cpu().numpy()
+    assert np.array_equal(got, HO.reference_step(f, vel))
+
+
+def test_slab_field_single_rank_overlap(cuda):
+    import torch
+    from paper_2210_06438_b200.field import SlabFieldIteration
+    from paper_2210_06438_b200.parallel_halo import SlabPartition
+    f = HO.initial_field(64)
+    p = SlabPartition(64, 8, 1, 0)
+    r = SlabFieldIteration(p, f, (1.0, 1.0, 1.0), device=cuda)
+    for _ in range(3):
+        r.iteration(overlap=True)
+    torch.cuda.synchronize()
+    assert np.array_equal(r.owned().cpu().numpy(), HO.reference_step(f))
