@@ -259,6 +259,23 @@ def run_sweep(wl, args, world, stream, peak):
             "launches_per_iter": launches[-1],
             "mean_team": wl.S * len(launches) / max(1, st["teams_formed"]),
             "solo_fast_path": st["solo_fast_path"]}
+    out["realtime_queue"] = {}
+    from paper_2210_06438_b200.strategy3 import (QueueExecutor,
+                                                 default_parents)
+    arrivals = list(range(wl.S))
+    for A in (1, 4, 16, 64, 128):
+        q = QueueExecutor("reconstruct", A, default_parents(wl.S, A), wl.n)
+        ms = timed(lambda k: q.run(wl.pools[k % len(wl.pools)], VELOCITY,
+                                   arrivals, wl.um, wl.up, wl.F,
+                                   amax=wl.amax), ks, kw, world, stream)
+        st = q.stats()
+        out["realtime_queue"][A] = {
+            "cell_updates_per_s": rate(wl.S, wl.n, ms), "ms_per_iter": ms,
+            "mean_team": st["teams_formed"] and
+            sum(k * v for k, v in st["size_histogram"].items())
+            / st["teams_formed"],
+            "solo_fast_path": st["solo_fast_path"]}
+        del q
     for E in (1, 8, 32, 128):
         # strategy 2: per-task launches (A = 1) spread over E streams
         step, nk, _, _ = plan_runner(wl, 1, E, parents=E)

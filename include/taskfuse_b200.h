@@ -197,6 +197,36 @@ int tf_executor_set_flags(tf_executor* ex, int32_t flags);
 int tf_executor_join(tf_executor* ex, tf_stream_t stream);
 int tf_executor_sync(tf_executor* ex);
 
+/* ---- device-queue executor (strategy 3 without per-team launches) ------- */
+/* A resident consumer grid drains sub-grid ids that the formation core
+ * publishes, one closed team at a time, into a ring in mapped pinned host
+ * memory; busy = published slices not yet completed.  The region must have
+ * exactly one executor (the queue).  run() returns once every arrival has
+ * been published; the consumer runs on `stream` and completes there.
+ * tf_queue_consumer_* are the device side (used by tf_qexec_*).            */
+typedef struct tf_qexec tf_qexec;
+int tf_qexec_create(tf_region* region, int32_t n, tf_qexec** out);
+void tf_qexec_destroy(tf_qexec* q);
+int tf_qexec_run_recon_flux(tf_qexec* q, const double* pool_ext,
+                            int64_t pool_slices, const int32_t* ids,
+                            int64_t count, double ax, double ay, double az,
+                            double* um, double* up, double* F, double* amax,
+                            int32_t flux_form, tf_stream_t stream,
+                            int64_t* teams_published);
+/* slices the consumer has completed so far (host view)                     */
+int64_t tf_qexec_completed(const tf_qexec* q);
+int tf_queue_consumer_ctas(int32_t n);
+/* ring_h/ctl_h: mapped pinned host ring + control block {published,
+ * final_count, completed}; ring_d/qdev: device mirror + {published,
+ * final_count, claim, done} (zeroed, final_count = -1, before launch).      */
+int tf_queue_consumer_launch(const double* pool_ext, int64_t pool_slices,
+                             int32_t n, const int32_t* ring_h, void* ctl_h,
+                             int32_t* ring_d, void* qdev, int32_t ctas,
+                             double ax, double ay, double az, double* um,
+                             double* up, double* F, double* amax,
+                             int32_t flux_form, int64_t timeout_ns,
+                             tf_stream_t stream);
+
 /* ---- captured team plans (CUDA graphs) ----------------------------------- */
 
 typedef struct tf_plan tf_plan;

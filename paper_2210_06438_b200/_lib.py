@@ -96,6 +96,16 @@ SIGNATURES = {
     "tf_field_halo_f64": (C.c_int, [_p, _i32, _i32, _i32, _i32, _p]),
     "tf_field_pad_f64": (C.c_int, [_p, _i32, _i32, _i32, _p, _p]),
     "tf_field_unpad_f64": (C.c_int, [_p, _i32, _i32, _i32, _p, _p]),
+    "tf_qexec_create": (C.c_int, [_p, _i32, C.POINTER(_p)]),
+    "tf_qexec_destroy": (None, [_p]),
+    "tf_qexec_run_recon_flux": (C.c_int, [_p, _p, _i64, _pi32, _i64, _f64,
+                                          _f64, _f64, _p, _p, _p, _p, _i32,
+                                          _p, _pi64]),
+    "tf_qexec_completed": (_i64, [_p]),
+    "tf_queue_consumer_ctas": (C.c_int, [_i32]),
+    "tf_queue_consumer_launch": (C.c_int, [_p, _i64, _i32, _p, _p, _p, _p,
+                                           _i32, _f64, _f64, _f64, _p, _p, _p,
+                                           _p, _i32, _i64, _p]),  # noqa
     "tf_version": (C.c_char_p, []),
     "tf_check_device": (C.c_int, [_i32]),
 }

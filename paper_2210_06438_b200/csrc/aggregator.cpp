@@ -55,6 +55,49 @@ struct Parent {
   int64_t forming = -1;
 };
 
+// Live teams in reusable slots: a team id is its slot index while alive
+// (ids are unique among live teams; a released slot is recycled, keeping
+// its tag vector's capacity, so steady-state formation never allocates).
+class TeamTable {
+ public:
+  int64_t create(int32_t parent) {
+    int64_t id;
+    if (!free_.empty()) {
+      id = free_.back();
+      free_.pop_back();
+    } else {
+      id = (int64_t)slots_.size();
+      slots_.emplace_back();
+    }
+    Slot& s = slots_[id];
+    s.alive = true;
+    s.team.parent = parent;
+    s.team.state = FORMING;
+    s.team.tags.clear();
+    return id;
+  }
+  Team* get(int64_t id) {
+    if (id < 0 || id >= (int64_t)slots_.size() || !slots_[id].alive)
+      return nullptr;
+    return &slots_[id].team;
+  }
+  const Team* get(int64_t id) const {
+    return const_cast<TeamTable*>(this)->get(id);
+  }
+  void release(int64_t id) {
+    slots_[id].alive = false;
+    free_.push_back(id);
+  }
+
+ private:
+  struct Slot {
+    bool alive = false;
+    Team team;
+  };
+  std::vector<Slot> slots_;
+  std::vector<int64_t> free_;
+};
+
 }  // namespace
 
 struct tf_region {
@@ -63,8 +106,7 @@ struct tf_region {
   int32_t executors = 1;
   std::vector<Parent> parents;
   int64_t arrivals = 0;
-  int64_t next_team = 0;
-  std::unordered_map<int64_t, Team> teams;
+  TeamTable teams;
   // per executor: forming teams holding a stream-idle watch, in watch order
   std::vector<std::vector<int64_t>> watchers;
   int64_t teams_formed = 0;
@@ -123,13 +165,8 @@ int tf_region_enter(tf_region* r, int64_t tag, tf_busy_fn busy, void* ctx,
   r->arrivals += 1;
   Parent& p = r->parents[pi];
   int64_t id = p.forming;
-  if (id < 0) {
-    id = r->next_team++;
-    Team t;
-    t.parent = pi;
-    r->teams.emplace(id, std::move(t));
-  }
-  Team& t = r->teams[id];
+  if (id < 0) id = r->teams.create(pi);
+  Team& t = *r->teams.get(id);
   out->parent = pi;
   out->executor = p.executor;
   out->team = id;
@@ -168,11 +205,11 @@ int tf_region_stream_idle(tf_region* r, int32_t executor, int64_t* out_teams,
   fire.swap(r->watchers[executor]);
   int32_t n = 0;
   for (int64_t id : fire) {
-    auto it = r->teams.find(id);
-    if (it == r->teams.end() || it->second.state != FORMING) continue;
-    Parent& p = r->parents[it->second.parent];
+    Team* t = r->teams.get(id);
+    if (!t || t->state != FORMING) continue;
+    Parent& p = r->parents[t->parent];
     if (p.forming == id) p.forming = -1;  // aggregator.py:328-332
-    close_team(r, id, it->second, DRAIN);
+    close_team(r, id, *t, DRAIN);
     if (out_teams && n < cap) out_teams[n] = id;
     ++n;
   }
@@ -181,17 +218,17 @@ int tf_region_stream_idle(tf_region* r, int32_t executor, int64_t* out_teams,
 
 int tf_region_team_size(const tf_region* r, int64_t team) {
   if (!r) return -TF_E_INVALID;
-  auto it = r->teams.find(team);
-  if (it == r->teams.end()) return -TF_E_INVALID;
-  return (int)it->second.tags.size();
+  const Team* t = r->teams.get(team);
+  if (!t) return -TF_E_INVALID;
+  return (int)t->tags.size();
 }
 
 int tf_region_team_members(const tf_region* r, int64_t team, int64_t* tags,
                            int32_t cap) {
   if (!r || !tags) return -TF_E_INVALID;
-  auto it = r->teams.find(team);
-  if (it == r->teams.end()) return -TF_E_INVALID;
-  const auto& v = it->second.tags;
+  const Team* t = r->teams.get(team);
+  if (!t) return -TF_E_INVALID;
+  const auto& v = t->tags;
   const int32_t n = std::min<int32_t>(cap, (int32_t)v.size());
   std::copy(v.begin(), v.begin() + n, tags);
   return (int)v.size();
@@ -199,9 +236,9 @@ int tf_region_team_members(const tf_region* r, int64_t team, int64_t* tags,
 
 int tf_region_team_parent(const tf_region* r, int64_t team) {
   if (!r) return -TF_E_INVALID;
-  auto it = r->teams.find(team);
-  if (it == r->teams.end()) return -TF_E_INVALID;
-  return it->second.parent;
+  const Team* t = r->teams.get(team);
+  if (!t) return -TF_E_INVALID;
+  return t->parent;
 }
 
 int tf_region_stats(const tf_region* r, int64_t* teams_formed,
@@ -218,9 +255,9 @@ int tf_region_stats(const tf_region* r, int64_t* teams_formed,
 // launch; the Python facade after every member left).
 int tf_region_release_team(tf_region* r, int64_t team) {
   if (!r) return TF_E_INVALID;
-  auto it = r->teams.find(team);
-  if (it == r->teams.end() || it->second.state == FORMING) return TF_E_INVALID;
-  r->teams.erase(it);
+  const Team* t = r->teams.get(team);
+  if (!t || t->state == FORMING) return TF_E_INVALID;
+  r->teams.release(team);
   return 0;
 }
 
@@ -275,9 +312,9 @@ struct ReconArgs {
 int launch_team(tf_executor* ex, int64_t team, const ReconArgs& a,
                 int64_t* launches) {
   tf_region* r = ex->region;
-  auto it = r->teams.find(team);
-  if (it == r->teams.end()) return TF_E_INVALID;
-  const Team& t = it->second;
+  const Team* tp = r->teams.get(team);
+  if (!tp) return TF_E_INVALID;
+  const Team& t = *tp;
   int32_t ids[TF_MAX_TEAM];
   const int T = (int)t.tags.size();
   for (int i = 0; i < T; ++i) ids[i] = (int32_t)t.tags[i];
@@ -293,7 +330,7 @@ int launch_team(tf_executor* ex, int64_t team, const ReconArgs& a,
   if (ce != cudaSuccess) return ce;
   ex->recorded[e] = 1;
   ex->busy_until[e] = now_ns() + kRecheckNs;  // just launched: busy
-  r->teams.erase(it);
+  r->teams.release(team);
   *launches += 1;
   return 0;
 }
@@ -437,6 +474,192 @@ int tf_executor_sync(tf_executor* ex) {
   }
   return 0;
 }
+
+}  // extern "C"
+
+// ------------------------------------------------- device-queue executor
+// Strategy 3 where closing a team publishes its sub-grid ids into a ring the
+// GPU's resident consumer grid drains (tf_queue_consumer_launch), instead of
+// launching a kernel.  The reference's signals map to the queue:
+//   busy  == published slices not all completed (per-CTA progress counters
+//            the consumer writes to mapped pinned memory)
+//   drain == observed by polling busy at arrivals (as the stream executor).
+// One queue == one executor (the region must have executors == 1).
+struct QueueCtlHost {   // mirrors QueueCtl (hydro_kernels.cu)
+  long long published;
+  long long final_count;
+  long long completed;
+};
+struct QueueDevInit {   // mirrors QueueDev
+  long long published;
+  long long final_count;
+  unsigned long long claim;
+  unsigned long long done;
+};
+
+struct tf_qexec {
+  tf_region* region = nullptr;
+  QueueCtlHost* ctl_h = nullptr;   // mapped pinned
+  void* ctl_hd = nullptr;          // its device alias
+  int32_t* ring_h = nullptr;       // mapped pinned
+  int32_t* ring_hd = nullptr;      // its device alias
+  int32_t* ring_d = nullptr;       // device mirror
+  int64_t ring_cap = 0;
+  void* qdev = nullptr;            // QueueDevInit on the device
+  int32_t ctas = 0;
+  int32_t n = 0;
+  int64_t published = 0;
+  int64_t busy_until = 0;
+  cudaEvent_t done_ev = nullptr;
+  bool in_flight = false;
+};
+
+namespace {
+
+int64_t q_done(const tf_qexec* q) {
+  return __atomic_load_n(&q->ctl_h->completed, __ATOMIC_ACQUIRE);
+}
+
+int q_busy(void* ctx, int32_t) {
+  tf_qexec* q = static_cast<tf_qexec*>(ctx);
+  const int64_t t = now_ns();
+  if (t < q->busy_until) return 1;
+  if (q_done(q) < q->published) {
+    q->busy_until = t + kRecheckNs;
+    return 1;
+  }
+  return 0;
+}
+
+void q_publish(tf_qexec* q, int64_t team) {
+  tf_region* r = q->region;
+  const Team* t = r->teams.get(team);
+  if (!t) return;
+  for (int64_t tag : t->tags) q->ring_h[q->published++] = (int32_t)tag;
+  // ids first, then the count (release): the consumer acquires the count
+  __atomic_store_n(&q->ctl_h->published, (long long)q->published,
+                   __ATOMIC_RELEASE);
+  q->busy_until = now_ns() + kRecheckNs;
+  r->teams.release(team);
+}
+
+}  // namespace
+
+extern "C" {
+
+int tf_qexec_create(tf_region* region, int32_t n, tf_qexec** out) {
+  if (!region || !out || region->executors != 1 || (n != 8 && n != 16))
+    return TF_E_INVALID;
+  const int ctas = tf_queue_consumer_ctas(n);
+  if (ctas < 1) return ctas < 0 ? -ctas : TF_E_INVALID;
+  tf_qexec* q = new tf_qexec();
+  q->region = region;
+  q->ctas = ctas;
+  q->n = n;
+  cudaError_t e = cudaHostAlloc(&q->ctl_h, sizeof(QueueCtlHost),
+                                cudaHostAllocMapped);
+  if (e == cudaSuccess)
+    e = cudaHostGetDevicePointer(&q->ctl_hd, q->ctl_h, 0);
+  if (e == cudaSuccess) e = cudaMalloc(&q->qdev, sizeof(QueueDevInit));
+  if (e == cudaSuccess)
+    e = cudaEventCreateWithFlags(&q->done_ev, cudaEventDisableTiming);
+  if (e != cudaSuccess) {
+    tf_qexec_destroy(q);
+    return e;
+  }
+  *out = q;
+  return 0;
+}
+
+void tf_qexec_destroy(tf_qexec* q) {
+  if (!q) return;
+  if (q->in_flight) cudaEventSynchronize(q->done_ev);
+  if (q->ctl_h) cudaFreeHost(q->ctl_h);
+  if (q->ring_h) cudaFreeHost(q->ring_h);
+  if (q->ring_d) cudaFree(q->ring_d);
+  if (q->qdev) cudaFree(q->qdev);
+  if (q->done_ev) cudaEventDestroy(q->done_ev);
+  delete q;
+}
+
+int tf_qexec_run_recon_flux(tf_qexec* q, const double* pool_ext,
+                            int64_t pool_slices, const int32_t* ids,
+                            int64_t count, double ax, double ay, double az,
+                            double* um, double* up, double* F, double* amax,
+                            int32_t flux_form, tf_stream_t stream,
+                            int64_t* teams_published) {
+  if (!q || !ids || count < 0 || !teams_published) return TF_E_INVALID;
+  for (int64_t i = 0; i < count; ++i)
+    if (ids[i] < 0 || ids[i] >= pool_slices) return TF_E_INVALID;
+  // the previous run's consumer must be gone before its counters reset
+  if (q->in_flight) {
+    cudaError_t e = cudaEventSynchronize(q->done_ev);
+    if (e != cudaSuccess) return e;
+    q->in_flight = false;
+  }
+  if (count > q->ring_cap || !q->ring_h) {
+    if (q->ring_h) cudaFreeHost(q->ring_h);
+    if (q->ring_d) cudaFree(q->ring_d);
+    q->ring_h = nullptr;
+    q->ring_d = nullptr;
+    const int64_t cap = count > 0 ? count : 1;
+    cudaError_t e = cudaHostAlloc(&q->ring_h, sizeof(int32_t) * cap,
+                                  cudaHostAllocMapped);
+    if (e == cudaSuccess)
+      e = cudaHostGetDevicePointer(reinterpret_cast<void**>(&q->ring_hd),
+                                   q->ring_h, 0);
+    if (e == cudaSuccess)
+      e = cudaMalloc(reinterpret_cast<void**>(&q->ring_d), sizeof(int32_t) * cap);
+    if (e != cudaSuccess) return e;
+    q->ring_cap = cap;
+  }
+  q->published = 0;
+  q->busy_until = 0;
+  q->ctl_h->published = 0;
+  q->ctl_h->final_count = -1;
+  q->ctl_h->completed = 0;
+  __atomic_thread_fence(__ATOMIC_SEQ_CST);
+  cudaStream_t st = (cudaStream_t)stream;
+  const QueueDevInit init{0, -1, 0, 0};
+  cudaError_t ce = cudaMemcpyAsync(q->qdev, &init, sizeof(init),
+                                   cudaMemcpyHostToDevice, st);
+  if (ce != cudaSuccess) return ce;
+  int rc = tf_queue_consumer_launch(
+      pool_ext, pool_slices, q->n, q->ring_hd, q->ctl_hd, q->ring_d, q->qdev,
+      q->ctas, ax, ay, az, um, up, F, amax, flux_form,
+      /*timeout_ns=*/2000000000LL, stream);
+  if (rc) return rc;
+  ce = cudaEventRecord(q->done_ev, st);
+  if (ce != cudaSuccess) return ce;
+  q->in_flight = true;
+  tf_region* r = q->region;
+  int64_t teams = 0;
+  std::vector<int64_t> closed;
+  auto drain = [&]() {
+    closed.assign(r->watchers[0].begin(), r->watchers[0].end());
+    const int k = tf_region_stream_idle(r, 0, closed.data(),
+                                        (int32_t)closed.size());
+    for (int i = 0; i < k; ++i, ++teams) q_publish(q, closed[i]);
+  };
+  for (int64_t i = 0; i < count; ++i) {
+    if (!r->watchers[0].empty() && !q_busy(q, 0)) drain();
+    tf_enter_result res;
+    rc = tf_region_enter(r, ids[i], q_busy, q, &res);
+    if (rc) break;
+    if (res.closed != FORMING) {
+      q_publish(q, res.team);
+      ++teams;
+    }
+  }
+  drain();  // arrivals done: the queue drains, closing what is left
+  // close the queue even on error so the consumer grid exits
+  __atomic_store_n(&q->ctl_h->final_count, (long long)q->published,
+                   __ATOMIC_RELEASE);
+  *teams_published = teams;
+  return rc;
+}
+
+int64_t tf_qexec_completed(const tf_qexec* q) { return q ? q_done(q) : -1; }
 
 }  // extern "C"
 

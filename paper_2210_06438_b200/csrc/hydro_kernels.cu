@@ -816,6 +816,163 @@ int dispatch_recon(const double* pool, int64_t slices, const int32_t* dev_ids,
 
 bool valid_n(int n) { return n == 8 || n == 16; }
 
+// ------------------------------------------------- device work queue
+// Strategy 3 with a device-side queue: a resident grid consumes the slices
+// the host's formation core publishes, team by team, into a ring in mapped
+// pinned memory — a team closure costs a few host stores instead of a
+// kernel launch.  Control block (mapped pinned memory):
+struct QueueCtl {
+  long long published;    // slices published so far (monotonic)
+  long long final_count;  // -1 while more may come
+  long long completed;    // slices finished (written by the fetcher only)
+};
+// device-side mirror, polled by the consumers through L2 (only the fetcher
+// CTA ever touches host memory, so the pollers do not flood PCIe)
+struct QueueDev {
+  long long published;
+  long long final_count;
+  unsigned long long claim;
+  unsigned long long done;
+};
+
+__device__ __forceinline__ long long ld_acquire_gpu(const long long* p) {
+  long long v;
+  asm volatile("ld.acquire.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_gpu(long long* p, long long v) {
+  asm volatile("st.release.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__device__ __forceinline__ long long ld_acquire_sys(const long long* p) {
+  long long v;
+  asm volatile("ld.acquire.sys.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ int ld_relaxed_sys(const int* p) {
+  int v;
+  asm volatile("ld.relaxed.sys.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(long long* p, long long v) {
+  asm volatile("st.release.sys.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Block 0 is the fetcher: its first warp mirrors newly published ids from
+// the host ring into device memory (coalesced), forwards the close marker,
+// and reports the device-side completion count back to the host.  Blocks
+// 1.. are consumers polling the device mirror.
+template <int THREADS>
+__device__ void queue_fetcher(const int* __restrict__ ring_h, QueueCtl* ctl,
+                              int* __restrict__ ring_d, QueueDev* qd,
+                              long long timeout_ns) {
+  if (threadIdx.x >= 32) return;
+  const int lane = threadIdx.x;
+  long long fetched = 0, reported = -1;
+  unsigned long long last_change = globaltimer();
+  for (;;) {
+    const long long pub = ld_acquire_sys(&ctl->published);
+    if (pub > fetched) {
+      for (long long k = fetched + lane; k < pub; k += 32)
+        ring_d[k] = ld_relaxed_sys(ring_h + k);
+      __syncwarp();
+      if (lane == 0) {
+        __threadfence();
+        st_release_gpu(&qd->published, pub);
+      }
+      fetched = pub;
+      last_change = globaltimer();
+    }
+    const long long fin = ld_acquire_sys(&ctl->final_count);
+    if (lane == 0 && fin >= 0 && fetched >= fin)
+      st_release_gpu(&qd->final_count, fin);
+    const long long done =
+        (long long)atomicAdd(&qd->done, 0ULL);  // coherent read
+    if (lane == 0 && done != reported) {
+      st_release_sys(&ctl->completed, done);
+      reported = done;
+      last_change = globaltimer();
+    }
+    if (fin >= 0 && fetched >= fin && done >= fin) break;
+    if ((long long)(globaltimer() - last_change) > timeout_ns) {
+      if (lane == 0) st_release_gpu(&qd->final_count, fetched);
+      break;
+    }
+    __nanosleep(100);
+  }
+}
+
+template <int N, int THREADS>
+__global__ void __launch_bounds__(THREADS, recon_min_blocks<THREADS, 2>())
+    k_queue_consumer(const __grid_constant__ CUtensorMap tmap,
+                     const int* __restrict__ ring_h, QueueCtl* ctl,
+                     int* __restrict__ ring_d, QueueDev* qd, double ax,
+                     double ay, double az, double* __restrict__ um,
+                     double* __restrict__ up, double* __restrict__ F,
+                     double* __restrict__ amax, int flux_form,
+                     long long timeout_ns) {
+  using G = Geo<N>;
+  constexpr int CELLS = G::CELLS;
+  if (blockIdx.x == 0) {
+    queue_fetcher<THREADS>(ring_h, ctl, ring_d, qd, timeout_ns);
+    return;
+  }
+  extern __shared__ __align__(128) double sbox[];
+  __shared__ __align__(8) uint64_t bar;
+  __shared__ double red[THREADS / 32];
+  __shared__ int s_g;
+  if (threadIdx.x == 0) mbar_init(&bar, 1);
+  __syncthreads();
+  uint32_t phase = 0;
+  for (;;) {
+    if (threadIdx.x == 0) {
+      const long long k = (long long)atomicAdd(&qd->claim, 1ULL);
+      const unsigned long long t0 = globaltimer();
+      int g;
+      for (;;) {
+        if (k < ld_acquire_gpu(&qd->published)) {
+          g = ring_d[k];
+          break;
+        }
+        const long long fin = ld_acquire_gpu(&qd->final_count);
+        if (fin >= 0 && k >= fin) {
+          g = -1;  // queue closed and drained
+          break;
+        }
+        if ((long long)(globaltimer() - t0) > timeout_ns) {
+          g = -2;  // nothing arrives: give the GPU back
+          break;
+        }
+        __nanosleep(100);
+      }
+      s_g = g;
+      if (g >= 0) {
+        mbar_expect_tx(&bar, G::BOX * (uint32_t)sizeof(double));
+        tma_load_box(sbox, &tmap, 0, 1, 1, g, &bar);
+      }
+    }
+    __syncthreads();
+    const int g = s_g;
+    if (g < 0) break;
+    mbar_wait(&bar, phase);
+    phase ^= 1;
+    const double speed = slice_compute<N, THREADS, 0, true>(
+        sbox, um + (int64_t)g * 3 * CELLS, up + (int64_t)g * 3 * CELLS,
+        F + (int64_t)g * 3 * CELLS, ax, ay, az, flux_form);
+    if (amax != nullptr) block_max_store<THREADS>(speed, red, amax + g);
+    __syncthreads();  // box consumed, this slice's stores issued
+    if (threadIdx.x == 0) {
+      __threadfence();
+      atomicAdd(&qd->done, 1ULL);
+    }
+  }
+}
+
 }  // namespace
 
 extern "C" {
@@ -982,6 +1139,62 @@ int tf_pool_to_field_f64(const double* pool_ext, int32_t grid_n, int32_t n,
                          double* field, tf_stream_t stream) {
   return field_pool(field, const_cast<double*>(pool_ext), grid_n, n, 1,
                     stream);
+}
+
+int tf_queue_consumer_ctas(int32_t n) {
+  if (!valid_n(n)) return -TF_E_INVALID;
+  int dev = 0, sms = 0, res = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  constexpr int TH = 512;
+  cudaError_t e;
+  if (n == 8) {
+    e = cudaFuncSetAttribute(k_queue_consumer<8, TH>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)(Geo<8>::BOX * sizeof(double)));
+    if (e == cudaSuccess)
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+          &res, k_queue_consumer<8, TH>, TH, Geo<8>::BOX * sizeof(double));
+  } else {
+    e = cudaFuncSetAttribute(k_queue_consumer<16, TH>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)(Geo<16>::BOX * sizeof(double)));
+    if (e == cudaSuccess)
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+          &res, k_queue_consumer<16, TH>, TH, Geo<16>::BOX * sizeof(double));
+  }
+  if (e != cudaSuccess) return -(int)e;
+  return sms * (res > 0 ? res : 1);
+}
+
+int tf_queue_consumer_launch(const double* pool_ext, int64_t pool_slices,
+                             int32_t n, const int32_t* ring_h, void* ctl_h,
+                             int32_t* ring_d, void* qdev, int32_t ctas,
+                             double ax, double ay, double az, double* um,
+                             double* up, double* F, double* amax,
+                             int32_t flux_form, int64_t timeout_ns,
+                             tf_stream_t stream) {
+  if (!valid_n(n) || !pool_ext || !ring_h || !ctl_h || !ring_d || !qdev ||
+      ctas < 1 || !um || !up || !F)
+    return TF_E_INVALID;
+  CUtensorMap map;
+  int rc = pool_map(pool_ext, pool_slices, n, &map);
+  if (rc) return rc;
+  constexpr int TH = 512;
+  cudaStream_t st = (cudaStream_t)stream;
+  QueueCtl* c = static_cast<QueueCtl*>(ctl_h);
+  QueueDev* q = static_cast<QueueDev*>(qdev);
+  // grid: the fetcher block + `ctas` consumers
+  if (n == 8)
+    k_queue_consumer<8, TH><<<ctas + 1, TH, Geo<8>::BOX * sizeof(double), st>>>(
+        map, ring_h, c, ring_d, q, ax, ay, az, um, up, F, amax, flux_form,
+        timeout_ns);
+  else
+    k_queue_consumer<16, TH>
+        <<<ctas + 1, TH, Geo<16>::BOX * sizeof(double), st>>>(
+            map, ring_h, c, ring_d, q, ax, ay, az, um, up, F, amax, flux_form,
+            timeout_ns);
+  return cudaGetLastError();
 }
 
 const char* tf_version(void) { return "taskfuse_b200 0.1 sm_100a"; }

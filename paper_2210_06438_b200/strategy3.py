@@ -241,6 +241,51 @@ class RealtimeExecutor:
             self.handle = None
 
 
+class QueueExecutor:
+    """Strategy 3 with a device-side work queue (tf_qexec): the formation
+    core's closed teams are PUBLISHED to a resident consumer grid instead of
+    launched — a team closure costs a few host stores; the starvation
+    signal is 'every published slice completed'."""
+
+    def __init__(self, name: str, max_team: int, parents: int, n: int = 8):
+        self.core = FormationCore(name, max_team, parents, 1)
+        self.lib = self.core.lib
+        h = C.c_void_p()
+        _lib.check(self.lib.tf_qexec_create(self.core.handle, n, C.byref(h)),
+                   "tf_qexec_create")
+        self.handle = h
+        self.n = n
+
+    def run(self, pool, velocity, ids, um, up, F, amax=None, flux_form=0,
+            stream=None) -> int:
+        """Publish the arrivals; returns teams published.  The consumer runs
+        on `stream` (default: the current stream)."""
+        arr = np.ascontiguousarray(np.asarray(ids, dtype=np.int32))
+        s = stream if stream is not None else torch.cuda.current_stream()
+        teams = C.c_int64()
+        ax, ay, az = (float(v) for v in velocity)
+        self._keep = arr
+        _lib.check(self.lib.tf_qexec_run_recon_flux(
+            self.handle, pool.data_ptr(), pool.shape[0],
+            arr.ctypes.data_as(C.POINTER(C.c_int32)), arr.size, ax, ay, az,
+            um.data_ptr(), up.data_ptr(), F.data_ptr(),
+            None if amax is None else amax.data_ptr(), int(flux_form),
+            s.cuda_stream, C.byref(teams)), "tf_qexec_run_recon_flux")
+        return teams.value
+
+    def completed(self) -> int:
+        return self.lib.tf_qexec_completed(self.handle)
+
+    def stats(self) -> dict:
+        return self.core.stats()
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h:
+            self.lib.tf_qexec_destroy(h)
+            self.handle = None
+
+
 class AggregatedIteration:
     """One device-resident hydro iteration with strategy-3 team launches:
     ghost fill -> reconstruct+flux (captured team plan) -> update -> swap.

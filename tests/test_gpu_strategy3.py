@@ -64,6 +64,30 @@ def test_team_plan_bit_exact(cuda, cfg2, A, E):
     assert bool((amax == 1.0).all())
 
 
+@pytest.mark.parametrize("A", [1, 16, 128])
+def test_queue_executor_bit_exact(cuda, cfg2, A):
+    """Device-queue strategy 3: every arrival published exactly once, the
+    consumer grid completes them all, results bit-exact; runs back to back
+    reuse the queue."""
+    import torch
+    from paper_2210_06438_b200.strategy3 import QueueExecutor, default_parents
+    pool, n, vel, oum, oup, oF = cfg2
+    S = pool.shape[0]
+    q = QueueExecutor("reconstruct", A, default_parents(S, A), n)
+    for rep in range(2):
+        um, up, F = _outs(S, n, cuda)
+        order = np.random.default_rng(rep).permutation(S)
+        teams = q.run(pool, vel, order, um, up, F)
+        torch.cuda.synchronize()
+        assert q.completed() == S
+        assert np.array_equal(F.cpu().numpy(), oF)
+        assert np.array_equal(up.cpu().numpy(), oup)
+    st = q.stats()
+    assert st["teams_formed"] == sum(st["size_histogram"].values())
+    assert sum(k * v for k, v in st["size_histogram"].items()) == 2 * S
+    assert max(st["size_histogram"]) <= A
+
+
 @pytest.mark.parametrize("grid,n,vel", [(32, 8, (1.0, 1.0, 1.0)),
                                         (64, 8, (-1.0, 0.5, -0.25)),
                                         (64, 16, (0.7, -1.3, 0.0))])
