@@ -106,6 +106,7 @@ struct tf_region {
   int32_t executors = 1;
   std::vector<Parent> parents;
   int64_t arrivals = 0;
+  int32_t next_parent = 0;  // == arrivals % parents.size(), kept incrementally
   TeamTable teams;
   // per executor: forming teams holding a stream-idle watch, in watch order
   std::vector<std::vector<int64_t>> watchers;
@@ -161,8 +162,9 @@ int32_t tf_region_parent_executor(const tf_region* r, int32_t parent) {
 int tf_region_enter(tf_region* r, int64_t tag, tf_busy_fn busy, void* ctx,
                     tf_enter_result* out) {
   if (!r || !out) return TF_E_INVALID;
-  const int32_t pi = (int32_t)(r->arrivals % (int64_t)r->parents.size());
+  const int32_t pi = r->next_parent;  // parents[arrivals % P]
   r->arrivals += 1;
+  if (++r->next_parent == (int32_t)r->parents.size()) r->next_parent = 0;
   Parent& p = r->parents[pi];
   int64_t id = p.forming;
   if (id < 0) id = r->teams.create(pi);
@@ -409,7 +411,7 @@ int tf_executor_run_recon_flux(tf_executor* ex, const double* pool_ext,
   for (int64_t i = 0; i < count; ++i) {
     // real-time drain signal: before the arrival joins its parent's forming
     // team, observe whether that parent's stream has gone idle meanwhile
-    const int32_t pi = (int32_t)(r->arrivals % (int64_t)r->parents.size());
+    const int32_t pi = r->next_parent;
     const int32_t pe = r->parents[pi].executor;
     if (!r->watchers[pe].empty() && !rt_busy(ex, pe)) {
       int rc = drain_executor(ex, pe, a, launches);
@@ -509,6 +511,7 @@ struct tf_qexec {
   int32_t ctas = 0;
   int32_t n = 0;
   int64_t published = 0;
+  int64_t seen_published = 0;
   int64_t busy_until = 0;
   cudaEvent_t done_ev = nullptr;
   bool in_flight = false;
@@ -523,6 +526,12 @@ int64_t q_done(const tf_qexec* q) {
 int q_busy(void* ctx, int32_t) {
   tf_qexec* q = static_cast<tf_qexec*>(ctx);
   const int64_t t = now_ns();
+  // work published since the last look cannot be finished yet
+  if (q->published != q->seen_published) {
+    q->seen_published = q->published;
+    q->busy_until = t + kRecheckNs;
+    return 1;
+  }
   if (t < q->busy_until) return 1;
   if (q_done(q) < q->published) {
     q->busy_until = t + kRecheckNs;
@@ -539,7 +548,6 @@ void q_publish(tf_qexec* q, int64_t team) {
   // ids first, then the count (release): the consumer acquires the count
   __atomic_store_n(&q->ctl_h->published, (long long)q->published,
                    __ATOMIC_RELEASE);
-  q->busy_until = now_ns() + kRecheckNs;
   r->teams.release(team);
 }
 
@@ -614,6 +622,7 @@ int tf_qexec_run_recon_flux(tf_qexec* q, const double* pool_ext,
     q->ring_cap = cap;
   }
   q->published = 0;
+  q->seen_published = 0;
   q->busy_until = 0;
   q->ctl_h->published = 0;
   q->ctl_h->final_count = -1;

@@ -164,7 +164,7 @@ __device__ __forceinline__ double slice_compute(
   const double av[3] = {ax, ay, az};
   const int stv[3] = {B * BZ, BZ, 1};
   double speed = 0.0;
-  if (!PAIR) {
+  if constexpr (!PAIR) {
     // one cell per thread-iteration, 8-byte stores
     for (int c = threadIdx.x; c < CELLS; c += THREADS) {
       const int ci = c / (C * C), cj = (c / C) % C, ck = c % C;
@@ -183,7 +183,7 @@ __device__ __forceinline__ double slice_compute(
       }
     }
     return speed;
-  }
+  } else {
   for (int p = threadIdx.x; p < PAIRS; p += THREADS) {
     const int ci = p / (C * HP);
     const int cj = (p / HP) % C;
@@ -210,6 +210,7 @@ __device__ __forceinline__ double slice_compute(
     }
   }
   return speed;
+  }
 }
 
 // Block-wide max of the per-thread signal speeds -> one store (reduce stage).
