@@ -1,0 +1,36 @@
+"""bench.py contract pieces that run without a GPU: the algorithmic byte
+counts (SURVEY §8 d) and the --impl reference line (the reference's CPU path
+timed on host cores)."""
+
+import json
+import os
+import subprocess
+import sys
+
+from conftest import ROOT
+
+
+def test_algorithmic_bytes():
+    sys.path.insert(0, str(ROOT))
+    import bench
+    assert bench.b_alg(8) == 84800          # 165.63 B per cell-update
+    assert bench.b_alg(16) == 482112
+    assert bench.b_step(8) == 16896         # 33.0 B per cell-update
+    assert abs(bench.b_alg(8) / 512 - 165.625) < 1e-9
+
+
+def test_reference_arm_line():
+    env = dict(os.environ, CUDA_VISIBLE_DEVICES="")
+    out = subprocess.run(
+        [sys.executable, str(ROOT / "bench.py"), "--impl", "reference",
+         "--steps", "1", "--warmup", "0"],
+        capture_output=True, text=True, timeout=600, env=env, cwd=str(ROOT))
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    assert line["impl"] == "reference"
+    assert line["unit"] == "cell-updates/s" and line["value"] > 0
+    assert line["higher_is_better"] is True
+    assert line["e2e"]["h2d_bytes_per_step"] == 0
+    assert line["cpu_baseline"]["kind"] == "port"
+    assert line["cpu_baseline"]["cores"] >= 1
+    assert line["warmup"] >= 3
