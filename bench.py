@@ -389,6 +389,9 @@ def fused_legs(args, steps, warmup, world, stream, peak):
     host_out = torch.empty_like(host_in).pin_memory()
     ms_e2e = timed(lambda k: it.run_host(host_in, host_out), steps, warmup,
                    world, stream)
+    from paper_2210_06438_b200.field import HostPipeline
+    pipe = HostPipeline(it, host_in, host_out, chunks=8)
+    ms_pipe = timed(lambda k: pipe.run(), steps, warmup, world, stream)
     S = (GRID // N_SUB) ** 3
     n = N_SUB
     fused_bytes = S * b_step(n)
@@ -403,6 +406,15 @@ def fused_legs(args, steps, warmup, world, stream, peak):
                 "ms_per_step": ms_e2e,
                 "h2d_bytes_per_step": host_in.numel() * 8,
                 "d2h_bytes_per_step": host_out.numel() * 8},
+        "e2e_pipelined": {
+            "value": rate(S * world, n, ms_pipe), "unit": UNIT,
+            "ms_per_step": ms_pipe,
+            "h2d_bytes_per_step": host_in.numel() * 8,
+            "d2h_bytes_per_step": host_out.numel() * 8,
+            "gpu_launches_per_step": pipe.launches,
+            "step": "field.HostPipeline: 8 x-chunks, upload / scatter+halo "
+                    "/ fused step / gather / download overlapped, captured "
+                    "as one CUDA graph"},
     }
 
 
@@ -596,18 +608,22 @@ def main():
     }
     e_ms, bi, bo, e_launch = e2e_leg(args, max(10, args.steps // 2), 3,
                                      world, stream)
-    line["e2e"] = {"value": rate(total_S, wl.n, e_ms), "unit": UNIT,
-                   "h2d_bytes_per_step": bi, "d2h_bytes_per_step": bo,
-                   "ms_per_step": e_ms,
-                   "step": "host field (pinned) -> device scatter -> ghost "
-                           "fill -> aggregated recon+flux teams -> update -> "
-                           "gather -> host field (AggregatedIteration."
-                           "run_host)",
-                   "gpu_launches_per_step": e_launch}
+    line["e2e_materialising"] = {
+        "value": rate(total_S, wl.n, e_ms), "unit": UNIT,
+        "h2d_bytes_per_step": bi, "d2h_bytes_per_step": bo,
+        "ms_per_step": e_ms,
+        "step": "host field (pinned) -> device scatter -> ghost fill -> "
+                "aggregated recon+flux teams (um/up/F to HBM) -> update -> "
+                "gather -> host field (AggregatedIteration.run_host)",
+        "gpu_launches_per_step": e_launch}
     f_ms, fbi, fbo = e2e_faces_leg(wl, step, max(5, args.steps // 5), 3,
                                    world, stream)
     line["fused_full_iteration"] = fused_legs(args, max(10, args.steps // 2),
                                               3, world, stream, peak)
+    # headline e2e: the public host->host iteration API (pinned host field
+    # in, one hydro iteration = reconstruct + flux + update of every
+    # sub-grid, pinned host field out), transfers overlapped with compute
+    line["e2e"] = dict(line["fused_full_iteration"]["e2e_pipelined"])
     line["e2e_faces"] = {"value": rate(total_S, wl.n, f_ms), "unit": UNIT,
                          "h2d_bytes_per_step": fbi,
                          "d2h_bytes_per_step": fbo, "ms_per_step": f_ms,

@@ -288,6 +288,14 @@ int tf_field_step_f64(const double* padded_in, int32_t X, int32_t Gy,
                       int32_t flags, tf_stream_t stream);
 int tf_field_halo_f64(double* padded, int32_t X, int32_t Gy, int32_t Gz,
                       int32_t periodic_x, tf_stream_t stream);
+/* y/z halos of padded layers [first, first+count) only; the periodic x halo
+ * (side 1: low halo <- last owned layers, 2: high <- first, 3: both).
+ * Used by the chunked host pipeline (FieldIteration.run_host_pipelined).    */
+int tf_field_halo_layers_f64(double* padded, int32_t X, int32_t Gy,
+                             int32_t Gz, int32_t first, int32_t count,
+                             tf_stream_t stream);
+int tf_field_halo_xwrap_f64(double* padded, int32_t X, int32_t Gy, int32_t Gz,
+                            int32_t side, tf_stream_t stream);
 int tf_field_pad_f64(const double* field, int32_t X, int32_t Gy, int32_t Gz,
                      double* padded, tf_stream_t stream);
 int tf_field_unpad_f64(const double* padded, int32_t X, int32_t Gy,

@@ -94,6 +94,9 @@ SIGNATURES = {
                                     _i32, _f64, _f64, _f64, _f64, _p, _i32,
                                     _p]),
     "tf_field_halo_f64": (C.c_int, [_p, _i32, _i32, _i32, _i32, _p]),
+    "tf_field_halo_layers_f64": (C.c_int, [_p, _i32, _i32, _i32, _i32, _i32,
+                                           _p]),
+    "tf_field_halo_xwrap_f64": (C.c_int, [_p, _i32, _i32, _i32, _i32, _p]),
     "tf_field_pad_f64": (C.c_int, [_p, _i32, _i32, _i32, _p, _p]),
     "tf_field_unpad_f64": (C.c_int, [_p, _i32, _i32, _i32, _p, _p]),
     "tf_qexec_create": (C.c_int, [_p, _i32, C.POINTER(_p)]),

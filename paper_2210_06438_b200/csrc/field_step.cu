@@ -402,6 +402,40 @@ int tf_field_halo_f64(double* padded, int32_t X, int32_t Gy, int32_t Gz,
   return cudaGetLastError();
 }
 
+int tf_field_halo_layers_f64(double* padded, int32_t X, int32_t Gy,
+                             int32_t Gz, int32_t first, int32_t count,
+                             tf_stream_t stream) {
+  if (!padded || X < 2 || Gy < 2 || Gz < 4 || first < 0 || count < 0 ||
+      first + count > X + 2 * HX)
+    return TF_E_INVALID;
+  if (count == 0) return 0;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int py = Gy + 2 * HY, pz = Gz + 2 * HZ;
+  double* base = padded + (size_t)first * py * pz;
+  k_halo_yz<<<grid_for((int64_t)count * 2 * HY * Gz), 256, 0, st>>>(base, count, Gy, Gz);
+  k_halo_z<<<grid_for((int64_t)count * py * 2 * HZ), 256, 0, st>>>(base, count, Gy, Gz);
+  return cudaGetLastError();
+}
+
+int tf_field_halo_xwrap_f64(double* padded, int32_t X, int32_t Gy, int32_t Gz,
+                            int32_t side, tf_stream_t stream) {
+  if (!padded || X < 2 || (side & ~3) || side == 0) return TF_E_INVALID;
+  const int py = Gy + 2 * HY, pz = Gz + 2 * HZ;
+  const size_t layer = (size_t)py * pz;
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaError_t e = cudaSuccess;
+  if (side & 1)  // low x halo <- the last owned layers
+    e = cudaMemcpyAsync(padded, padded + (size_t)X * layer,
+                        HX * layer * sizeof(double), cudaMemcpyDeviceToDevice,
+                        st);
+  if (e == cudaSuccess && (side & 2))  // high x halo <- the first owned layers
+    e = cudaMemcpyAsync(padded + (size_t)(X + HX) * layer,
+                        padded + (size_t)HX * layer,
+                        HX * layer * sizeof(double), cudaMemcpyDeviceToDevice,
+                        st);
+  return e;
+}
+
 int tf_field_pad_f64(const double* field, int32_t X, int32_t Gy, int32_t Gz,
                      double* padded, tf_stream_t stream) {
   if (!field || !padded || X < 1 || Gy < 1 || Gz < 1) return TF_E_INVALID;

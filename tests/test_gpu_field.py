@@ -53,6 +53,47 @@ def test_field_host_roundtrip(cuda):
     assert np.array_equal(hout.numpy(), HO.advect_once(f))
 
 
+@pytest.mark.parametrize("grid,n,chunks,vel", [
+    (64, 8, 8, (1.0, 1.0, 1.0)), (128, 8, 8, (-1.0, 0.5, -0.25)),
+    (128, 8, 4, (0.7, -1.3, 0.0)), (128, 16, 8, (1.0, 1.0, 1.0)),
+    (32, 8, 8, (1.0, 1.0, 1.0))])
+def test_field_host_pipelined(cuda, grid, n, chunks, vel):
+    """Chunked, transfer-overlapped host round trip == one reference
+    iteration; repeated calls chain correctly."""
+    import torch
+    from paper_2210_06438_b200.field import FieldIteration
+    f = HO.stress_field(grid)
+    it = FieldIteration(grid, n, vel, max_team=32, executors=2)
+    hin = torch.from_numpy(f).pin_memory()
+    hout = torch.empty_like(hin).pin_memory()
+    it.run_host_pipelined(hin, hout, chunks=chunks)
+    torch.cuda.synchronize()
+    assert np.array_equal(hout.numpy(), HO.advect_once(f, vel))
+    h2 = torch.empty_like(hin).pin_memory()
+    it.run_host_pipelined(hout, h2, chunks=chunks)
+    torch.cuda.synchronize()
+    assert np.array_equal(h2.numpy(),
+                          HO.advect_once(HO.advect_once(f, vel), vel))
+
+
+def test_host_pipeline_graph(cuda):
+    import torch
+    from paper_2210_06438_b200.field import FieldIteration, HostPipeline
+    f = HO.stress_field(128)
+    it = FieldIteration(128, 8, (1.0, 1.0, 1.0))
+    hin = torch.from_numpy(f).pin_memory()
+    hout = torch.full_like(hin, float("nan")).pin_memory()
+    pipe = HostPipeline(it, hin, hout, chunks=8)
+    hout.fill_(float("nan"))
+    pipe.run()
+    torch.cuda.synchronize()
+    assert np.array_equal(hout.numpy(), HO.advect_once(f))
+    hin.copy_(torch.from_numpy(HO.initial_field(128)))   # new input, replay
+    pipe.run()
+    torch.cuda.synchronize()
+    assert np.array_equal(hout.numpy(), HO.advect_once(HO.initial_field(128)))
+
+
 @pytest.mark.parametrize("world,n,grid,vel", [
     (2, 8, 32, (1.0, 1.0, 1.0)), (4, 8, 64, (-1.0, 0.5, -0.25)),
     (2, 16, 64, (0.7, -1.3, 0.0)), (8, 8, 64, (1.0, 1.0, 1.0))])
