@@ -24,7 +24,6 @@
 #include <cudaTypedefs.h>
 #include <stdint.h>
 
-#include <cstdlib>
 #include <mutex>
 #include <unordered_map>
 
@@ -93,15 +92,13 @@ struct TeamIds {
 
 template <int N>
 struct FGeo {
-  static constexpr int C = N + 2;
-  static constexpr int BX = N + 4, BY = N + 4, BZ = N + 8;
+  static constexpr int BX = N + 4, BY = N + 4, BZ = N + 8;  // stencil box
   static constexpr int BOX = BX * BY * BZ;
-  static constexpr int CELLS = C * C * C;
 };
 
 // One CTA per sub-grid: fused recon+flux+update.  Sub-grid id -> lattice
 // coordinates in the (mx, m, m) local lattice.
-template <int N, int THREADS, bool DEV_IDS, bool DIRECT>
+template <int N, int THREADS, bool DEV_IDS>
 __global__ void __launch_bounds__(THREADS)
     k_step_fused(const __grid_constant__ CUtensorMap tmap,
                  const int32_t* __restrict__ dev_ids,
@@ -109,10 +106,8 @@ __global__ void __launch_bounds__(THREADS)
                  double ay, double az, double dt_dx, double* __restrict__ out,
                  int64_t pyz, int pz) {
   using G = FGeo<N>;
-  constexpr int C = G::C, BY = G::BY, BZ = G::BZ, CELLS = G::CELLS;
-  extern __shared__ __align__(128) double smem[];
-  double* sbox = smem;             // BOX
-  double* sF = smem + G::BOX;      // 3 * CELLS
+  constexpr int BY = G::BY, BZ = G::BZ;
+  extern __shared__ __align__(128) double sbox[];
   __shared__ __align__(8) uint64_t bar;
 
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -128,49 +123,25 @@ __global__ void __launch_bounds__(THREADS)
   __syncthreads();
   mbar_wait(&bar);
 
+  // Each thread: its owned cells' 6 face fluxes straight from the box, then
+  // update_body (kernels.py:100-111: x, y, z accumulation order, no FMA).
+  // Every interior face is computed twice — measured cheaper than a 24 KB
+  // shared flux array plus a block barrier (1.89 -> 0.745 ms on 262 144
+  // sub-grids); the arithmetic and its order are unchanged.
   const int stx = BY * BZ, sty = BZ;
-  if (DIRECT) {
-    // each thread: its owned cells' 6 face fluxes straight from the box
-    // (every interior face is computed twice — cheaper than a 24 KB shared
-    // flux array and a block barrier); same arithmetic, same order
-    for (int o = threadIdx.x; o < N * N * N; o += THREADS) {
-      const int i = o / (N * N), j = (o / N) % N, k = o % N;
-      // owned (i,j,k) = box (i+2, j+2, k+4); its minus face = box - stride
-      const int b = ((i + 2) * BY + (j + 2)) * BZ + (k + 4);
-      double div = __dsub_rn(face_flux(sbox, b, stx, ax),
-                             face_flux(sbox, b - stx, stx, ax));
-      div = __dadd_rn(div, __dsub_rn(face_flux(sbox, b, sty, ay),
-                                     face_flux(sbox, b - sty, sty, ay)));
-      div = __dadd_rn(div, __dsub_rn(face_flux(sbox, b, 1, az),
-                                     face_flux(sbox, b - 1, 1, az)));
-      const int64_t x = (int64_t)bx * N + i + HX, y = (int64_t)by * N + j + HY,
-                    z = (int64_t)bz * N + k + HZ;
-      out[x * pyz + y * pz + z] = __dsub_rn(sbox[b], __dmul_rn(dt_dx, div));
-    }
-    return;
-  }
-  // cube c (0..C-1) = global b*n-1+c = box index (c+1, c+1, c+3)
-  for (int c = threadIdx.x; c < CELLS; c += THREADS) {
-    const int ci = c / (C * C), cj = (c / C) % C, ck = c % C;
-    const int b = ((ci + 1) * BY + (cj + 1)) * BZ + (ck + 3);
-    // the last face layer (the np.roll wrap) is never read by the update;
-    // for a < 0 its upwind cell lies outside the box, so it is skipped
-    sF[c] = (ax < 0.0 && ci == C - 1) ? 0.0 : face_flux(sbox, b, stx, ax);
-    sF[CELLS + c] = (ay < 0.0 && cj == C - 1) ? 0.0 : face_flux(sbox, b, sty, ay);
-    sF[2 * CELLS + c] = (az < 0.0 && ck == C - 1) ? 0.0 : face_flux(sbox, b, 1, az);
-  }
-  __syncthreads();
-  // update_body (kernels.py:100-111): x, y, z accumulation order, no FMA
   for (int o = threadIdx.x; o < N * N * N; o += THREADS) {
     const int i = o / (N * N), j = (o / N) % N, k = o % N;
-    const int own = ((i + 1) * C + (j + 1)) * C + (k + 1);
-    double div = __dsub_rn(sF[own], sF[own - C * C]);
-    div = __dadd_rn(div, __dsub_rn(sF[CELLS + own], sF[CELLS + own - C]));
-    div = __dadd_rn(div, __dsub_rn(sF[2 * CELLS + own], sF[2 * CELLS + own - 1]));
-    const double u = sbox[((i + 2) * BY + (j + 2)) * BZ + (k + 4)];
+    // owned (i,j,k) = box (i+2, j+2, k+4); its minus face = box - stride
+    const int b = ((i + 2) * BY + (j + 2)) * BZ + (k + 4);
+    double div = __dsub_rn(face_flux(sbox, b, stx, ax),
+                           face_flux(sbox, b - stx, stx, ax));
+    div = __dadd_rn(div, __dsub_rn(face_flux(sbox, b, sty, ay),
+                                   face_flux(sbox, b - sty, sty, ay)));
+    div = __dadd_rn(div, __dsub_rn(face_flux(sbox, b, 1, az),
+                                   face_flux(sbox, b - 1, 1, az)));
     const int64_t x = (int64_t)bx * N + i + HX, y = (int64_t)by * N + j + HY,
                   z = (int64_t)bz * N + k + HZ;
-    out[x * pyz + y * pz + z] = __dsub_rn(u, __dmul_rn(dt_dx, div));
+    out[x * pyz + y * pz + z] = __dsub_rn(sbox[b], __dmul_rn(dt_dx, div));
   }
 }
 
@@ -278,14 +249,15 @@ int field_map(const double* P, int X, int Gy, int Gz, int n, CUtensorMap* out) {
   return 0;
 }
 
-template <int N, bool DEV_IDS, int TH, bool DIRECT>
-int launch_step_var(const CUtensorMap& map, const int32_t* dev_ids,
-                    const TeamIds& team, int T, int m, double ax, double ay,
-                    double az, double dt_dx, double* out, int X, int Gy,
-                    int Gz, cudaStream_t st, int flags) {
-  constexpr size_t smem =
-      (FGeo<N>::BOX + (DIRECT ? 0 : 3 * FGeo<N>::CELLS)) * sizeof(double);
-  auto kern = k_step_fused<N, TH, DEV_IDS, DIRECT>;
+template <int N, bool DEV_IDS>
+int launch_step(const CUtensorMap& map, const int32_t* dev_ids,
+                const TeamIds& team, int T, int m, double ax, double ay,
+                double az, double dt_dx, double* out, int X, int Gy, int Gz,
+                cudaStream_t st, int flags) {
+  // 128 threads per sub-grid: measured best of 128/256/512
+  constexpr int TH = 128;
+  constexpr size_t smem = FGeo<N>::BOX * sizeof(double);
+  auto kern = k_step_fused<N, TH, DEV_IDS>;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(
@@ -307,29 +279,6 @@ int launch_step_var(const CUtensorMap& map, const int32_t* dev_ids,
   (void)X;
   return cudaLaunchKernelEx(&cfg, kern, map, dev_ids, team, m, ax, ay, az,
                             dt_dx, out, pyz, (int)pz);
-}
-
-template <int N, bool DEV_IDS>
-int launch_step(const CUtensorMap& map, const int32_t* dev_ids,
-                const TeamIds& team, int T, int m, double ax, double ay,
-                double az, double dt_dx, double* out, int X, int Gy, int Gz,
-                cudaStream_t st, int flags) {
-  // TASKFUSE_STEP_VARIANT (A/B only): 0 shared flux array / 512 threads,
-  // 1 direct / 512, 2 direct / 256, 3 direct / 128 (default; measured
-  // 0.745 ms vs 1.89 ms for variant 0 on 262 144 sub-grids)
-  static const int var = [] {
-    const char* v = getenv("TASKFUSE_STEP_VARIANT");
-    return v ? atoi(v) : 3;
-  }();
-#define TF_STEP(TH_, D_)                                                   \
-  return launch_step_var<N, DEV_IDS, TH_, D_>(map, dev_ids, team, T, m, ax, \
-                                              ay, az, dt_dx, out, X, Gy, Gz, \
-                                              st, flags)
-  if (var == 0) TF_STEP(512, false);
-  if (var == 2) TF_STEP(256, true);
-  if (var == 3) TF_STEP(128, true);
-  TF_STEP(512, true);
-#undef TF_STEP
 }
 
 int grid_for(int64_t total) {

@@ -227,29 +227,17 @@ __device__ __forceinline__ void block_max_store(double v, double* red,
   }
 }
 
-// Code-shape variants of the team kernel (measured):
-// VAR 0 scalar 8-B stores, >= 6 CTAs/SM; VAR 1 z-pairs, 16-B stores, >= 6
-// CTAs/SM; VAR 2 z-pairs, register-unconstrained.
-template <int N, int VAR>
-struct ReconShape {
-  // VAR: 0 scalar/1536, 1 pair/1536, 2 pair/2048, 4 pair/1024, 5 scalar/2048
-  static constexpr bool pair = VAR != 0 && VAR != 5;
-  // resident threads per SM the register budget must allow (2048 -> <= 32
-  // registers/thread, full occupancy; 1536 -> 42; 1024 -> 64)
-  static constexpr int sm_threads =
-      (VAR == 2 || VAR == 5) ? 2048 : (VAR == 4 ? 1024 : 1536);
-};
-template <int THREADS, int VAR>
+// Register budget: <= 32 registers/thread so 2048 threads (4 CTAs of 512)
+// are resident per SM — measured best on B200 (DESIGN.md §4 table).
+template <int THREADS>
 constexpr int recon_min_blocks() {
-  return ReconShape<8, VAR>::sm_threads / THREADS > 0
-             ? ReconShape<8, VAR>::sm_threads / THREADS
-             : 1;
+  return 2048 / THREADS > 0 ? 2048 / THREADS : 1;
 }
 
 // Fused reconstruct + flux.  MODE 0: um, up and F; MODE 1: um, up only
 // (reconstruct_body alone).  One CTA per aggregated slice.
-template <int N, int THREADS, int MODE, bool DEV_IDS, int VAR = 0>
-__global__ void __launch_bounds__(THREADS, recon_min_blocks<THREADS, VAR>())
+template <int N, int THREADS, int MODE, bool DEV_IDS>
+__global__ void __launch_bounds__(THREADS, recon_min_blocks<THREADS>())
     k_recon_flux(const __grid_constant__ CUtensorMap tmap,
                  const int32_t* __restrict__ dev_ids,
                  const __grid_constant__ TeamIds team, int out_mode, double ax,
@@ -278,157 +266,10 @@ __global__ void __launch_bounds__(THREADS, recon_min_blocks<THREADS, VAR>())
   mbar_wait(&bar, 0);
 
   const int64_t slot = out_mode ? (int64_t)g : (int64_t)s;
-  const double speed = slice_compute<N, THREADS, MODE,
-                                     ReconShape<N, VAR>::pair>(
+  const double speed = slice_compute<N, THREADS, MODE>(
       sbox, um + slot * 3 * CELLS, up + slot * 3 * CELLS,
       MODE == 0 ? F + slot * 3 * CELLS : nullptr, ax, ay, az, flux_form);
   if (MODE == 0 && amax != nullptr) block_max_store<THREADS>(speed, red, amax + slot);
-}
-
-__device__ __forceinline__ void bulk_store(void* gdst, const void* ssrc,
-                                           uint32_t bytes) {
-  asm volatile(
-      "cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(
-          reinterpret_cast<uint64_t>(gdst)),
-      "r"(smem_u32(ssrc)), "r"(bytes)
-      : "memory");
-}
-
-// VAR 3 (n = 8, MODE 0): outputs staged in shared memory one axis at a time
-// and written by TMA bulk stores (cp.async.bulk.global.shared::cta, 8000 B
-// per array), double-buffered across axes; the threads never issue a global
-// store.
-template <bool DEV_IDS>
-__global__ void __launch_bounds__(256, 3)
-    k_recon_flux_bulkstore(const __grid_constant__ CUtensorMap tmap,
-                           const int32_t* __restrict__ dev_ids,
-                           const __grid_constant__ TeamIds team, int out_mode,
-                           double ax, double ay, double az,
-                           double* __restrict__ um, double* __restrict__ up,
-                           double* __restrict__ F, double* __restrict__ amax,
-                           int flux_form) {
-  constexpr int N = 8, THREADS = 256;
-  using G = Geo<N>;
-  constexpr int C = G::C, B = G::B, BZ = G::BZ, CELLS = G::CELLS;
-  constexpr int HP = C / 2, PAIRS = C * C * HP;
-  extern __shared__ __align__(128) double smem[];
-  double* sbox = smem;                       // G::BOX doubles
-  double* stage = smem + G::BOX;             // [2][3][CELLS]
-  __shared__ __align__(8) uint64_t bar;
-  __shared__ double red[THREADS / 32];
-
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  const int s = blockIdx.x;
-  const int g = DEV_IDS ? (dev_ids ? dev_ids[s] : s) : team.id[s];
-  if (threadIdx.x == 0) {
-    mbar_init(&bar, 1);
-    mbar_expect_tx(&bar, G::BOX * (uint32_t)sizeof(double));
-    tma_load_box(sbox, &tmap, 0, 1, 1, g, &bar);
-  }
-  __syncthreads();
-  mbar_wait(&bar, 0);
-  const int64_t slot = out_mode ? (int64_t)g : (int64_t)s;
-  double* outs[3] = {um + slot * 3 * CELLS, up + slot * 3 * CELLS,
-                     F + slot * 3 * CELLS};
-  const double av[3] = {ax, ay, az};
-  const int stv[3] = {B * BZ, BZ, 1};
-  double speed = 0.0;
-#pragma unroll 1
-  for (int axis = 0; axis < 3; ++axis) {
-    double* st_buf = stage + (axis & 1) * 3 * CELLS;
-    if (axis == 2) {
-      // buffer 0 is reused: its bulk stores (axis 0) must have read it
-      if (threadIdx.x == 0)
-        asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-      __syncthreads();
-    }
-    const int st = stv[axis];
-    const double a = av[axis];
-    for (int p = threadIdx.x; p < PAIRS; p += THREADS) {
-      const int ci = p / (C * HP);
-      const int cj = (p / HP) % C;
-      const int ck = 2 * (p % HP);
-      const int c = (ci * C + cj) * C + ck;
-      const int b = ((ci + 1) * B + (cj + 1)) * BZ + (ck + 2);
-      const int pos0 = axis == 0 ? ci : (axis == 1 ? cj : ck);
-      const int pos1 = axis == 2 ? ck + 1 : pos0;
-      const Faces r0 = cell_axis(sbox, b, st, pos0, C, a, 0, flux_form);
-      const Faces r1 = cell_axis(sbox, b + 1, st, pos1, C, a, 0, flux_form);
-      *reinterpret_cast<double2*>(st_buf + c) = make_double2(r0.vm, r1.vm);
-      *reinterpret_cast<double2*>(st_buf + CELLS + c) =
-          make_double2(r0.vp, r1.vp);
-      *reinterpret_cast<double2*>(st_buf + 2 * CELLS + c) =
-          make_double2(r0.f, r1.f);
-      speed = fmax(speed, fabs(a));
-    }
-    // make the generic-proxy smem writes visible to the bulk-copy engine
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      for (int k = 0; k < 3; ++k)
-        bulk_store(outs[k] + axis * CELLS, st_buf + k * CELLS,
-                   CELLS * (uint32_t)sizeof(double));
-      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-    }
-  }
-  if (amax != nullptr) block_max_store<THREADS>(speed, red, amax + slot);
-  // shared memory must outlive the bulk stores' reads
-  if (threadIdx.x == 0)
-    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-}
-
-// Persistent variant for large aggregated launches (T >> #SMs): a grid of
-// resident CTAs walks the slices with a static stride (the host sizes the
-// grid so every CTA gets the same count, +-1) and double-buffers the TMA
-// stencil boxes: slice j+2's load is in flight while slice j is computed
-// and stored.  One block barrier per slice.
-template <int N, int THREADS, int MODE, int VAR>
-__global__ void __launch_bounds__(THREADS, recon_min_blocks<THREADS, VAR>())
-    k_recon_flux_persistent(const __grid_constant__ CUtensorMap tmap,
-                            const int32_t* __restrict__ dev_ids, int T,
-                            int out_mode, double ax, double ay, double az,
-                            double* __restrict__ um, double* __restrict__ up,
-                            double* __restrict__ F, double* __restrict__ amax,
-                            int flux_form) {
-  using G = Geo<N>;
-  constexpr int CELLS = G::CELLS;
-  extern __shared__ __align__(128) double sbuf[];  // 2 boxes
-  __shared__ __align__(8) uint64_t bar[2];
-  __shared__ double red[THREADS / 32];
-  const int stride = gridDim.x;
-  if (threadIdx.x == 0) {
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
-    for (int k = 0; k < 2; ++k) {
-      const int s = blockIdx.x + k * stride;
-      if (s < T) {
-        mbar_expect_tx(&bar[k], G::BOX * (uint32_t)sizeof(double));
-        tma_load_box(sbuf + k * G::BOX, &tmap, 0, 1, 1,
-                     dev_ids ? dev_ids[s] : s, &bar[k]);
-      }
-    }
-  }
-  __syncthreads();
-  int j = 0;
-  for (int s = blockIdx.x; s < T; s += stride, ++j) {
-    const int k = j & 1;
-    const int g = dev_ids ? dev_ids[s] : s;
-    mbar_wait(&bar[k], (j >> 1) & 1);
-    const int64_t slot = out_mode ? (int64_t)g : (int64_t)s;
-    const double speed = slice_compute<N, THREADS, MODE,
-                                       ReconShape<N, VAR>::pair>(
-        sbuf + k * G::BOX, um + slot * 3 * CELLS, up + slot * 3 * CELLS,
-        MODE == 0 ? F + slot * 3 * CELLS : nullptr, ax, ay, az, flux_form);
-    if (MODE == 0 && amax != nullptr)
-      block_max_store<THREADS>(speed, red, amax + slot);
-    __syncthreads();  // every thread is done with buffer k
-    const int s2 = s + 2 * stride;
-    if (threadIdx.x == 0 && s2 < T) {
-      mbar_expect_tx(&bar[k], G::BOX * (uint32_t)sizeof(double));
-      tma_load_box(sbuf + k * G::BOX, &tmap, 0, 1, 1,
-                   dev_ids ? dev_ids[s2] : s2, &bar[k]);
-    }
-  }
 }
 
 // flux_body alone (kernels.py:84-93), elementwise over (slot, axis, cell).
@@ -633,17 +474,12 @@ constexpr int recon_threads() {
 
 template <int N, int MODE, bool DEV_IDS>
 int launch_recon(const CUtensorMap& map, const int32_t* dev_ids,
-                 const TeamIds& team, int T, int out_mode, double ax, double ay,
-                 double az, double* um, double* up, double* F, double* amax,
-                 int flux_form, cudaStream_t st, int flags);
-
-template <int N, int MODE, bool DEV_IDS, int VAR, int TH = recon_threads<N>()>
-int launch_recon_var(const CUtensorMap& map, const int32_t* dev_ids,
                      const TeamIds& team, int T, int out_mode, double ax,
                      double ay, double az, double* um, double* up, double* F,
                      double* amax, int flux_form, cudaStream_t st, int flags) {
+  constexpr int TH = recon_threads<N>();
   constexpr size_t smem = Geo<N>::BOX * sizeof(double);
-  auto kern = k_recon_flux<N, TH, MODE, DEV_IDS, VAR>;
+  auto kern = k_recon_flux<N, TH, MODE, DEV_IDS>;
   static bool attr_done = false;  // benign race: idempotent attribute set
   if (!attr_done) {
     cudaError_t e = cudaFuncSetAttribute(
@@ -668,118 +504,6 @@ int launch_recon_var(const CUtensorMap& map, const int32_t* dev_ids,
                             az, um, up, F, amax, flux_form);
 }
 
-template <int N, int MODE, bool DEV_IDS>
-int launch_recon(const CUtensorMap& map, const int32_t* dev_ids,
-                 const TeamIds& team, int T, int out_mode, double ax, double ay,
-                 double az, double* um, double* up, double* F, double* amax,
-                 int flux_form, cudaStream_t st, int flags) {
-  // TASKFUSE_RECON_VARIANT selects the code shape (A/B measurements only)
-  static const int var = [] {
-    const char* v = getenv("TASKFUSE_RECON_VARIANT");
-    return v ? atoi(v) : 2;
-  }();
-  static const int threads = [] {
-    const char* v = getenv("TASKFUSE_RECON_THREADS");
-    return v ? atoi(v) : 0;
-  }();
-#define TF_RECON_CASE(V, TH_)                                               \
-  if (N == 8 && var == V && threads == TH_)                                 \
-    return launch_recon_var<N, MODE, DEV_IDS, V, TH_>(                      \
-        map, dev_ids, team, T, out_mode, ax, ay, az, um, up, F, amax,       \
-        flux_form, st, flags);
-  TF_RECON_CASE(0, 256)
-  TF_RECON_CASE(2, 256)
-  TF_RECON_CASE(4, 256)
-  TF_RECON_CASE(5, 256)
-  TF_RECON_CASE(4, 512)
-  TF_RECON_CASE(5, 512)
-  TF_RECON_CASE(0, 512)
-#undef TF_RECON_CASE
-  if (var == 3 && N == 8 && MODE == 0) {
-    constexpr size_t smem = (Geo<8>::BOX + 6 * Geo<8>::CELLS) * sizeof(double);
-    auto kern = k_recon_flux_bulkstore<DEV_IDS>;
-    static bool attr_done = false;
-    if (!attr_done) {
-      cudaError_t e = cudaFuncSetAttribute(
-          kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      if (e != cudaSuccess) return e;
-      attr_done = true;
-    }
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)T);
-    cfg.blockDim = dim3(256);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = (flags & TF_LAUNCH_OVERLAP_PREV) ? 1 : 0;
-    return cudaLaunchKernelEx(&cfg, kern, map, dev_ids, team, out_mode, ax,
-                              ay, az, um, up, F, amax, flux_form);
-  }
-  if (var == 1)
-    return launch_recon_var<N, MODE, DEV_IDS, 1>(map, dev_ids, team, T,
-                                                 out_mode, ax, ay, az, um, up,
-                                                 F, amax, flux_form, st, flags);
-  if (var == 2)
-    return launch_recon_var<N, MODE, DEV_IDS, 2>(map, dev_ids, team, T,
-                                                 out_mode, ax, ay, az, um, up,
-                                                 F, amax, flux_form, st, flags);
-  return launch_recon_var<N, MODE, DEV_IDS, 0>(map, dev_ids, team, T, out_mode,
-                                               ax, ay, az, um, up, F, amax,
-                                               flux_form, st, flags);
-}
-
-template <int N, int MODE, int VAR>
-int launch_recon_persistent_var(const CUtensorMap& map, const int32_t* dev_ids,
-                                int T, int out_mode, double ax, double ay,
-                                double az, double* um, double* up, double* F,
-                                double* amax, int flux_form, cudaStream_t st) {
-  constexpr int TH = recon_threads<N>();
-  constexpr size_t smem = 2 * Geo<N>::BOX * sizeof(double);
-  auto kern = k_recon_flux_persistent<N, TH, MODE, VAR>;
-  static int resident = 0;  // CTAs per SM (benign race: idempotent)
-  static int sms = 0;
-  if (!resident) {
-    cudaError_t e = cudaFuncSetAttribute(
-        kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, kern, TH,
-                                                      smem);
-    if (e != cudaSuccess) return e;
-    if (resident < 1) resident = 1;
-  }
-  // equal slices per CTA: waves = ceil(T / resident grid), grid = ceil(T/waves)
-  const int max_grid = sms * resident;
-  const int waves = (T + max_grid - 1) / max_grid;
-  const int grid = (T + waves - 1) / waves;
-  kern<<<grid, TH, smem, st>>>(map, dev_ids, T, out_mode, ax, ay, az, um, up,
-                               F, amax, flux_form);
-  return cudaGetLastError();
-}
-
-template <int N, int MODE>
-int launch_recon_persistent(const CUtensorMap& map, const int32_t* dev_ids,
-                            int T, int out_mode, double ax, double ay,
-                            double az, double* um, double* up, double* F,
-                            double* amax, int flux_form, cudaStream_t st) {
-  static const int var = [] {
-    const char* v = getenv("TASKFUSE_RECON_VARIANT");
-    return v ? atoi(v) : 2;
-  }();
-  if (var == 0)
-    return launch_recon_persistent_var<N, MODE, 0>(map, dev_ids, T, out_mode,
-                                                   ax, ay, az, um, up, F, amax,
-                                                   flux_form, st);
-  return launch_recon_persistent_var<N, MODE, 2>(map, dev_ids, T, out_mode, ax,
-                                                 ay, az, um, up, F, amax,
-                                                 flux_form, st);
-}
-
 template <int MODE, bool DEV_IDS>
 int dispatch_recon(const double* pool, int64_t slices, const int32_t* dev_ids,
                    const TeamIds& team, int T, int n, int out_mode, double ax,
@@ -790,22 +514,6 @@ int dispatch_recon(const double* pool, int64_t slices, const int32_t* dev_ids,
   CUtensorMap map;
   int rc = pool_map(pool, slices, n, &map);
   if (rc) return rc;
-  // The persistent double-buffered kernel is opt-in (TASKFUSE_PERSISTENT=1
-  // for launches of > 296 slices, =2 always): measured on B200 it reaches
-  // 75% of HBM vs 85% for one CTA per slice.
-  static const int policy = [] {
-    const char* v = getenv("TASKFUSE_PERSISTENT");
-    return v ? atoi(v) : 0;
-  }();
-  if (DEV_IDS && (policy == 2 || (policy == 1 && T > 2 * 148))) {
-    if (n == 8)
-      return launch_recon_persistent<8, MODE>(map, dev_ids, T, out_mode, ax,
-                                              ay, az, um, up, F, amax,
-                                              flux_form, st);
-    return launch_recon_persistent<16, MODE>(map, dev_ids, T, out_mode, ax, ay,
-                                             az, um, up, F, amax, flux_form,
-                                             st);
-  }
   if (n == 8)
     return launch_recon<8, MODE, DEV_IDS>(map, dev_ids, team, T, out_mode, ax,
                                           ay, az, um, up, F, amax, flux_form,
@@ -909,7 +617,7 @@ __device__ void queue_fetcher(const int* __restrict__ ring_h, QueueCtl* ctl,
 }
 
 template <int N, int THREADS>
-__global__ void __launch_bounds__(THREADS, recon_min_blocks<THREADS, 2>())
+__global__ void __launch_bounds__(THREADS, recon_min_blocks<THREADS>())
     k_queue_consumer(const __grid_constant__ CUtensorMap tmap,
                      const int* __restrict__ ring_h, QueueCtl* ctl,
                      int* __restrict__ ring_d, QueueDev* qd, double ax,

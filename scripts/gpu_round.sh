@@ -11,4 +11,5 @@ timeout 900 python bench.py --workload cfg5 --steps 10 --warmup 3 > gpurun_out/b
 echo done
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_recon_flux -s 40 -c 1 -o gpurun_out/prof_team python bench.py --profile-only --steps 3 --warmup 3 > gpurun_out/ncu_team.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_step_fused -s 3 -c 1 -o gpurun_out/prof_fused python bench.py --workload cfg5 --cfg5-grid 256 --steps 2 --warmup 3 > gpurun_out/ncu_fused.log 2>&1
+timeout 120 python scripts/probe_pcie.py > gpurun_out/pcie.log 2>&1
 echo done2
