@@ -195,11 +195,13 @@ class Workload:
         torch.cuda.synchronize()
 
 
-def plan_runner(wl, max_team, executors, parents=None, overlap=True):
+def plan_runner(wl, max_team, executors, parents=None, overlap=True,
+                team_buffers=False):
     from paper_2210_06438_b200.strategy3 import TeamPlan, form_teams
     teams = form_teams(range(wl.S), max_team, executors, parents)
     plans = [TeamPlan(teams, p, wl.n, VELOCITY, wl.um, wl.up, wl.F,
-                      executors, amax=wl.amax, overlap=overlap)
+                      executors, amax=wl.amax, overlap=overlap,
+                      team_buffers=team_buffers)
              for p in wl.pools]
     hist = {}
     for t in teams:
@@ -245,7 +247,8 @@ def run_sweep(wl, args, world, stream, peak):
            "strategy1": {}}
     ks, kw = max(5, args.steps // 2), 3
     for A in (1, 4, 16, 64, 128):
-        step, nk, hist, _ = plan_runner(wl, A, args.executors)
+        step, nk, hist, _ = plan_runner(wl, A, args.executors,
+                                        team_buffers=args.outputs == "team")
         ms = timed(step, ks, kw, world, stream)
         out["aggregation"][A] = {
             "cell_updates_per_s": rate(wl.S, wl.n, ms), "ms_per_iter": ms,
@@ -513,10 +516,16 @@ def main():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--max-team", type=int, default=128)
-    ap.add_argument("--executors", type=int, default=4)
+    # one executor = the paper's strategy-3 configuration (all parents on one
+    # stream); with PDL between consecutive teams it is also the fastest
+    ap.add_argument("--executors", type=int, default=1)
     ap.add_argument("--mode", choices=("plan", "realtime", "single"),
                     default="plan")
     ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--outputs", choices=("team", "subgrid"), default="team",
+                    help="team: each team writes its lease of the packed team "
+                         "buffers (the reference's slice_alloc layout); "
+                         "subgrid: per-sub-grid scratch slots")
     ap.add_argument("--no-overlap", action="store_true",
                     help="disable PDL overlap of consecutive team launches")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -548,7 +557,8 @@ def main():
     wl = Workload()
     if args.mode == "plan":
         step, nk, hist, _ = plan_runner(wl, args.max_team, args.executors,
-                                        overlap=not args.no_overlap)
+                                        overlap=not args.no_overlap,
+                                        team_buffers=args.outputs == "team")
         launches_per_step = nk
     elif args.mode == "realtime":
         step, launches, _ = realtime_runner(wl, args.max_team, args.executors)
@@ -589,6 +599,8 @@ def main():
             "subgrids_per_gpu": wl.S, "subgrid_n": wl.n, "grid": GRID,
             "max_team": args.max_team, "executors": args.executors,
             "mode": args.mode, "team_histogram": hist,
+            "outputs": ("packed team leases (slice_alloc layout)"
+                        if args.outputs == "team" else "per-sub-grid slots"),
             "parallelism": f"sub-grid partition x{world} (no collective)",
             "l2": "two input pools alternate; per-step working set "
                   f"{(bytes_step + wl.S * 8 * 2744) / 1e6:.0f} MB vs 126 MB L2"},

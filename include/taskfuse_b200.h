@@ -233,7 +233,11 @@ typedef struct tf_plan tf_plan;
 
 /* Capture one iteration's formed teams (flat ids, team_offsets[nteams+1],
  * executor per team) as a CUDA graph: one tf_recon_flux_team_f64 node per
- * team on its executor's branch, outputs per sub-grid (out_mode 1).        */
+ * team on its executor's branch.  Outputs per sub-grid id (out_mode 1), or
+ * with TF_PLAN_TEAM_BUFFERS in flags into the iteration's packed team
+ * buffers: team t's slice s at flat index team_offsets[t] + s — the
+ * reference's slice_alloc lease layout (aggregator.py:121-128).            */
+#define TF_PLAN_TEAM_BUFFERS 2
 int tf_plan_capture_recon_flux(const int32_t* ids, const int64_t* team_offsets,
                                const int32_t* team_executor, int64_t nteams,
                                int32_t executors, const double* pool_ext,

@@ -25,6 +25,7 @@ TF_E_INVALID = 1001
 TF_E_NO_TMA = 1002
 MAX_TEAM = 128
 TF_LAUNCH_OVERLAP_PREV = 1
+TF_PLAN_TEAM_BUFFERS = 2
 
 
 class EnterResult(C.Structure):

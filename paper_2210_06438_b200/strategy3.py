@@ -147,7 +147,10 @@ class TeamPlan:
     """One iteration's teams captured as a CUDA graph (tf_plan)."""
 
     def __init__(self, teams, pool, n, velocity, um, up, F, executors,
-                 amax=None, flux_form=0, overlap=True):
+                 amax=None, flux_form=0, overlap=True, team_buffers=False):
+        """team_buffers: write each team's outputs into its lease of the
+        iteration's packed team buffers (slot = flat slice index in closure
+        order, `self.order`) instead of per-sub-grid slots."""
         self.lib = _lib.load()
         ids = np.concatenate([np.asarray(t.ids, dtype=np.int32)
                               for t in teams]) if teams else \
@@ -170,8 +173,11 @@ class TeamPlan:
             exe.ctypes.data_as(C.POINTER(C.c_int32)), len(teams), executors,
             pool.data_ptr(), S, n, ax, ay, az, um.data_ptr(), up.data_ptr(),
             F.data_ptr(), None if amax is None else amax.data_ptr(),
-            int(flux_form), _lib.TF_LAUNCH_OVERLAP_PREV if overlap else 0,
+            int(flux_form),
+            (_lib.TF_LAUNCH_OVERLAP_PREV if overlap else 0)
+            | (_lib.TF_PLAN_TEAM_BUFFERS if team_buffers else 0),
             C.byref(h))
+        self.order = ids      # flat slice index -> sub-grid id
         _lib.check(rc, "tf_plan_capture_recon_flux")
         self.handle = h
         self.kernels = self.lib.tf_plan_kernels(h)

@@ -64,6 +64,27 @@ def test_team_plan_bit_exact(cuda, cfg2, A, E):
     assert bool((amax == 1.0).all())
 
 
+@pytest.mark.parametrize("A,E", [(16, 4), (128, 4)])
+def test_team_plan_team_buffers(cuda, cfg2, A, E):
+    """Outputs into the packed team leases: flat slot k holds sub-grid
+    plan.order[k] (the reference's slice_alloc layout)."""
+    import torch
+    from paper_2210_06438_b200.strategy3 import TeamPlan, form_teams
+    pool, n, vel, oum, oup, oF = cfg2
+    S = pool.shape[0]
+    um, up, F = _outs(S, n, cuda)
+    amax = torch.full((S,), float("nan"), dtype=torch.float64, device=cuda)
+    plan = TeamPlan(form_teams(range(S), A, E), pool, n, vel, um, up, F, E,
+                    amax=amax, team_buffers=True)
+    plan.launch()
+    torch.cuda.synchronize()
+    order = np.asarray(plan.order)
+    assert sorted(order.tolist()) == list(range(S))
+    assert np.array_equal(F.cpu().numpy(), oF[order])
+    assert np.array_equal(um.cpu().numpy(), oum[order])
+    assert bool((amax == 1.0).all())
+
+
 @pytest.mark.parametrize("A", [1, 16, 128])
 def test_queue_executor_bit_exact(cuda, cfg2, A):
     """Device-queue strategy 3: every arrival published exactly once, the
