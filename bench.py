@@ -243,17 +243,19 @@ def rate(S, n, ms):
 def run_sweep(wl, args, world, stream, peak):
     """Aggregation sweep 1..128 (plan-graph and real-time executor),
     strategy 2 (A=1 over many streams), strategy 1 (16^3, A=1)."""
-    out = {"aggregation": {}, "realtime": {}, "strategy2": {},
-           "strategy1": {}}
+    out = {"aggregation": {}, "aggregation_4_executors": {}, "realtime": {},
+           "strategy2": {}, "strategy1": {}}
     ks, kw = max(5, args.steps // 2), 3
     for A in (1, 4, 16, 64, 128):
-        step, nk, hist, _ = plan_runner(wl, A, args.executors,
-                                        team_buffers=args.outputs == "team")
-        ms = timed(step, ks, kw, world, stream)
-        out["aggregation"][A] = {
-            "cell_updates_per_s": rate(wl.S, wl.n, ms), "ms_per_iter": ms,
-            "launches": nk, "hbm_frac": wl.S * b_alg(wl.n) / (ms * 1e-3)
-            / (peak * 1e9)}
+        for key, E in (("aggregation", args.executors),
+                       ("aggregation_4_executors", 4)):
+            step, nk, hist, _ = plan_runner(
+                wl, A, E, team_buffers=args.outputs == "team")
+            ms = timed(step, ks, kw, world, stream)
+            out[key][A] = {
+                "cell_updates_per_s": rate(wl.S, wl.n, ms), "ms_per_iter": ms,
+                "launches": nk, "executors": E,
+                "hbm_frac": wl.S * b_alg(wl.n) / (ms * 1e-3) / (peak * 1e9)}
         rstep, launches, ex = realtime_runner(wl, A, args.executors)
         ms = timed(rstep, ks, kw, world, stream)
         st = ex.stats()
@@ -286,10 +288,10 @@ def run_sweep(wl, args, world, stream, peak):
         out["strategy2"][E] = {"cell_updates_per_s": rate(wl.S, wl.n, ms),
                                "ms_per_iter": ms, "launches": nk}
     wl16 = Workload(n=16, grid=wl.grid, field=FIELD)
-    for A in (1,):
-        step, nk, _, _ = plan_runner(wl16, A, args.executors)
+    for E in sorted({args.executors, 4}):
+        step, nk, _, _ = plan_runner(wl16, 1, E)
         ms = timed(step, ks, kw, world, stream)
-        out["strategy1"][f"16^3_A{A}"] = {
+        out["strategy1"][f"16^3_A1_E{E}"] = {
             "cell_updates_per_s": rate(wl16.S, 16, ms), "ms_per_iter": ms,
             "launches": nk, "hbm_frac": wl16.S * b_alg(16) / (ms * 1e-3)
             / (peak * 1e9)}
