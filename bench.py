@@ -55,6 +55,30 @@ def b_step(n: int) -> int:
     return 8 * (c ** 3 + 6 * c ** 2 + n ** 3)
 
 
+def ncu_traffic_per_launch(team: int):
+    """DRAM bytes (read + write) per team launch of T slices, from the
+    committed ncu capture of the recon+flux kernel (one launch over 4096
+    slices; writes still resident in L2 at kernel end are not counted)."""
+    path = os.path.join(ROOT, "profiles", "r01_ncu_recon_flux_single.txt")
+    try:
+        vals = {}
+        with open(path) as fh:
+            for line in fh:
+                parts = line.split()
+                if len(parts) >= 2 and parts[0] in (
+                        "dram__bytes_read.sum", "dram__bytes_write.sum",
+                        "launch__grid_size"):
+                    scale = {"Mbyte": 1e6, "Gbyte": 1e9, "Kbyte": 1e3,
+                             "byte": 1.0}.get(parts[2] if len(parts) > 2
+                                              else "", 1.0)
+                    vals[parts[0]] = float(parts[1]) * scale
+        per_slice = (vals["dram__bytes_read.sum"]
+                     + vals["dram__bytes_write.sum"]) / vals["launch__grid_size"]
+        return per_slice * team
+    except (OSError, KeyError, ValueError):
+        return None
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -610,10 +634,15 @@ def main():
         "roofline": {
             "bound": "hbm", "achieved": achieved, "peak": peak,
             "unit": "GB/s", "frac": achieved / peak, "peak_source": peak_src,
-            "traffic": None,
+            "traffic": ncu_traffic_per_launch(args.max_team),
+            "alg_bytes_per_launch": b_alg(wl.n) * args.max_team,
             "per_subgrid_alg_bytes": b_alg(wl.n),
             "note": "achieved = algorithmic bytes of the whole step / step "
-                    "time (all launches are the recon+flux kernel)",
+                    "time (every launch in the step is the recon+flux team "
+                    "kernel); traffic = dram read+write per team launch from "
+                    "the committed ncu --set full capture of the same kernel "
+                    "(profiles/r01_ncu_recon_flux_single.txt), per slice x "
+                    "team size",
             "kernel_alone": {
                 "ms": ms_single,
                 "achieved": bytes_step / (ms_single * 1e-3) / 1e9,
