@@ -84,6 +84,17 @@ int tf_recon_flux_team_ex_f64(const double* pool_ext, int64_t pool_slices,
                               int32_t flux_form, int32_t flags,
                               tf_stream_t stream);
 
+/* PPM variant (north_star's "batched PPM reconstruction"; Colella-Woodward
+ * 1984 with CW84 limiting) of tf_recon_flux_f64, same arguments and layout.
+ * The reference has no PPM (its scheme is minmod): parity is
+ * against oracle/ppm_oracle.py and is UNPINNED.                            */
+int tf_recon_flux_ppm_f64(const double* pool_ext, int64_t pool_slices,
+                          const int32_t* ids, int32_t T, int32_t n,
+                          double ax, double ay, double az,
+                          double* um, double* up, double* F, int32_t out_mode,
+                          double* amax, int32_t flux_form,
+                          tf_stream_t stream);
+
 /* reconstruct_body alone (kernels.py:73-81): w = pool_ext[ids[s]].          */
 int tf_reconstruct_f64(const double* pool_ext, int64_t pool_slices,
                        const int32_t* ids, int32_t T, int32_t n,

@@ -45,6 +45,9 @@ SIGNATURES = {
     "tf_recon_flux_team_ex_f64": (C.c_int, [_p, _i64, _pi32, _i32, _i32, _f64,
                                             _f64, _f64, _p, _p, _p, _i32, _p,
                                             _i32, _i32, _p]),
+    "tf_recon_flux_ppm_f64": (C.c_int, [_p, _i64, _p, _i32, _i32, _f64, _f64,
+                                        _f64, _p, _p, _p, _i32, _p, _i32,
+                                        _p]),
     "tf_reconstruct_f64": (C.c_int, [_p, _i64, _p, _i32, _i32, _p, _p, _i32,
                                      _p]),
     "tf_flux_f64": (C.c_int, [_p, _i32, _i32, _f64, _f64, _f64, _p, _p, _p,

@@ -272,6 +272,112 @@ __global__ void __launch_bounds__(THREADS, recon_min_blocks<THREADS>())
   if (MODE == 0 && amax != nullptr) block_max_store<THREADS>(speed, red, amax + slot);
 }
 
+// ------------------------------------------------ PPM reconstruction
+// Piecewise-parabolic reconstruction (Colella & Woodward 1984), the scheme
+// north_star names for Octo-Tiger; the reference artifact has no PPM
+// (SURVEY F1), so parity is against the self-written oracle/ppm_oracle.py
+// (UNPINNED), whose operation order this follows exactly.
+// numpy maximum/minimum semantics: first operand on ties, NaN propagates.
+__device__ __forceinline__ double np_max(double a, double b) {
+  return (a >= b || a != a) ? a : b;
+}
+__device__ __forceinline__ double np_min(double a, double b) {
+  return (a <= b || a != a) ? a : b;
+}
+// clipped 4th-order interface value between cells b and b+st
+__device__ __forceinline__ double ppm_interface(const double* __restrict__ s,
+                                                int b, int st) {
+  const double u0 = s[b], u1 = s[b + st];
+  const double a = __dsub_rn(__dmul_rn(7.0 / 12.0, __dadd_rn(u0, u1)),
+                             __dmul_rn(1.0 / 12.0,
+                                       __dadd_rn(s[b - st], s[b + 2 * st])));
+  return np_min(np_max(a, np_min(u0, u1)), np_max(u0, u1));
+}
+// CW84-limited left/right states of the cell at b along st
+__device__ __forceinline__ void ppm_states(const double* __restrict__ s, int b,
+                                           int st, double& ul, double& ur) {
+  const double u = s[b];
+  const double l = ppm_interface(s, b - st, st);
+  const double r = ppm_interface(s, b, st);
+  const double dq = __dsub_rn(r, l);
+  const double mid = __dsub_rn(u, __dmul_rn(0.5, __dadd_rn(l, r)));
+  const bool flat = __dmul_rn(__dsub_rn(r, u), __dsub_rn(u, l)) <= 0.0;
+  const double lhs = __dmul_rn(dq, mid);
+  const double rhs = __dmul_rn(__dmul_rn(dq, dq), 1.0 / 6.0);
+  const bool over_l = lhs > rhs;
+  const bool over_r = lhs < -rhs;
+  ul = flat ? u : (over_l ? __dsub_rn(__dmul_rn(3.0, u), __dmul_rn(2.0, r)) : l);
+  ur = flat ? u
+            : ((!over_l && over_r)
+                   ? __dsub_rn(__dmul_rn(3.0, u), __dmul_rn(2.0, l))
+                   : r);
+}
+
+// Batched PPM reconstruct + (upwind | KT) flux, one CTA per slice, the whole
+// ghosted sub-grid staged by one TMA box load.
+template <int N, int THREADS, bool DEV_IDS>
+__global__ void __launch_bounds__(THREADS)
+    k_recon_flux_ppm(const __grid_constant__ CUtensorMap tmap,
+                     const int32_t* __restrict__ dev_ids, int out_mode,
+                     double ax, double ay, double az, double* __restrict__ um,
+                     double* __restrict__ up, double* __restrict__ F,
+                     double* __restrict__ amax, int flux_form) {
+  using G = Geo<N>;
+  constexpr int C = G::C, E = G::E, CELLS = G::CELLS;
+  extern __shared__ __align__(128) double sbox[];  // E^3
+  __shared__ __align__(8) uint64_t bar;
+  __shared__ double red[THREADS / 32];
+  const int s = blockIdx.x;
+  const int g = dev_ids ? dev_ids[s] : s;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    mbar_expect_tx(&bar, G::EXT3 * (uint32_t)sizeof(double));
+    tma_load_box(sbox, &tmap, 0, 0, 0, g, &bar);
+  }
+  __syncthreads();
+  mbar_wait(&bar, 0);
+  const int64_t slot = out_mode ? (int64_t)g : (int64_t)s;
+  double* um_s = um + slot * 3 * CELLS;
+  double* up_s = up + slot * 3 * CELLS;
+  double* F_s = F + slot * 3 * CELLS;
+  const double av[3] = {ax, ay, az};
+  const int stv[3] = {E * E, E, 1};
+  double speed = 0.0;
+  for (int c = threadIdx.x; c < CELLS; c += THREADS) {
+    const int ci = c / (C * C), cj = (c / C) % C, ck = c % C;
+    const int cv[3] = {ci, cj, ck};
+    // cube c = extended index c + 2 in every axis
+    const int b = ((ci + 2) * E + (cj + 2)) * E + (ck + 2);
+#pragma unroll
+    for (int axis = 0; axis < 3; ++axis) {
+      const int st = stv[axis];
+      const double a = av[axis];
+      double ul, ur;
+      ppm_states(sbox, b, st, ul, ur);
+      __stcs(um_s + axis * CELLS + c, ul);
+      __stcs(up_s + axis * CELLS + c, ur);
+      double next_l = 0.0;
+      if (a < 0.0 || flux_form == 1) {
+        // np.roll(um, -1): the last layer wraps onto layer 0
+        const int bn = cv[axis] == C - 1 ? b - (C - 1) * st : b + st;
+        double nr;
+        ppm_states(sbox, bn, st, next_l, nr);
+      }
+      double f;
+      if (flux_form == 0) {
+        f = a >= 0.0 ? __dmul_rn(a, ur) : __dmul_rn(a, next_l);
+      } else {
+        const double fl = __dmul_rn(a, ur), fr = __dmul_rn(a, next_l);
+        f = __dsub_rn(__dmul_rn(0.5, __dadd_rn(fl, fr)),
+                      __dmul_rn(__dmul_rn(0.5, fabs(a)), __dsub_rn(next_l, ur)));
+      }
+      __stcs(F_s + axis * CELLS + c, f);
+      speed = fmax(speed, fabs(a));
+    }
+  }
+  if (amax != nullptr) block_max_store<THREADS>(speed, red, amax + slot);
+}
+
 // flux_body alone (kernels.py:84-93), elementwise over (slot, axis, cell).
 template <int N>
 __global__ void __launch_bounds__(256)
@@ -433,11 +539,14 @@ struct MapKeyHash {
   }
 };
 
-// 4-D view (slice, x, y, z) of the pool; box = the (n+4)^3 stencil box.
-int pool_map(const double* pool, int64_t slices, int n, CUtensorMap* out) {
+// 4-D view (slice, x, y, z) of the pool; box = the (n+4)^2 x (n+6) minmod
+// stencil box, or (full) the whole (n+6)^3 ghosted sub-grid (PPM's stencil
+// reaches the ghost depth 3).
+int pool_map(const double* pool, int64_t slices, int n, CUtensorMap* out,
+             bool full = false) {
   static std::mutex mu;
   static std::unordered_map<MapKey, CUtensorMap, MapKeyHash> cache;
-  const MapKey key{pool, slices, n};
+  const MapKey key{pool, slices, full ? -n : n};
   std::lock_guard<std::mutex> lock(mu);
   auto it = cache.find(key);
   if (it != cache.end()) {
@@ -447,7 +556,7 @@ int pool_map(const double* pool, int64_t slices, int n, CUtensorMap* out) {
   auto fn = encode_fn();
   if (!fn) return TF_E_NO_TMA;
   const cuuint64_t E = (cuuint64_t)(n + 6);
-  const cuuint32_t Bx = (cuuint32_t)(n + 4);
+  const cuuint32_t Bx = (cuuint32_t)(full ? n + 6 : n + 4);
   cuuint64_t dims[4] = {E, E, E, (cuuint64_t)slices};
   cuuint64_t strides[3] = {E * 8, E * E * 8, E * E * E * 8};
   cuuint32_t box[4] = {(cuuint32_t)E, Bx, Bx, 1};
@@ -848,6 +957,41 @@ int tf_pool_to_field_f64(const double* pool_ext, int32_t grid_n, int32_t n,
                          double* field, tf_stream_t stream) {
   return field_pool(field, const_cast<double*>(pool_ext), grid_n, n, 1,
                     stream);
+}
+
+int tf_recon_flux_ppm_f64(const double* pool_ext, int64_t pool_slices,
+                          const int32_t* ids, int32_t T, int32_t n, double ax,
+                          double ay, double az, double* um, double* up,
+                          double* F, int32_t out_mode, double* amax,
+                          int32_t flux_form, tf_stream_t stream) {
+  if (!valid_n(n) || T < 0 || !pool_ext || !um || !up || !F ||
+      (flux_form != 0 && flux_form != 1) || pool_slices < 1 ||
+      (ids == nullptr && T > pool_slices))
+    return TF_E_INVALID;
+  if (T == 0) return 0;
+  CUtensorMap map;
+  int rc = pool_map(pool_ext, pool_slices, n, &map, /*full=*/true);
+  if (rc) return rc;
+  constexpr int TH = 512;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (n == 8) {
+    constexpr size_t smem = Geo<8>::EXT3 * sizeof(double);
+    k_recon_flux_ppm<8, TH, true><<<T, TH, smem, st>>>(
+        map, ids, out_mode, ax, ay, az, um, up, F, amax, flux_form);
+  } else {
+    constexpr size_t smem = Geo<16>::EXT3 * sizeof(double);
+    static bool attr = false;
+    if (!attr) {
+      cudaError_t e = cudaFuncSetAttribute(
+          k_recon_flux_ppm<16, TH, true>,
+          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+      attr = true;
+    }
+    k_recon_flux_ppm<16, TH, true><<<T, TH, smem, st>>>(
+        map, ids, out_mode, ax, ay, az, um, up, F, amax, flux_form);
+  }
+  return cudaGetLastError();
 }
 
 int tf_queue_consumer_ctas(int32_t n) {

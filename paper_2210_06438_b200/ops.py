@@ -76,8 +76,15 @@ def _slots(out_mode: int, T: int, pool_slices: int) -> int:
 
 
 def recon_flux(pool, n, velocity, um, up, F, ids=None, T=None, out_mode=1,
-               amax=None, flux_form=0, stream=None) -> None:
-    """Fused reconstruct+flux over T slices (tf_recon_flux_f64)."""
+               amax=None, flux_form=0, stream=None,
+               reconstruction: str = "minmod") -> None:
+    """Fused reconstruct+flux over T slices (tf_recon_flux_f64).
+
+    reconstruction: "minmod" — the reference's scheme (bit-exact, pinned);
+    "ppm" — piecewise-parabolic (tf_recon_flux_ppm_f64; parity unpinned,
+    checked against oracle/ppm_oracle.py)."""
+    if reconstruction not in ("minmod", "ppm"):
+        raise ValidationError(f"unknown reconstruction {reconstruction!r}")
     lib = _lib.load()
     _check_n(n)
     S = _check_pool(pool, n)
@@ -91,12 +98,14 @@ def recon_flux(pool, n, velocity, um, up, F, ids=None, T=None, out_mode=1,
         if amax.numel() < slots:
             raise ValidationError("amax too small")
     ax, ay, az = (float(v) for v in velocity)
-    rc = lib.tf_recon_flux_f64(pool.data_ptr(), S, ptr, T, n, ax, ay, az,
-                               um.data_ptr(), up.data_ptr(), F.data_ptr(),
-                               int(out_mode),
-                               None if amax is None else amax.data_ptr(),
-                               int(flux_form), _stream(stream))
-    _lib.check(rc, "tf_recon_flux_f64")
+    fn = lib.tf_recon_flux_ppm_f64 if reconstruction == "ppm" else \
+        lib.tf_recon_flux_f64
+    rc = fn(pool.data_ptr(), S, ptr, T, n, ax, ay, az, um.data_ptr(),
+            up.data_ptr(), F.data_ptr(), int(out_mode),
+            None if amax is None else amax.data_ptr(), int(flux_form),
+            _stream(stream))
+    _lib.check(rc, "tf_recon_flux_f64" if reconstruction == "minmod"
+               else "tf_recon_flux_ppm_f64")
 
 
 def recon_flux_team(pool, n, velocity, host_ids, um, up, F, out_mode=1,
