@@ -25,6 +25,22 @@ def test_header_symbols_exported(native_lib):
         assert s in _lib.SIGNATURES, f"{s} not bound in _lib.SIGNATURES"
 
 
+def test_no_cpu_fallback():
+    """The product path refuses host tensors instead of computing on the CPU."""
+    import pytest
+    import torch
+    from paper_2210_06438_b200 import ops
+    from paper_2210_06438_b200.errors import TaskfuseCudaError
+    pool = torch.zeros((1, 14, 14, 14), dtype=torch.float64)
+    faces = torch.zeros((1, 3, 10, 10, 10), dtype=torch.float64)
+    with pytest.raises(TaskfuseCudaError, match="CUDA device"):
+        ops.recon_flux(pool, 8, (1, 1, 1), faces, faces, faces)
+    with pytest.raises(TaskfuseCudaError):
+        ops.ghost_fill(pool, 8, 1)
+    with pytest.raises(TaskfuseCudaError):
+        ops.update(pool, 8, faces, 0.3, pool)
+
+
 def test_version(native_lib):
     assert b"sm_100a" in native_lib.tf_version()
 
