@@ -30,6 +30,8 @@ import sys
 import threading
 import time
 
+import numpy as np
+
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
@@ -152,8 +154,17 @@ def dist_setup(gpus: int):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
         import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # one process per GPU; the modulo only matters when a test squeezes
+        # several ranks onto fewer GPUs (TASKFUSE_DIST_BACKEND=gloo)
+        if torch.cuda.is_available():
+            local = local % torch.cuda.device_count()
+            torch.cuda.set_device(local)
+        backend = os.environ.get("TASKFUSE_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group(
+                "nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     elif torch.cuda.is_available():
         torch.cuda.set_device(0)
     return world, rank, local
@@ -170,7 +181,8 @@ def max_over_ranks(world, x: float) -> float:
         return x
     import torch
     import torch.distributed as dist
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -242,7 +254,8 @@ def realtime_runner(wl, max_team, executors, parents=None, overlap=False):
     parents = parents or default_parents(wl.S, max_team)
     ex = RealtimeExecutor("reconstruct", max_team, executors, parents,
                           overlap=overlap)
-    arrivals = list(range(wl.S))
+    # an int32 array, so the per-step C call does not convert a list
+    arrivals = np.arange(wl.S, dtype=np.int32)
     launches = []
 
     def step(k):
@@ -291,7 +304,8 @@ def run_sweep(wl, args, world, stream, peak):
     out["realtime_queue"] = {}
     from paper_2210_06438_b200.strategy3 import (QueueExecutor,
                                                  default_parents)
-    arrivals = list(range(wl.S))
+    # an int32 array, so the per-step C call does not convert a list
+    arrivals = np.arange(wl.S, dtype=np.int32)
     for A in (1, 4, 16, 64, 128):
         q = QueueExecutor("reconstruct", A, default_parents(wl.S, A), wl.n)
         ms = timed(lambda k: q.run(wl.pools[k % len(wl.pools)], VELOCITY,
