@@ -303,6 +303,21 @@ int tf_field_step_f64(const double* padded_in, int32_t X, int32_t Gy,
                       int32_t flags, tf_stream_t stream);
 int tf_field_halo_f64(double* padded, int32_t X, int32_t Gy, int32_t Gz,
                       int32_t periodic_x, tf_stream_t stream);
+/* Multi-GPU fused step + exchange: as tf_field_step_f64 (device ids), and
+ * the slab's 2 lowest / highest owned x layers are ALSO stored into the
+ * ring neighbours' next padded fields (peer_lo = left's, peer_hi = right's,
+ * NVLink peer pointers from CUDA IPC) at their high / low x halo.  Then
+ * tf_peer_barrier publishes `epoch` to both neighbours' flag words
+ * (release, system scope) and waits for theirs (acquire); *err = 1 instead
+ * of hanging if a neighbour does not arrive within timeout_ns.            */
+int tf_field_step_peer_f64(const double* padded_in, int32_t X, int32_t Gy,
+                           int32_t Gz, int32_t n, const int32_t* ids,
+                           int32_t T, double ax, double ay, double az,
+                           double dt_dx, double* padded_out, double* peer_lo,
+                           double* peer_hi, tf_stream_t stream);
+int tf_peer_barrier(long long* my_flags, long long* left_flags,
+                    long long* right_flags, long long epoch,
+                    long long timeout_ns, int* err, tf_stream_t stream);
 /* y/z halos of padded layers [first, first+count) only; the periodic x halo
  * (side 1: low halo <- last owned layers, 2: high <- first, 3: both).
  * Used by the chunked host pipeline (FieldIteration.run_host_pipelined).    */

@@ -98,6 +98,10 @@ SIGNATURES = {
                                     _i32, _f64, _f64, _f64, _f64, _p, _i32,
                                     _p]),
     "tf_field_halo_f64": (C.c_int, [_p, _i32, _i32, _i32, _i32, _p]),
+    "tf_field_step_peer_f64": (C.c_int, [_p, _i32, _i32, _i32, _i32, _p, _i32,
+                                         _f64, _f64, _f64, _f64, _p, _p, _p,
+                                         _p]),
+    "tf_peer_barrier": (C.c_int, [_p, _p, _p, _i64, _i64, _p, _p]),
     "tf_field_halo_layers_f64": (C.c_int, [_p, _i32, _i32, _i32, _i32, _i32,
                                            _p]),
     "tf_field_halo_xwrap_f64": (C.c_int, [_p, _i32, _i32, _i32, _i32, _p]),

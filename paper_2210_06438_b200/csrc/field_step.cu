@@ -104,7 +104,8 @@ __global__ void __launch_bounds__(THREADS)
                  const int32_t* __restrict__ dev_ids,
                  const __grid_constant__ TeamIds team, int m, double ax,
                  double ay, double az, double dt_dx, double* __restrict__ out,
-                 int64_t pyz, int pz) {
+                 int64_t pyz, int pz, double* peer_lo, double* peer_hi, int X,
+                 int mx) {
   using G = FGeo<N>;
   constexpr int BY = G::BY, BZ = G::BZ;
   extern __shared__ __align__(128) double sbox[];
@@ -141,7 +142,16 @@ __global__ void __launch_bounds__(THREADS)
                                    face_flux(sbox, b - 1, 1, az)));
     const int64_t x = (int64_t)bx * N + i + HX, y = (int64_t)by * N + j + HY,
                   z = (int64_t)bz * N + k + HZ;
-    out[x * pyz + y * pz + z] = __dsub_rn(sbox[b], __dmul_rn(dt_dx, div));
+    const double v = __dsub_rn(sbox[b], __dmul_rn(dt_dx, div));
+    out[x * pyz + y * pz + z] = v;
+    // multi-GPU: the slab's two lowest / highest owned x layers are also
+    // the ring neighbours' next-iteration x halo — store them straight into
+    // the neighbours' padded fields over NVLink (peer pointers), so the
+    // exchange rides on the compute instead of following it
+    if (peer_lo != nullptr && bx == 0 && i < HX)
+      peer_lo[((int64_t)X + HX + i) * pyz + y * pz + z] = v;
+    if (peer_hi != nullptr && bx == mx - 1 && i >= N - HX)
+      peer_hi[(int64_t)(i - (N - HX)) * pyz + y * pz + z] = v;
   }
 }
 
@@ -253,7 +263,8 @@ template <int N, bool DEV_IDS>
 int launch_step(const CUtensorMap& map, const int32_t* dev_ids,
                 const TeamIds& team, int T, int m, double ax, double ay,
                 double az, double dt_dx, double* out, int X, int Gy, int Gz,
-                cudaStream_t st, int flags) {
+                cudaStream_t st, int flags, double* peer_lo = nullptr,
+                double* peer_hi = nullptr) {
   // 128 threads per sub-grid: measured best of 128/256/512
   constexpr int TH = 128;
   constexpr size_t smem = FGeo<N>::BOX * sizeof(double);
@@ -276,9 +287,44 @@ int launch_step(const CUtensorMap& map, const int32_t* dev_ids,
   a[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = a;
   cfg.numAttrs = (flags & TF_LAUNCH_OVERLAP_PREV) ? 1 : 0;
-  (void)X;
   return cudaLaunchKernelEx(&cfg, kern, map, dev_ids, team, m, ax, ay, az,
-                            dt_dx, out, pyz, (int)pz);
+                            dt_dx, out, pyz, (int)pz, peer_lo, peer_hi, X,
+                            X / N);
+}
+
+// Peer barrier for the fused multi-GPU iteration: tell both ring
+// neighbours "my epoch-k halo stores into you are done" (release, system
+// scope, after a system fence), then wait until both have told me the same.
+// Flags live in each rank's own device memory; peers write them over
+// NVLink.  Slot 0 = from my left neighbour, slot 1 = from my right.
+__global__ void k_peer_barrier(long long* my_flags, long long* left_flags,
+                               long long* right_flags, long long epoch,
+                               long long timeout_ns, int* err) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  __threadfence_system();
+  asm volatile("st.release.sys.global.b64 [%0], %1;" ::"l"(left_flags + 1),
+               "l"(epoch)
+               : "memory");
+  asm volatile("st.release.sys.global.b64 [%0], %1;" ::"l"(right_flags + 0),
+               "l"(epoch)
+               : "memory");
+  unsigned long long t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (;;) {
+    long long a, b;
+    asm volatile("ld.acquire.sys.global.b64 %0, [%1];" : "=l"(a)
+                 : "l"(my_flags) : "memory");
+    asm volatile("ld.acquire.sys.global.b64 %0, [%1];" : "=l"(b)
+                 : "l"(my_flags + 1) : "memory");
+    if (a >= epoch && b >= epoch) return;
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if ((long long)(t - t0) > timeout_ns) {
+      atomicExch(err, 1);  // a neighbour never arrived: fail, do not hang
+      return;
+    }
+    __nanosleep(256);
+  }
 }
 
 int grid_for(int64_t total) {
@@ -348,6 +394,40 @@ int tf_field_halo_f64(double* padded, int32_t X, int32_t Gy, int32_t Gz,
                           cudaMemcpyDeviceToDevice, st);
     if (e != cudaSuccess) return e;
   }
+  return cudaGetLastError();
+}
+
+int tf_field_step_peer_f64(const double* padded_in, int32_t X, int32_t Gy,
+                           int32_t Gz, int32_t n, const int32_t* ids,
+                           int32_t T, double ax, double ay, double az,
+                           double dt_dx, double* padded_out, double* peer_lo,
+                           double* peer_hi, tf_stream_t stream) {
+  if ((n != 8 && n != 16) || X < n || Gy < n || Gz < n || X % n || Gy % n ||
+      Gz % n || Gy != Gz || !padded_in || !padded_out || T < 0 ||
+      padded_in == padded_out)
+    return TF_E_INVALID;
+  if (T == 0) return 0;
+  const int m = Gy / n;
+  if (!ids && T > (X / n) * m * m) return TF_E_INVALID;
+  CUtensorMap map;
+  int rc = field_map(padded_in, X, Gy, Gz, n, &map);
+  if (rc) return rc;
+  TeamIds team{};
+  cudaStream_t st = (cudaStream_t)stream;
+  return n == 8 ? launch_step<8, true>(map, ids, team, T, m, ax, ay, az, dt_dx,
+                                       padded_out, X, Gy, Gz, st, 0, peer_lo,
+                                       peer_hi)
+                : launch_step<16, true>(map, ids, team, T, m, ax, ay, az,
+                                        dt_dx, padded_out, X, Gy, Gz, st, 0,
+                                        peer_lo, peer_hi);
+}
+
+int tf_peer_barrier(long long* my_flags, long long* left_flags,
+                    long long* right_flags, long long epoch,
+                    long long timeout_ns, int* err, tf_stream_t stream) {
+  if (!my_flags || !left_flags || !right_flags || !err) return TF_E_INVALID;
+  k_peer_barrier<<<1, 32, 0, (cudaStream_t)stream>>>(
+      my_flags, left_flags, right_flags, epoch, timeout_ns, err);
   return cudaGetLastError();
 }
 

@@ -24,7 +24,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from .errors import ValidationError
+from .errors import TaskfuseCudaError, ValidationError
 from .parallel_halo import SlabPartition, exchange_halos
 from .strategy3 import Team, form_teams
 
@@ -290,6 +290,88 @@ class HostPipeline:
 
     def run(self) -> None:
         self.graph.replay()
+
+
+class PeerSlabFieldIteration(_FieldBase):
+    """x-slab rank with the exchange FUSED into the compute: the fused step
+    stores the slab's boundary layers straight into the ring neighbours'
+    next padded fields through CUDA-IPC peer pointers (NVLink on a
+    multi-GPU node), then a device-side peer barrier (release/acquire flags
+    in each rank's memory, written by the neighbours) orders the iterations.
+    No NCCL call and no pack/unpack on the data path; NCCL/gloo is used once,
+    at setup, to swap the IPC handles."""
+
+    def __init__(self, part: SlabPartition, slab_field=None,
+                 velocity=(1.0, 1.0, 1.0), dt_dx=None, device=None,
+                 group=None, timeout_s: float = 10.0):
+        super().__init__(part.mx * part.n, part.grid_n, part.n, velocity,
+                         dt_dx, device)
+        self.part = part
+        self.timeout_ns = int(timeout_s * 1e9)
+        dev = self.device
+        self.flags = torch.zeros(2, dtype=torch.int64, device=dev)
+        self.err = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.epoch = 0
+        if slab_field is not None:
+            if isinstance(slab_field, np.ndarray):
+                slab_field = torch.from_numpy(np.ascontiguousarray(slab_field))
+            self.load(slab_field.to(dev, torch.float64))
+        if part.world == 1:
+            mine = {"P": self.P, "flags": self.flags}
+            self.left = self.right = mine
+        else:
+            import torch.distributed as dist
+            from torch.multiprocessing.reductions import reduce_tensor
+            handles = {"P": [reduce_tensor(p) for p in self.P],
+                       "flags": reduce_tensor(self.flags)}
+            every = [None] * part.world
+            dist.all_gather_object(every, handles, group=group)
+
+            def open_(h):
+                fn, args = h
+                return fn(*args)
+
+            def peer(r):
+                return {"P": [open_(h) for h in every[r]["P"]],
+                        "flags": open_(every[r]["flags"])}
+            self.left = peer(part.left)
+            self.right = self.left if part.right == part.left else \
+                peer(part.right)
+        self._prime()
+
+    def _barrier(self, stream=None) -> None:
+        self.epoch += 1
+        _lib.check(self.lib.tf_peer_barrier(
+            self.flags.data_ptr(), self.left["flags"].data_ptr(),
+            self.right["flags"].data_ptr(), self.epoch, self.timeout_ns,
+            self.err.data_ptr(), self._s(stream)), "tf_peer_barrier")
+
+    def _prime(self) -> None:
+        """Initial x halo of the current field: copy my boundary layers into
+        the neighbours' halos over the peer mapping, then barrier."""
+        X, c = self.X, self.cur
+        self.halo(False)
+        self.left["P"][c][X + HX:X + 2 * HX].copy_(self.P[c][HX:2 * HX])
+        self.right["P"][c][0:HX].copy_(self.P[c][X:X + HX])
+        self._barrier()
+
+    def iteration(self) -> None:
+        cur, nxt = self.cur, 1 - self.cur
+        self.halo(False)          # y/z halos incl. the received x layers
+        ax, ay, az = self.velocity
+        _lib.check(self.lib.tf_field_step_peer_f64(
+            self.P[cur].data_ptr(), self.X, self.G, self.G, self.n, None,
+            self.S, ax, ay, az, self.dt_dx, self.P[nxt].data_ptr(),
+            self.left["P"][nxt].data_ptr(), self.right["P"][nxt].data_ptr(),
+            self._s()), "tf_field_step_peer_f64")
+        self._barrier()
+        self.swap()
+
+    def check(self) -> None:
+        """Raise if a peer barrier timed out."""
+        if int(self.err.item()):
+            raise TaskfuseCudaError("peer barrier timed out: a neighbour "
+                                    "rank did not arrive")
 
 
 class SlabFieldIteration(_FieldBase):

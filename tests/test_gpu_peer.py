@@ -1,0 +1,80 @@
+"""Fused compute + exchange over peer memory (field.PeerSlabFieldIteration):
+the step kernel stores its boundary layers straight into the neighbours'
+padded fields through CUDA-IPC mappings, ordered by a device-side peer
+barrier.  One rank in-process, and two real processes sharing the one GPU
+(IPC within a device, gloo only to swap the handles) — bit-identical to the
+whole-grid reference."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+
+from oracle import hydro_oracle as HO
+
+pytestmark = pytest.mark.gpu
+
+
+def test_peer_single_rank(cuda):
+    import torch
+    from paper_2210_06438_b200.field import PeerSlabFieldIteration
+    from paper_2210_06438_b200.parallel_halo import SlabPartition
+    f = HO.stress_field(64)
+    vel = (-1.0, 0.5, -0.25)
+    r = PeerSlabFieldIteration(SlabPartition(64, 8, 1, 0), f, vel,
+                               device=cuda)
+    for _ in range(3):
+        r.iteration()
+    torch.cuda.synchronize()
+    r.check()
+    assert np.array_equal(r.owned().cpu().numpy(), HO.reference_step(f, vel))
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _rank(rank, world, port, grid, n, vel, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch
+    import torch.distributed as dist
+    from paper_2210_06438_b200.field import PeerSlabFieldIteration
+    from paper_2210_06438_b200.parallel_halo import SlabPartition
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        part = SlabPartition(grid, n, world, rank)
+        f = HO.stress_field(grid)
+        r = PeerSlabFieldIteration(part, part.slab(f), vel,
+                                   device=torch.device("cuda", 0))
+        for _ in range(3):
+            r.iteration()
+        torch.cuda.synchronize()
+        r.check()
+        q.put((rank, r.owned().cpu().numpy()))
+        dist.barrier()   # keep the IPC-shared buffers alive until all read
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_peer_two_processes_one_gpu(cuda, world):
+    import torch.multiprocessing as mp
+    grid, n, vel = 64, 8, (0.7, -1.3, 0.0)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_rank, args=(r, world, port, grid, n, vel, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    got = dict(q.get(timeout=300) for _ in range(world))
+    for p in procs:
+        p.join(timeout=120)
+    assert all(p.exitcode == 0 for p in procs)
+    whole = np.concatenate([got[r] for r in range(world)], axis=0)
+    assert np.array_equal(whole, HO.reference_step(HO.stress_field(grid),
+                                                   vel))
