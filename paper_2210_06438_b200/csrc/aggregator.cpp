@@ -499,8 +499,9 @@ struct QueueDevInit {   // mirrors QueueDev
   unsigned long long done;
 };
 
-struct tf_qexec {
-  tf_region* region = nullptr;
+// One queue instance; runs alternate between two so that run k+1 can
+// publish while run k's consumer grid is still draining its tail.
+struct QueueSlot {
   QueueCtlHost* ctl_h = nullptr;   // mapped pinned
   void* ctl_hd = nullptr;          // its device alias
   int32_t* ring_h = nullptr;       // mapped pinned
@@ -508,19 +509,27 @@ struct tf_qexec {
   int32_t* ring_d = nullptr;       // device mirror
   int64_t ring_cap = 0;
   void* qdev = nullptr;            // QueueDevInit on the device
+  cudaEvent_t done_ev = nullptr;
+  bool in_flight = false;
+};
+
+struct tf_qexec {
+  tf_region* region = nullptr;
+  QueueSlot slots[2];
+  int cur = 1;
   int32_t ctas = 0;
   int32_t n = 0;
   int64_t published = 0;
   int64_t seen_published = 0;
   int64_t busy_until = 0;
-  cudaEvent_t done_ev = nullptr;
-  bool in_flight = false;
+  QueueSlot& slot() { return slots[cur]; }
+  const QueueSlot& slot() const { return slots[cur]; }
 };
 
 namespace {
 
 int64_t q_done(const tf_qexec* q) {
-  return __atomic_load_n(&q->ctl_h->completed, __ATOMIC_ACQUIRE);
+  return __atomic_load_n(&q->slot().ctl_h->completed, __ATOMIC_ACQUIRE);
 }
 
 int q_busy(void* ctx, int32_t) {
@@ -544,9 +553,10 @@ void q_publish(tf_qexec* q, int64_t team) {
   tf_region* r = q->region;
   const Team* t = r->teams.get(team);
   if (!t) return;
-  for (int64_t tag : t->tags) q->ring_h[q->published++] = (int32_t)tag;
+  QueueSlot& S = q->slot();
+  for (int64_t tag : t->tags) S.ring_h[q->published++] = (int32_t)tag;
   // ids first, then the count (release): the consumer acquires the count
-  __atomic_store_n(&q->ctl_h->published, (long long)q->published,
+  __atomic_store_n(&S.ctl_h->published, (long long)q->published,
                    __ATOMIC_RELEASE);
   r->teams.release(team);
 }
@@ -564,13 +574,15 @@ int tf_qexec_create(tf_region* region, int32_t n, tf_qexec** out) {
   q->region = region;
   q->ctas = ctas;
   q->n = n;
-  cudaError_t e = cudaHostAlloc(&q->ctl_h, sizeof(QueueCtlHost),
-                                cudaHostAllocMapped);
-  if (e == cudaSuccess)
-    e = cudaHostGetDevicePointer(&q->ctl_hd, q->ctl_h, 0);
-  if (e == cudaSuccess) e = cudaMalloc(&q->qdev, sizeof(QueueDevInit));
-  if (e == cudaSuccess)
-    e = cudaEventCreateWithFlags(&q->done_ev, cudaEventDisableTiming);
+  cudaError_t e = cudaSuccess;
+  for (QueueSlot& S : q->slots) {
+    if (e == cudaSuccess)
+      e = cudaHostAlloc(&S.ctl_h, sizeof(QueueCtlHost), cudaHostAllocMapped);
+    if (e == cudaSuccess) e = cudaHostGetDevicePointer(&S.ctl_hd, S.ctl_h, 0);
+    if (e == cudaSuccess) e = cudaMalloc(&S.qdev, sizeof(QueueDevInit));
+    if (e == cudaSuccess)
+      e = cudaEventCreateWithFlags(&S.done_ev, cudaEventDisableTiming);
+  }
   if (e != cudaSuccess) {
     tf_qexec_destroy(q);
     return e;
@@ -581,12 +593,14 @@ int tf_qexec_create(tf_region* region, int32_t n, tf_qexec** out) {
 
 void tf_qexec_destroy(tf_qexec* q) {
   if (!q) return;
-  if (q->in_flight) cudaEventSynchronize(q->done_ev);
-  if (q->ctl_h) cudaFreeHost(q->ctl_h);
-  if (q->ring_h) cudaFreeHost(q->ring_h);
-  if (q->ring_d) cudaFree(q->ring_d);
-  if (q->qdev) cudaFree(q->qdev);
-  if (q->done_ev) cudaEventDestroy(q->done_ev);
+  for (QueueSlot& S : q->slots) {
+    if (S.in_flight) cudaEventSynchronize(S.done_ev);
+    if (S.ctl_h) cudaFreeHost(S.ctl_h);
+    if (S.ring_h) cudaFreeHost(S.ring_h);
+    if (S.ring_d) cudaFree(S.ring_d);
+    if (S.qdev) cudaFree(S.qdev);
+    if (S.done_ev) cudaEventDestroy(S.done_ev);
+  }
   delete q;
 }
 
@@ -599,48 +613,52 @@ int tf_qexec_run_recon_flux(tf_qexec* q, const double* pool_ext,
   if (!q || !ids || count < 0 || !teams_published) return TF_E_INVALID;
   for (int64_t i = 0; i < count; ++i)
     if (ids[i] < 0 || ids[i] >= pool_slices) return TF_E_INVALID;
-  // the previous run's consumer must be gone before its counters reset
-  if (q->in_flight) {
-    cudaError_t e = cudaEventSynchronize(q->done_ev);
+  // alternate queue slots: this run publishes while the previous run's
+  // consumer may still drain its tail; the slot's own previous use (two
+  // runs ago) must be gone before its counters reset
+  q->cur ^= 1;
+  QueueSlot& S = q->slot();
+  if (S.in_flight) {
+    cudaError_t e = cudaEventSynchronize(S.done_ev);
     if (e != cudaSuccess) return e;
-    q->in_flight = false;
+    S.in_flight = false;
   }
-  if (count > q->ring_cap || !q->ring_h) {
-    if (q->ring_h) cudaFreeHost(q->ring_h);
-    if (q->ring_d) cudaFree(q->ring_d);
-    q->ring_h = nullptr;
-    q->ring_d = nullptr;
+  if (count > S.ring_cap || !S.ring_h) {
+    if (S.ring_h) cudaFreeHost(S.ring_h);
+    if (S.ring_d) cudaFree(S.ring_d);
+    S.ring_h = nullptr;
+    S.ring_d = nullptr;
     const int64_t cap = count > 0 ? count : 1;
-    cudaError_t e = cudaHostAlloc(&q->ring_h, sizeof(int32_t) * cap,
+    cudaError_t e = cudaHostAlloc(&S.ring_h, sizeof(int32_t) * cap,
                                   cudaHostAllocMapped);
     if (e == cudaSuccess)
-      e = cudaHostGetDevicePointer(reinterpret_cast<void**>(&q->ring_hd),
-                                   q->ring_h, 0);
+      e = cudaHostGetDevicePointer(reinterpret_cast<void**>(&S.ring_hd),
+                                   S.ring_h, 0);
     if (e == cudaSuccess)
-      e = cudaMalloc(reinterpret_cast<void**>(&q->ring_d), sizeof(int32_t) * cap);
+      e = cudaMalloc(reinterpret_cast<void**>(&S.ring_d), sizeof(int32_t) * cap);
     if (e != cudaSuccess) return e;
-    q->ring_cap = cap;
+    S.ring_cap = cap;
   }
   q->published = 0;
   q->seen_published = 0;
   q->busy_until = 0;
-  q->ctl_h->published = 0;
-  q->ctl_h->final_count = -1;
-  q->ctl_h->completed = 0;
+  S.ctl_h->published = 0;
+  S.ctl_h->final_count = -1;
+  S.ctl_h->completed = 0;
   __atomic_thread_fence(__ATOMIC_SEQ_CST);
   cudaStream_t st = (cudaStream_t)stream;
   const QueueDevInit init{0, -1, 0, 0};
-  cudaError_t ce = cudaMemcpyAsync(q->qdev, &init, sizeof(init),
+  cudaError_t ce = cudaMemcpyAsync(S.qdev, &init, sizeof(init),
                                    cudaMemcpyHostToDevice, st);
   if (ce != cudaSuccess) return ce;
   int rc = tf_queue_consumer_launch(
-      pool_ext, pool_slices, q->n, q->ring_hd, q->ctl_hd, q->ring_d, q->qdev,
+      pool_ext, pool_slices, q->n, S.ring_hd, S.ctl_hd, S.ring_d, S.qdev,
       q->ctas, ax, ay, az, um, up, F, amax, flux_form,
       /*timeout_ns=*/2000000000LL, stream);
   if (rc) return rc;
-  ce = cudaEventRecord(q->done_ev, st);
+  ce = cudaEventRecord(S.done_ev, st);
   if (ce != cudaSuccess) return ce;
-  q->in_flight = true;
+  S.in_flight = true;
   tf_region* r = q->region;
   int64_t teams = 0;
   std::vector<int64_t> closed;
@@ -662,7 +680,7 @@ int tf_qexec_run_recon_flux(tf_qexec* q, const double* pool_ext,
   }
   drain();  // arrivals done: the queue drains, closing what is left
   // close the queue even on error so the consumer grid exits
-  __atomic_store_n(&q->ctl_h->final_count, (long long)q->published,
+  __atomic_store_n(&S.ctl_h->final_count, (long long)q->published,
                    __ATOMIC_RELEASE);
   *teams_published = teams;
   return rc;

@@ -681,46 +681,67 @@ __device__ __forceinline__ unsigned long long globaltimer() {
   return t;
 }
 
-// Block 0 is the fetcher: its first warp mirrors newly published ids from
-// the host ring into device memory (coalesced), forwards the close marker,
-// and reports the device-side completion count back to the host.  Blocks
-// 1.. are consumers polling the device mirror.
+// Block 0 is the fetcher: it mirrors newly published ids from the host ring
+// into device memory (all its threads, several independent PCIe reads in
+// flight per thread — one warp reading 32 ids per round trip was the
+// bottleneck), forwards the close marker, and reports the device-side
+// completion count back to the host.  Blocks 1.. are consumers polling the
+// device mirror.
 template <int THREADS>
 __device__ void queue_fetcher(const int* __restrict__ ring_h, QueueCtl* ctl,
                               int* __restrict__ ring_d, QueueDev* qd,
                               long long timeout_ns) {
-  if (threadIdx.x >= 32) return;
-  const int lane = threadIdx.x;
+  __shared__ long long s_pub, s_fin, s_done;
+  __shared__ int s_stop;
+  constexpr int U = 4;  // loads in flight per thread
   long long fetched = 0, reported = -1;
   unsigned long long last_change = globaltimer();
   for (;;) {
-    const long long pub = ld_acquire_sys(&ctl->published);
+    if (threadIdx.x == 0) {
+      s_pub = ld_acquire_sys(&ctl->published);
+      s_fin = ld_acquire_sys(&ctl->final_count);
+      s_done = (long long)atomicAdd(&qd->done, 0ULL);  // coherent read
+    }
+    __syncthreads();
+    const long long pub = s_pub, fin = s_fin, done = s_done;
     if (pub > fetched) {
-      for (long long k = fetched + lane; k < pub; k += 32)
-        ring_d[k] = ld_relaxed_sys(ring_h + k);
-      __syncwarp();
-      if (lane == 0) {
+      for (long long k0 = fetched; k0 < pub; k0 += (long long)THREADS * U) {
+        int v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const long long k = k0 + u * THREADS + threadIdx.x;
+          v[u] = k < pub ? ld_relaxed_sys(ring_h + k) : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const long long k = k0 + u * THREADS + threadIdx.x;
+          if (k < pub) ring_d[k] = v[u];
+        }
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
         __threadfence();
         st_release_gpu(&qd->published, pub);
       }
       fetched = pub;
       last_change = globaltimer();
     }
-    const long long fin = ld_acquire_sys(&ctl->final_count);
-    if (lane == 0 && fin >= 0 && fetched >= fin)
-      st_release_gpu(&qd->final_count, fin);
-    const long long done =
-        (long long)atomicAdd(&qd->done, 0ULL);  // coherent read
-    if (lane == 0 && done != reported) {
-      st_release_sys(&ctl->completed, done);
-      reported = done;
-      last_change = globaltimer();
+    if (threadIdx.x == 0) {
+      if (fin >= 0 && fetched >= fin) st_release_gpu(&qd->final_count, fin);
+      if (done != reported) {
+        st_release_sys(&ctl->completed, done);
+        last_change = globaltimer();
+      }
+      int stop = fin >= 0 && fetched >= fin && done >= fin;
+      if (!stop && (long long)(globaltimer() - last_change) > timeout_ns) {
+        st_release_gpu(&qd->final_count, fetched);
+        stop = 1;
+      }
+      s_stop = stop;
     }
-    if (fin >= 0 && fetched >= fin && done >= fin) break;
-    if ((long long)(globaltimer() - last_change) > timeout_ns) {
-      if (lane == 0) st_release_gpu(&qd->final_count, fetched);
-      break;
-    }
+    reported = done;
+    __syncthreads();
+    if (s_stop) break;
     __nanosleep(100);
   }
 }

@@ -11,7 +11,7 @@ n, grid = 8, 128
 f = sod_field(grid, "cuda"); pool = pool_from_field(f, n); ops.ghost_fill(pool, n, grid // n)
 S = pool.shape[0]; c = n + 2
 um = torch.empty((S,3,c,c,c), dtype=torch.float64, device="cuda"); up = torch.empty_like(um); F = torch.empty_like(um)
-arr = list(range(S))
+arr = np.arange(S, dtype=np.int32)
 for A in (1, 4, 16, 64, 128):
     q = QueueExecutor("reconstruct", A, default_parents(S, A), n)
     for _ in range(3): q.run(pool, (1,1,1), arr, um, up, F)
