@@ -110,6 +110,7 @@ struct tf_region {
   TeamTable teams;
   // per executor: forming teams holding a stream-idle watch, in watch order
   std::vector<std::vector<int64_t>> watchers;
+  std::vector<int64_t> fire_scratch;  // tf_region_stream_idle's swap buffer
   int64_t teams_formed = 0;
   int64_t solo_fast_path = 0;
   int64_t histogram[TF_MAX_TEAM + 1] = {0};
@@ -203,8 +204,8 @@ int tf_region_enter(tf_region* r, int64_t tag, tf_busy_fn busy, void* ctx,
 int tf_region_stream_idle(tf_region* r, int32_t executor, int64_t* out_teams,
                           int32_t cap) {
   if (!r || executor < 0 || executor >= r->executors) return -TF_E_INVALID;
-  std::vector<int64_t> fire;
-  fire.swap(r->watchers[executor]);
+  std::vector<int64_t>& fire = r->fire_scratch;
+  fire.swap(r->watchers[executor]);  // keeps both buffers' capacity
   int32_t n = 0;
   for (int64_t id : fire) {
     Team* t = r->teams.get(id);
@@ -215,6 +216,7 @@ int tf_region_stream_idle(tf_region* r, int32_t executor, int64_t* out_teams,
     if (out_teams && n < cap) out_teams[n] = id;
     ++n;
   }
+  fire.clear();
   return n;
 }
 
@@ -521,7 +523,6 @@ struct tf_qexec {
   int32_t n = 0;
   int64_t published = 0;
   int64_t seen_published = 0;
-  int64_t busy_until = 0;
   QueueSlot& slot() { return slots[cur]; }
   const QueueSlot& slot() const { return slots[cur]; }
 };
@@ -532,21 +533,18 @@ int64_t q_done(const tf_qexec* q) {
   return __atomic_load_n(&q->slot().ctl_h->completed, __ATOMIC_ACQUIRE);
 }
 
+// busy = published slices not all completed.  No clock: the completion
+// count lives in host memory (the fetcher CTA writes it), so a read costs a
+// cache hit, or one miss per device-side update — unlike cudaEventQuery there
+// is nothing to throttle.
 int q_busy(void* ctx, int32_t) {
   tf_qexec* q = static_cast<tf_qexec*>(ctx);
-  const int64_t t = now_ns();
   // work published since the last look cannot be finished yet
   if (q->published != q->seen_published) {
     q->seen_published = q->published;
-    q->busy_until = t + kRecheckNs;
     return 1;
   }
-  if (t < q->busy_until) return 1;
-  if (q_done(q) < q->published) {
-    q->busy_until = t + kRecheckNs;
-    return 1;
-  }
-  return 0;
+  return q_done(q) < q->published;
 }
 
 void q_publish(tf_qexec* q, int64_t team) {
@@ -641,7 +639,6 @@ int tf_qexec_run_recon_flux(tf_qexec* q, const double* pool_ext,
   }
   q->published = 0;
   q->seen_published = 0;
-  q->busy_until = 0;
   S.ctl_h->published = 0;
   S.ctl_h->final_count = -1;
   S.ctl_h->completed = 0;
