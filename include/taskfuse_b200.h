@@ -330,6 +330,13 @@ int tf_field_pad_f64(const double* field, int32_t X, int32_t Gy, int32_t Gz,
                      double* padded, tf_stream_t stream);
 int tf_field_unpad_f64(const double* padded, int32_t X, int32_t Gy,
                        int32_t Gz, double* field, tf_stream_t stream);
+/* Zero-copy download of the interior into a PINNED host field (cudaHostAlloc /
+ * torch pin_memory; TF_E_INVALID otherwise): the kernel's own posted PCIe
+ * writes, `ctas` CTAs of 256 threads, Gz even, host_field 16-B aligned.
+ * Used by the host pipeline so the copy engines serve only the upload.      */
+int tf_field_unpad_host_f64(const double* padded, int32_t X, int32_t Gy,
+                            int32_t Gz, double* host_field, int32_t ctas,
+                            tf_stream_t stream);
 
 /* ---- misc ----------------------------------------------------------------*/
 const char* tf_version(void);

@@ -201,6 +201,28 @@ __global__ void k_pad_io(double* __restrict__ field, double* __restrict__ P,
   }
 }
 
+// Zero-copy download: owned cells of the padded field straight into a
+// pinned host field over PCIe (GPU-initiated posted writes, 16 B per
+// thread, z rows contiguous on both sides).  A small grid on its own stream
+// saturates the link without crowding the SMs the step kernels need; the
+// copy engines stay free for the upload direction (CE up + kernel down
+// measured 45.8 GB/s per direction concurrently vs 27 for two kernels).
+__global__ void k_unpad_host(const double* __restrict__ P,
+                             double* __restrict__ host, int X, int Gy,
+                             int Gz) {
+  const int py = Gy + 2 * HY, pz = Gz + 2 * HZ;
+  const int hz = Gz / 2;
+  const int64_t total = (int64_t)X * Gy * hz;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t x = t / ((int64_t)Gy * hz);
+    const int y = (int)((t / hz) % Gy), z2 = (int)(t % hz);
+    const int64_t p = ((x + HX) * py + y + HY) * (int64_t)pz + HZ + 2 * z2;
+    const double2 v = *reinterpret_cast<const double2*>(P + p);
+    *reinterpret_cast<double2*>(host + 2 * t) = v;
+  }
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   static std::once_flag once;
@@ -470,6 +492,22 @@ int tf_field_pad_f64(const double* field, int32_t X, int32_t Gy, int32_t Gz,
   if (!field || !padded || X < 1 || Gy < 1 || Gz < 1) return TF_E_INVALID;
   k_pad_io<<<grid_for((int64_t)X * Gy * Gz), 256, 0, (cudaStream_t)stream>>>(
       const_cast<double*>(field), padded, X, Gy, Gz, 0);
+  return cudaGetLastError();
+}
+
+int tf_field_unpad_host_f64(const double* padded, int32_t X, int32_t Gy,
+                            int32_t Gz, double* host_field, int32_t ctas,
+                            tf_stream_t stream) {
+  if (!host_field || !padded || X < 1 || Gy < 1 || Gz < 2 || (Gz & 1) ||
+      ctas < 1)
+    return TF_E_INVALID;
+  if (reinterpret_cast<uintptr_t>(host_field) & 15) return TF_E_INVALID;
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, host_field) != cudaSuccess ||
+      a.type != cudaMemoryTypeHost)
+    return TF_E_INVALID;  // must be pinned (page-locked, device-mapped)
+  k_unpad_host<<<ctas, 256, 0, (cudaStream_t)stream>>>(padded, host_field, X,
+                                                       Gy, Gz);
   return cudaGetLastError();
 }
 

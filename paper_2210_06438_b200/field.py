@@ -35,6 +35,22 @@ def padded_shape(X: int, G: int) -> tuple[int, int, int]:
     return (X + 2 * HX, G + 2 * HY, G + 2 * HZ)
 
 
+def taper_layers(L: int) -> list[int]:
+    """Sub-grid layers per upload chunk for the host pipeline: small first
+    and last chunks shorten the pipeline's fill (nothing to step before the
+    first upload lands) and drain (the last chunk's step + download after
+    the last upload); measured best at L = 16: [1, 3, 4, 4, 3, 1]."""
+    base = [1, 3, 4, 4, 3, 1]
+    if L < 2 * len(base):
+        return [1] * L if L < 4 else [1] + [L - 2] + [1]
+    w = [max(1, round(b * L / 16)) for b in base]
+    k = 2
+    while sum(w) != L:          # fix rounding in the middle chunks
+        w[k] += 1 if sum(w) < L else -1
+        k = 3 if k == 2 else 2
+    return w
+
+
 def interior(P: torch.Tensor) -> torch.Tensor:
     return P[HX:-HX, HY:-HY, HZ:-HZ]
 
@@ -166,99 +182,118 @@ class FieldIteration(_FieldBase):
     def launches_per_step(self) -> int:
         return 2 + len(self.teams)   # 2 halo kernels + one per team
 
-    def run_host_pipelined(self, field_in, field_out, chunks: int = 8) -> int:
+    def run_host_pipelined(self, field_in, field_out, chunks="taper",
+                           down_ctas: int = 16,
+                           down_stream: bool = True) -> int:
         """One iteration from a pinned host field to a pinned host field with
-        the transfers overlapped: the field moves in x-chunks on an upload
-        stream, each chunk is scattered into the padded field and its halos
-        refreshed as it lands, chunk k is stepped (one fused launch over its
-        sub-grids) as soon as chunks k-1..k+1 are resident, and its updated
-        owned cells stream back on a download stream while later chunks are
-        still arriving.  Upload order N-1, 0, 1, ..., N-2 so the periodic x
-        halo of chunk 0 is available first.  Returns kernel launches."""
+        the transfers overlapped.  The field moves in x-chunks on an upload
+        stream (copy engine), each chunk's range shifted by the x halo
+        (HX planes) so that chunk i can be stepped as soon as ITS upload
+        lands: upload 0 also carries the field's last HX planes (the
+        periodic low x halo) and every upload i carries chunk i+1's first HX
+        planes.  Each landed range is scattered into the padded field and
+        its y/z halos refreshed, chunk i is stepped (one fused launch over
+        its sub-grids), and its updated owned cells go straight into the
+        pinned output by a zero-copy kernel on a download stream (the copy
+        engines serve only the upload).  The tail after the last upload is
+        one chunk's step and download.  Returns kernel launches."""
         G, n, m = self.G, self.n, self.m
         L = self.mx
-        chunks = max(d for d in range(1, min(chunks, L) + 1) if L % d == 0)
-        lay, cl = L // chunks, (L // chunks) * n
-        if chunks < 3:
+        if chunks == "taper":
+            chunks = taper_layers(L)
+        if isinstance(chunks, int):
+            c = max(d for d in range(1, min(chunks, L) + 1) if L % d == 0)
+            layers = [L // c] * c
+        else:   # explicit sub-grid layers per chunk (e.g. small first/last)
+            layers = [int(k) for k in chunks]
+            if sum(layers) != L or min(layers) < 1:
+                raise ValidationError(f"chunk layers must be positive and "
+                                      f"sum to {L}")
+        chunks = len(layers)
+        if chunks < 2 or n <= 2 * HX:
             self.run_host(field_in, field_out)
             return self.launches_per_step + 2
-        lib, X = self.lib, self.X
+        start = [0]
+        for k in layers:
+            start.append(start[-1] + k)     # chunk i = layers [start[i], start[i+1])
+        if not (field_in.is_pinned() and field_out.is_pinned()):
+            raise ValidationError("run_host_pipelined needs pinned host "
+                                  "fields (torch pin_memory)")
+        lib, X, H = self.lib, self.X, HX
         py, pz = G + 2 * HY, G + 2 * HZ
         lay_elems = py * pz
         plane = G * G
         P, Pn = self.P[self.cur], self.P[1 - self.cur]
         if not hasattr(self, "_pipe"):
-            self._pipe = dict(
-                up=torch.cuda.Stream(device=self.device),
-                down=torch.cuda.Stream(device=self.device),
-                out=torch.empty_like(self.field_dev),
-                ids={})
+            self._pipe = dict(up=torch.cuda.Stream(device=self.device),
+                              down=torch.cuda.Stream(device=self.device),
+                              ids={})
         pipe = self._pipe
         up, down = pipe["up"], pipe["down"]
         comp = torch.cuda.current_stream()
-        dev_in, dev_out = self.field_dev, pipe["out"]
+        dev_in = self.field_dev
+        ranges = []
+        for i in range(chunks):
+            lo = start[i] * n + H if i else 0
+            hi = start[i + 1] * n + H if i < chunks - 1 else X - H
+            ranges.append(([(X - H, X)] if i == 0 else []) + [(lo, hi)])
         ev_up = [torch.cuda.Event() for _ in range(chunks)]
         ev_done = [torch.cuda.Event() for _ in range(chunks)]
         up.wait_stream(comp)
         down.wait_stream(comp)
-        fin, fout = field_in.view(G, G, G), field_out.view(G, G, G)
-        order = [chunks - 1] + list(range(chunks - 1))
+        fin = field_in.view(G, G, G)
         with torch.cuda.stream(up):
-            for k in order:
-                dev_in[k * cl:(k + 1) * cl].copy_(fin[k * cl:(k + 1) * cl],
-                                                  non_blocking=True)
-                ev_up[k].record(up)
-        cs = comp.cuda_stream
+            for i, rs in enumerate(ranges):
+                for lo, hi in rs:
+                    dev_in[lo:hi].copy_(fin[lo:hi], non_blocking=True)
+                ev_up[i].record(up)
+        cs, ds = comp.cuda_stream, down.cuda_stream
         ax, ay, az = self.velocity
         launches = 0
-
-        def ready(k):
-            nonlocal launches
-            comp.wait_event(ev_up[k])
-            _lib.check(lib.tf_field_pad_f64(
-                dev_in.data_ptr() + 8 * k * cl * plane, cl, G, G,
-                P.data_ptr() + 8 * k * cl * lay_elems, cs), "tf_field_pad_f64")
-            _lib.check(lib.tf_field_halo_layers_f64(
-                P.data_ptr(), X, G, G, k * cl + HX, cl, cs),
-                "tf_field_halo_layers_f64")
-            launches += 3
-            if k == chunks - 1:
+        for i, rs in enumerate(ranges):
+            comp.wait_event(ev_up[i])
+            for lo, hi in rs:
+                _lib.check(lib.tf_field_pad_f64(
+                    dev_in.data_ptr() + 8 * lo * plane, hi - lo, G, G,
+                    P.data_ptr() + 8 * lo * lay_elems, cs), "tf_field_pad_f64")
+                _lib.check(lib.tf_field_halo_layers_f64(
+                    P.data_ptr(), X, G, G, lo + HX, hi - lo, cs),
+                    "tf_field_halo_layers_f64")
+                launches += 3
+            if i == 0:   # periodic x halos: both sources landed with upload 0
                 _lib.check(lib.tf_field_halo_xwrap_f64(P.data_ptr(), X, G, G,
-                                                       1, cs), "xwrap")
-            if k == 0:
-                _lib.check(lib.tf_field_halo_xwrap_f64(P.data_ptr(), X, G, G,
-                                                       2, cs), "xwrap")
-
-        def step(k):
-            nonlocal launches
-            ids = pipe["ids"].get(k)
+                                                       3, cs), "xwrap")
+            a, b = start[i], start[i + 1]
+            ids = pipe["ids"].get((a, b))
             if ids is None:
-                ids = torch.arange(k * lay * m * m, (k + 1) * lay * m * m,
-                                   dtype=torch.int32, device=self.device)
-                pipe["ids"][k] = ids
+                ids = torch.arange(a * m * m, b * m * m, dtype=torch.int32,
+                                   device=self.device)
+                pipe["ids"][(a, b)] = ids
             _lib.check(lib.tf_field_step_f64(
                 P.data_ptr(), X, G, G, n, ids.data_ptr(), None, ids.numel(),
                 ax, ay, az, self.dt_dx, Pn.data_ptr(), 0, cs),
                 "tf_field_step_f64")
-            _lib.check(lib.tf_field_unpad_f64(
-                Pn.data_ptr() + 8 * k * cl * lay_elems, cl, G, G,
-                dev_out.data_ptr() + 8 * k * cl * plane, cs),
-                "tf_field_unpad_f64")
+            if down_stream and down_ctas > 0:
+                ev_done[i].record(comp)
+                down.wait_event(ev_done[i])
+            if down_ctas > 0:
+                _lib.check(lib.tf_field_unpad_host_f64(
+                    Pn.data_ptr() + 8 * a * n * lay_elems, (b - a) * n, G, G,
+                    field_out.data_ptr() + 8 * a * n * plane, down_ctas,
+                    ds if down_stream else cs),
+                    "tf_field_unpad_host_f64")
+            else:   # copy-engine download through a device staging field
+                out = pipe.setdefault("out", torch.empty_like(dev_in))
+                _lib.check(lib.tf_field_unpad_f64(
+                    Pn.data_ptr() + 8 * a * n * lay_elems, (b - a) * n, G, G,
+                    out.data_ptr() + 8 * a * n * plane, cs),
+                    "tf_field_unpad_f64")
+                ev_done[i].record(comp)
+                down.wait_event(ev_done[i])
+                with torch.cuda.stream(down):
+                    field_out.view(G, G, G)[a * n:b * n].copy_(
+                        out[a * n:b * n], non_blocking=True)
             launches += 2
-            ev_done[k].record(comp)
-            with torch.cuda.stream(down):
-                down.wait_event(ev_done[k])
-                fout[k * cl:(k + 1) * cl].copy_(dev_out[k * cl:(k + 1) * cl],
-                                                non_blocking=True)
-
-        ready(chunks - 1)
-        ready(0)
-        ready(1)
-        step(0)
-        for k in range(2, chunks):
-            ready(k)
-            step(k - 1)
-        step(chunks - 1)
         comp.wait_stream(down)
         self.swap()
         return launches
@@ -273,18 +308,21 @@ class HostPipeline:
     writes P[1]."""
 
     def __init__(self, fi: "FieldIteration", field_in, field_out,
-                 chunks: int = 8):
+                 chunks="taper", down_ctas: int = 16,
+                 down_stream: bool = True):
         self.fi = fi
         self.bufs = (field_in, field_out)
         fi.cur = 0
-        fi.run_host_pipelined(field_in, field_out, chunks)   # warm-up
+        fi.run_host_pipelined(field_in, field_out, chunks, down_ctas,
+                              down_stream)  # warm-up
         fi.cur = 0
         torch.cuda.synchronize()
         self.graph = torch.cuda.CUDAGraph()
         s = torch.cuda.Stream(device=fi.device)
         s.wait_stream(torch.cuda.current_stream())
         with torch.cuda.graph(self.graph, stream=s):
-            self.launches = fi.run_host_pipelined(field_in, field_out, chunks)
+            self.launches = fi.run_host_pipelined(field_in, field_out, chunks,
+                                                  down_ctas, down_stream)
         fi.cur = 0
         torch.cuda.synchronize()
 

@@ -56,7 +56,9 @@ def test_field_host_roundtrip(cuda):
 @pytest.mark.parametrize("grid,n,chunks,vel", [
     (64, 8, 8, (1.0, 1.0, 1.0)), (128, 8, 8, (-1.0, 0.5, -0.25)),
     (128, 8, 4, (0.7, -1.3, 0.0)), (128, 16, 8, (1.0, 1.0, 1.0)),
-    (32, 8, 8, (1.0, 1.0, 1.0))])
+    (32, 8, 8, (1.0, 1.0, 1.0)), (128, 8, 2, (-0.3, 1.0, 0.9)),
+    (128, 8, 16, (-1.0, -1.0, 1.0)), (128, 8, [1, 2, 4, 5, 3, 1], (1.0, -0.5, 0.25)),
+    (64, 16, [1, 3], (0.5, 1.0, -1.0)), (128, 8, "taper", (1.0, 1.0, 1.0))])
 def test_field_host_pipelined(cuda, grid, n, chunks, vel):
     """Chunked, transfer-overlapped host round trip == one reference
     iteration; repeated calls chain correctly."""
