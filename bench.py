@@ -334,7 +334,31 @@ def run_sweep(wl, args, world, stream, peak):
             "launches": nk, "hbm_frac": wl16.S * b_alg(16) / (ms * 1e-3)
             / (peak * 1e9)}
     del wl16
+    out["config3"] = config3_sweep(args, world, stream, peak, ks, kw)
     return out
+
+
+def config3_sweep(args, world, stream, peak, ks, kw):
+    """BASELINE config 3: 32 768 8^3 sub-grids (grid 256, the reference's
+    Gaussian blast field), maximum aggregation (A = 128) vs strategy 2
+    (A = 1 over 8 / 32 / 128 streams)."""
+    wl3 = Workload(n=N_SUB, grid=256, field="blast")
+    res = {"workload": "config 3: grid 256, 32768 8^3 sub-grids, blast",
+           "aggregation_A128": {}, "strategy2": {}}
+    for E in sorted({args.executors, 4}):
+        step, nk, _, _ = plan_runner(wl3, 128, E, team_buffers=True)
+        ms = timed(step, ks, kw, world, stream)
+        res["aggregation_A128"][f"E{E}"] = {
+            "cell_updates_per_s": rate(wl3.S, wl3.n, ms), "ms_per_iter": ms,
+            "launches": nk,
+            "hbm_frac": wl3.S * b_alg(wl3.n) / (ms * 1e-3) / (peak * 1e9)}
+    for E in (8, 32, 128):
+        step, nk, _, _ = plan_runner(wl3, 1, E, parents=E)
+        ms = timed(step, max(3, ks // 4), kw, world, stream)
+        res["strategy2"][E] = {"cell_updates_per_s": rate(wl3.S, wl3.n, ms),
+                               "ms_per_iter": ms, "launches": nk}
+    del wl3
+    return res
 
 
 def cpu_baseline_leg(S, n, grid, steps=2, min_seconds=10.0):
