@@ -49,13 +49,29 @@ print(f"d2h alone {t(lambda: hout.copy_(d2, non_blocking=True)):.3f} ms")
 print(f"h2d+d2h concurrent {t(both):.3f} ms")
 print(f"device step {t(it.step):.3f} ms")
 print(f"run_host (serial) {t(lambda: it.run_host(hin, hout)):.3f} ms")
-for ch in (8, [1, 2, 3, 4, 3, 2, 1], [1, 3, 4, 4, 3, 1], [1, 2, 5, 5, 2, 1]):
-    for dc in (0, 16, 24):
-        for ds in (True,):
-            p = HostPipeline(it, hin, hout, chunks=ch, down_ctas=dc,
-                             down_stream=ds)
-            print(f"HostPipeline chunks={ch} down_ctas={dc} down_stream={ds}:"
-                  f" {t(p.run):.3f} ms", flush=True)
+def graph_of(fn):
+    it.cur = 0
+    fn()
+    it.cur = 0
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    st = torch.cuda.Stream()
+    st.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.graph(g, stream=st):
+        fn()
+    it.cur = 0
+    torch.cuda.synchronize()
+    return g
+
+
+for ch in ([1, 3, 4, 4, 3, 1], [1, 2, 3, 4, 3, 2, 1], 8, 16):
+    g = graph_of(lambda: it.run_host_pipelined(hin, hout, ch, 16, True))
+    print(f"chunks={ch}: {t(g.replay):.3f} ms", flush=True)
+import numpy as np  # noqa
+from oracle import hydro_oracle as HO  # noqa
+g.replay()
+torch.cuda.synchronize()
+print("bit-exact:", np.array_equal(hout.numpy(), HO.advect_once(hin.numpy())))
 
 # timeline of one pipelined iteration (kineto/CUPTI activity records)
 if len(sys.argv) > 1 and sys.argv[1] == "trace":
