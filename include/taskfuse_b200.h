@@ -338,6 +338,13 @@ int tf_field_unpad_host_f64(const double* padded, int32_t X, int32_t Gy,
                             int32_t Gz, double* host_field, int32_t ctas,
                             tf_stream_t stream);
 
+/* ---- device seam ---------------------------------------------------------*/
+/* enqueue_copy (reference device.py:237-252) as a real copy: `bytes` from
+ * src to dst in stream order; pinned host and device pointers in any
+ * combination (cudaMemcpyDefault).                                          */
+int tf_memcpy_async(void* dst, const void* src, int64_t bytes,
+                    tf_stream_t stream);
+
 /* ---- misc ----------------------------------------------------------------*/
 const char* tf_version(void);
 /* sm_100a device check: 0 iff device `dev` is compute capability 10.0.    */

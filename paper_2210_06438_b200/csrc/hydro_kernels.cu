@@ -1071,6 +1071,16 @@ int tf_queue_consumer_launch(const double* pool_ext, int64_t pool_slices,
   return cudaGetLastError();
 }
 
+// device.py:237-252 enqueue_copy: a real stream-ordered copy (pinned host
+// <-> device, or device <-> device), direction inferred from the pointers.
+int tf_memcpy_async(void* dst, const void* src, int64_t bytes,
+                    tf_stream_t stream) {
+  if (bytes < 0 || (bytes > 0 && (!dst || !src))) return TF_E_INVALID;
+  if (bytes == 0) return 0;
+  return cudaMemcpyAsync(dst, src, (size_t)bytes, cudaMemcpyDefault,
+                         (cudaStream_t)stream);
+}
+
 const char* tf_version(void) { return "taskfuse_b200 0.1 sm_100a"; }
 
 int tf_check_device(int32_t dev) {

@@ -12,7 +12,8 @@ that, and `CudaDevice` keeps only the seam the upper layers call
     enqueue_kernel(sid, spec, launch=None, body=None)
                                     launch(stream) issues the real kernel
     enqueue_copy(sid, dir, nbytes, src=None, dst=None)
-                                    real cudaMemcpyAsync when buffers given
+                                    real stream-ordered copy (tf_memcpy_async)
+                                    when buffers are given
     raw_alloc(kind, nbytes)         device / pinned-host bytes
     outstanding(sid)
 
@@ -31,6 +32,7 @@ from typing import Callable
 
 import torch
 
+from . import _lib
 from .errors import CapacityError, UsageError, ValidationError
 
 MAX_STREAMS = 128
@@ -66,11 +68,12 @@ class _Op:
 
 
 class _Stream:
-    __slots__ = ("index", "stream", "queue", "idle_callbacks")
+    __slots__ = ("index", "stream", "handle", "queue", "idle_callbacks")
 
     def __init__(self, index, stream):
         self.index = index
         self.stream = stream
+        self.handle = stream.cuda_stream
         self.queue: deque[_Op] = deque()
         self.idle_callbacks: list[Callable[[int], None]] = []
 
@@ -88,6 +91,10 @@ class CudaDevice:
         self.bytes_copied = 0
         self.raw_allocations = {"device": 0, "pinned_host": 0}
         self.sync_count = 0
+        self._index = self.device.index if self.device.index is not None \
+            else torch.cuda.current_device()
+        self._free_events: list = []   # retired ops' events, reused
+        self._lib = _lib.load()
         sched.attach_device(self)
 
     # -- streams -----------------------------------------------------------
@@ -130,7 +137,8 @@ class CudaDevice:
 
     # -- work submission ---------------------------------------------------
     def _submit(self, s: _Stream, kind: str, label: str):
-        ev = torch.cuda.Event()
+        ev = self._free_events.pop() if self._free_events else \
+            torch.cuda.Event()
         ev.record(s.stream)
         tok = self.sched.new_token(f"{label}@s{s.index}")
         s.queue.append(_Op(ev, tok, kind))
@@ -145,8 +153,15 @@ class CudaDevice:
         if body is not None:
             body()
         if launch is not None:
-            with torch.cuda.stream(s.stream):
+            # the stream is also made current for torch ops inside launch;
+            # set/restore directly (torch.cuda.stream() re-queries the
+            # device on every entry, a measurable cost per visit)
+            prev = torch.cuda.current_stream(self._index)
+            torch.cuda.set_stream(s.stream)
+            try:
                 launch(s.stream)
+            finally:
+                torch.cuda.set_stream(prev)
         self.kernels_enqueued += 1
         if self.record_events:
             self.events.append((self.sched.now, "kernel_enqueue", s.index,
@@ -163,9 +178,12 @@ class CudaDevice:
             raise UsageError("copy size must be >= 0")
         s = self._stream(sid)
         if src is not None and dst is not None and nbytes:
-            n = nbytes // src.element_size()
-            with torch.cuda.stream(s.stream):
-                dst.view(-1)[:n].copy_(src.view(-1)[:n], non_blocking=True)
+            if nbytes > min(src.numel() * src.element_size(),
+                            dst.numel() * dst.element_size()):
+                raise UsageError("copy larger than its buffers")
+            _lib.check(self._lib.tf_memcpy_async(
+                dst.data_ptr(), src.data_ptr(), nbytes, s.handle),
+                "tf_memcpy_async")
         self.copies_enqueued += 1
         self.bytes_copied += nbytes
         return self._submit(s, "copy", f"copy:{direction}")
@@ -188,6 +206,7 @@ class CudaDevice:
         progress = False
         while s.queue and s.queue[0].event.query():
             op = s.queue.popleft()
+            self._free_events.append(op.event)
             op.token.fire()
             progress = True
         if progress and not s.queue and s.idle_callbacks:

@@ -39,6 +39,47 @@ from .scenario import (ITERATIONS_PER_STEP, VELOCITY, HydroState, dt_over_dx,
 ITEM_BYTES = 8
 
 
+class _IdRing:
+    """Team id lists for the stage kernels in a pinned host ring, read by
+    the kernels zero-copy (no per-launch tensor, pin or copy).  Reuse is
+    fenced per half ring: crossing into a half waits for events recorded on
+    every executor stream when that half was last left, i.e. for launches
+    issued a half ring ago (in practice long finished)."""
+
+    def __init__(self, streams, size: int = 1 << 16):
+        self.buf = torch.empty(size, dtype=torch.int32).pin_memory()
+        self.np = self.buf.numpy()
+        self.size, self.half = size, size // 2
+        self.pos = 0
+        self.cur = 0                  # the half being written
+        self.streams = streams
+        self.fence = [None, None]     # per half: events from when we left it
+
+    def put(self, args) -> torch.Tensor:
+        T = len(args)
+        if self.pos + T > self.size:
+            self._cross(0)
+            self.pos = 0
+        elif self.cur == 0 and self.pos + T > self.half:
+            self._cross(1)
+            self.pos = self.half
+        a = self.pos
+        self.np[a:a + T] = args
+        self.pos = a + T
+        return self.buf[a:a + T]
+
+    def _cross(self, into: int) -> None:
+        self.cur = into
+        for ev in self.fence[into] or ():
+            ev.synchronize()
+        left = []
+        for st in self.streams:
+            ev = torch.cuda.Event()
+            ev.record(st)
+            left.append(ev)
+        self.fence[1 - into] = left
+
+
 class HydroSim:
     def __init__(self, sched: Scheduler, state: HydroState,
                  executors: ExecutorPool, buffers: BufferPool | None = None,
@@ -64,6 +105,9 @@ class HydroSim:
             for k in KERNEL_ORDER}
         for k, region in self.regions.items():
             region.register_kernel(k, partial(self._launch, k))
+        dev = executors.device
+        self._ids_ring = _IdRing([dev.stream(e.stream_id)
+                                  for e in executors.executors])
 
     @property
     def scratch(self):
@@ -72,8 +116,7 @@ class HydroSim:
                 for b in self.state.blocks}
 
     def _ids(self, args) -> torch.Tensor:
-        host = torch.tensor(args, dtype=torch.int32).pin_memory()
-        return host.to(self.state.device, non_blocking=True)
+        return self._ids_ring.put(args)
 
     def _launch(self, kernel: str, stream, args) -> None:
         """One batched launch for a whole team (slice order = args order)."""

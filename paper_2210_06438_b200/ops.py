@@ -37,13 +37,16 @@ def _need_cuda_f64(t: torch.Tensor, name: str) -> None:
 
 
 def _ids_ptr(ids) -> tuple[int | None, int | None]:
-    """Device ids tensor -> (pointer, count); None -> (None, None)."""
+    """ids tensor -> (pointer, count); None -> (None, None).  A device
+    tensor, or a PINNED host tensor, which the kernel reads zero-copy over
+    PCIe (one 4-byte load per CTA) — a team's ids then need no copy."""
     if ids is None:
         return None, None
-    if not (isinstance(ids, torch.Tensor) and ids.is_cuda
-            and ids.dtype == torch.int32 and ids.dim() == 1
-            and ids.is_contiguous()):
-        raise ValidationError("ids must be a contiguous 1-D int32 CUDA tensor")
+    if not (isinstance(ids, torch.Tensor) and ids.dtype == torch.int32
+            and ids.dim() == 1 and ids.is_contiguous()
+            and (ids.is_cuda or ids.is_pinned())):
+        raise ValidationError("ids must be a contiguous 1-D int32 CUDA or "
+                              "pinned host tensor")
     return ids.data_ptr(), ids.numel()
 
 

@@ -13,7 +13,7 @@ pytestmark = pytest.mark.gpu
 
 
 def run_sim(n, grid, steps, executors=1, max_team=1, field=None,
-            velocity=(1.0, 1.0, 1.0), poison=False):
+            velocity=(1.0, 1.0, 1.0), poison=False, id_ring=None):
     from paper_2210_06438_b200.device import CudaDevice
     from paper_2210_06438_b200.executorpool import ExecutorPool
     from paper_2210_06438_b200.hydro import HydroSim, driver, make_state
@@ -27,6 +27,10 @@ def run_sim(n, grid, steps, executors=1, max_team=1, field=None,
     sim = HydroSim(sched, state, pool, max_team=max_team, velocity=velocity)
     if poison:
         sim.scratch_pool.poison()
+    if id_ring is not None:   # a tiny ring: wraps every few launches
+        from paper_2210_06438_b200.hydro.step import _IdRing
+        sim._ids_ring = _IdRing([device.stream(e.stream_id)
+                                 for e in pool.executors], size=id_ring)
     sched.spawn(lambda: driver(sim, steps), label="driver")
     sched.run()
     return state, sim, device
@@ -147,3 +151,14 @@ def test_ghost_exchange_matches_periodic_window(cuda):
     idx = np.arange(-3, 8 + 3) % 16
     assert np.array_equal(state.u[(0, 0, 0)].cpu().numpy(),
                           field[np.ix_(idx, idx, idx)])
+
+
+def test_team_id_ring_wraps(cuda, hydro_golden):
+    """Team ids go to the kernels through a pinned ring read zero-copy;
+    a 64-entry ring wraps every few teams and must stay fenced."""
+    from paper_2210_06438_b200.hydro import assemble
+    case = _golden(hydro_golden, "blast16_n8_v111")
+    state, sim, _ = run_sim(8, 16, steps=2, executors=4, max_team=8,
+                            id_ring=64)
+    assert HO.digest(assemble(state)) == case["reference_step_2"]
+    assert sim._ids_ring.size == 64
