@@ -12,13 +12,15 @@
 // pack kernel).
 //
 // Step kernel.  One CTA per sub-grid of the team: ONE TMA box load of the
-// (n+4) x (n+4) x (n+8) stencil box straight from P (the sub-grid's "ghost
-// exchange" is just the box overlapping its neighbours), the fluxes of all
-// (n+2)^3 faces into shared memory with the reference's arithmetic
-// (cell_axis, kernels.py:73-93), then the no-FMA update of the n^3 owned
-// cells (kernels.py:100-111) into the next padded field.  Algorithmic bytes
-// per 8^3 sub-grid: 8 * [12*12*16 read + 512 written] = 22.5 KB, vs
-// 84.8 KB + 36 KB ghost fill + 28 KB update for the materialising path.
+// sub-grid's stencil box straight from P (the sub-grid's "ghost exchange"
+// is just the box overlapping its neighbours), then every owned cell's six
+// face fluxes with the reference's arithmetic (face_flux, kernels.py:73-93)
+// and the no-FMA update (kernels.py:100-111) into the next padded field.
+// n = 8 uses k_step_cols8 (swizzled 11 x 11 x 16 box, threads own z
+// columns, 16-B shared loads); n = 16 uses k_step_fused (full box, one
+// cell per thread-iteration).  Algorithmic bytes per 8^3 sub-grid (SURVEY
+// B_step): 8 * [(n+2)^3 + 6 (n+2)^2 + n^3] = 16.9 KB, vs 84.8 KB + 36 KB
+// ghost fill + 28 KB update for the materialising path.
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
@@ -155,6 +157,134 @@ __global__ void __launch_bounds__(THREADS)
   }
 }
 
+// ---- n = 8: one thread per owned z column, swizzled box ------------------
+// The box's z rows are 16 doubles = 128 B, so the TMA load can use the
+// 128-byte swizzle (16-B chunk c of box row r lands at chunk c ^ (r & 7)).
+// Each of the CTA's 64 threads owns one (x, y) column of 8 cells and reads
+// whole 16-B z pairs: its own column once (z halo included, kept in
+// registers; each z face flux is formed once and carried to the next
+// cell), and the three neighbour columns along x and along y that the
+// upwind faces need.  A quarter warp (8 threads, consecutive y) touches 8
+// consecutive box rows — 8 distinct swizzled chunks, no bank conflict —
+// and every load moves 16 B: 30 vector loads per 8 cells instead of ~10
+// scalar, 2-way-conflicted loads per cell.  The x/y extent of the box is
+// 11, not 12: an upwind face reads 2 cells upstream and 1 downstream, so
+// the box origin shifts by one cell against the flow (a < 0); 15.5 KB per
+// sub-grid keeps 13 CTAs resident.  Same arithmetic, same order as
+// face_flux / update_body: bit-identical.
+__device__ __forceinline__ double2 ld_swz(const unsigned char* box, int r,
+                                          int c) {
+  return *reinterpret_cast<const double2*>(box + r * 128 +
+                                           ((c ^ (r & 7)) << 4));
+}
+
+// Flux through the face between cells u0 and up1 (face_flux, kernels.py:
+// 73-93): upwind a*(u0 + sigma0/2) for a >= 0, a*(up1 - sigma1/2) for a < 0.
+__device__ __forceinline__ double face(double um1, double u0, double up1,
+                                       double up2, double a) {
+  if (a >= 0.0)
+    return __dmul_rn(a, __dadd_rn(u0, __dmul_rn(0.5, minmod(__dsub_rn(up1, u0),
+                                                          __dsub_rn(u0, um1)))));
+  return __dmul_rn(a, __dsub_rn(up1, __dmul_rn(0.5, minmod(__dsub_rn(up2, up1),
+                                                         __dsub_rn(up1, u0)))));
+}
+
+constexpr int COLS8_BXY = 11;                                    // box x, y
+constexpr int COLS8_BOX_BYTES = COLS8_BXY * COLS8_BXY * 16 * 8;  // 15 488
+
+// CPT = owned cells per thread along z (8: one thread per column, 64
+// threads; 4: two threads per column, 128 threads — twice the parallelism
+// per sub-grid for small team launches).
+template <int CPT>
+constexpr int cols8_threads() { return 64 * (8 / CPT); }
+template <int CPT>
+constexpr int cols8_min_blocks() { return CPT == 8 ? 13 : 8; }
+
+template <int CPT, bool DEV_IDS>
+__global__ void __launch_bounds__(cols8_threads<CPT>(), cols8_min_blocks<CPT>())
+    k_step_cols8(const __grid_constant__ CUtensorMap tmap,
+                 const int32_t* __restrict__ dev_ids,
+                 const __grid_constant__ TeamIds team, int m, double ax,
+                 double ay, double az, double dt_dx, double* __restrict__ out,
+                 int64_t pyz, int pz, double* peer_lo, double* peer_hi, int X,
+                 int mx) {
+  constexpr int N = 8, BY = COLS8_BXY;
+  // no static shared memory: the dynamic window starts 1024-B aligned, as
+  // the 128-B swizzle requires; the mbarrier sits after the box
+  extern __shared__ __align__(1024) unsigned char box[];
+  uint64_t* bar = reinterpret_cast<uint64_t*>(box + COLS8_BOX_BYTES);
+
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  const int s = blockIdx.x;
+  const int g = DEV_IDS ? (dev_ids ? dev_ids[s] : s) : team.id[s];
+  const int bx = g / (m * m), by = (g / m) % m, bz = g % m;
+  // against the flow the box needs 2 cells, with it 1 (+1 origin if a < 0)
+  const int sx = ax >= 0.0 ? 0 : 1, sy = ay >= 0.0 ? 0 : 1;
+  if (threadIdx.x == 0) {
+    mbar_init(bar);
+    mbar_expect_tx(bar, COLS8_BOX_BYTES);
+    tma_load_3d(box, &tmap, bz * N, by * N + sy, bx * N + sx, bar);
+  }
+  __syncthreads();
+  mbar_wait(bar);
+
+  const int col = threadIdx.x & 63, part = threadIdx.x >> 6;
+  const int i = col >> 3, j = col & 7;
+  const int r0 = (i + 2 - sx) * BY + (j + 2 - sy);  // own box row
+  const int k0 = part * CPT;                        // first owned z
+  // own column, box z k0+2 .. k0+CPT+5 (chunks k0/2+1 ..): u[z - k0 - 2]
+  double u[CPT + 4];
+#pragma unroll
+  for (int q = 0; q < CPT / 2 + 2; ++q) {
+    const double2 v = ld_swz(box, r0, k0 / 2 + 1 + q);
+    u[2 * q] = v.x;
+    u[2 * q + 1] = v.y;
+  }
+  // the far neighbour an upwind face needs: -2 for a >= 0, +2 for a < 0
+  const int fx = ax >= 0.0 ? -2 : 2, fy = ay >= 0.0 ? -2 : 2;
+  const int64_t x = (int64_t)bx * N + i + HX, y = (int64_t)by * N + j + HY;
+  double* o = out + x * pyz + y * pz + (int64_t)bz * N + HZ;
+  // z flux through the face below owned cell k0
+  double fz = face(u[0], u[1], u[2], u[3], az);
+#pragma unroll
+  for (int q = 0; q < CPT / 2; ++q) {  // owned z pair k0+2q, k0+2q+1
+    const int c = k0 / 2 + 2 + q;      // its box chunk
+    const double2 xm = ld_swz(box, r0 - BY, c), xp = ld_swz(box, r0 + BY, c),
+                  xf = ld_swz(box, r0 + fx * BY, c);
+    const double2 ym = ld_swz(box, r0 - 1, c), yp = ld_swz(box, r0 + 1, c),
+                  yf = ld_swz(box, r0 + fy, c);
+    double v[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int z = 2 * q + h + 2;  // index into u
+      const double u0 = u[z];
+      const double xmv = h ? xm.y : xm.x, xpv = h ? xp.y : xp.x,
+                   xfv = h ? xf.y : xf.x;
+      const double ymv = h ? ym.y : ym.x, ypv = h ? yp.y : yp.x,
+                   yfv = h ? yf.y : yf.x;
+      // update_body order: ((dFx + dFy) + dFz), kernels.py:100-111; the far
+      // value serves as um2 (a >= 0) or up2 (a < 0) — face() reads only one
+      double div = __dsub_rn(face(xmv, u0, xpv, xfv, ax),
+                             face(xfv, xmv, u0, xpv, ax));
+      div = __dadd_rn(div, __dsub_rn(face(ymv, u0, ypv, yfv, ay),
+                                     face(yfv, ymv, u0, ypv, ay)));
+      const double fz_up = face(u[z - 1], u0, u[z + 1], u[z + 2], az);
+      div = __dadd_rn(div, __dsub_rn(fz_up, fz));
+      fz = fz_up;
+      v[h] = __dsub_rn(u0, __dmul_rn(dt_dx, div));
+    }
+    const double2 w = make_double2(v[0], v[1]);
+    const int k = k0 + 2 * q;  // owned z of this pair
+    *reinterpret_cast<double2*>(o + k) = w;
+    if (peer_lo != nullptr && bx == 0 && i < HX)
+      *reinterpret_cast<double2*>(peer_lo + ((int64_t)X + HX + i) * pyz +
+                                  y * pz + (int64_t)bz * N + HZ + k) = w;
+    if (peer_hi != nullptr && bx == mx - 1 && i >= N - HX)
+      *reinterpret_cast<double2*>(peer_hi + (int64_t)(i - (N - HX)) * pyz +
+                                  y * pz + (int64_t)bz * N + HZ + k) = w;
+  }
+}
+
 // Periodic y and z halo of every x layer (z after y so corners are right).
 __global__ void k_halo_yz(double* __restrict__ P, int layers, int Gy, int Gz) {
   const int py = Gy + 2 * HY, pz = Gz + 2 * HZ;
@@ -266,13 +396,16 @@ int field_map(const double* P, int X, int Gy, int Gz, int n, CUtensorMap* out) {
   const cuuint64_t pz = Gz + 2 * HZ, py = Gy + 2 * HY, px = X + 2 * HX;
   cuuint64_t dims[3] = {pz, py, px};
   cuuint64_t strides[2] = {pz * 8, pz * py * 8};
-  cuuint32_t box[3] = {(cuuint32_t)(n + 8), (cuuint32_t)(n + 4),
-                       (cuuint32_t)(n + 4)};
+  // n = 8: 11 x 11 x 16 (k_step_cols8); n = 16: the full (n+4)^2 (n+8)
+  const cuuint32_t bxy = n == 8 ? COLS8_BXY : (cuuint32_t)(n + 4);
+  cuuint32_t box[3] = {(cuuint32_t)(n + 8), bxy, bxy};
   cuuint32_t es[3] = {1, 1, 1};
   CUtensorMap m;
   if (fn(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(P), dims,
          strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-         CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+         // n = 8: z rows of exactly 128 B -> swizzled for k_step_cols8
+         n == 8 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+         CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return TF_E_INVALID;
   if (cache.size() > 256) cache.clear();
@@ -287,10 +420,19 @@ int launch_step(const CUtensorMap& map, const int32_t* dev_ids,
                 double az, double dt_dx, double* out, int X, int Gy, int Gz,
                 cudaStream_t st, int flags, double* peer_lo = nullptr,
                 double* peer_hi = nullptr) {
-  // 128 threads per sub-grid: measured best of 128/256/512
-  constexpr int TH = 128;
-  constexpr size_t smem = FGeo<N>::BOX * sizeof(double);
-  auto kern = k_step_fused<N, TH, DEV_IDS>;
+  // n = 8: k_step_cols8 — one thread per column (CPT 8) for launches that
+  // fill the GPU many times over (config 5: 206 vs 191 G cell-updates/s),
+  // two per column (CPT 4) for team-sized launches, where per-sub-grid
+  // latency decides (config 2 team plan: 41 vs 45 us).  n = 16: 128
+  // threads per sub-grid, measured best of 128/256/512.
+  const int cpt = T >= 4096 ? 8 : 4;
+  const int TH = N == 8 ? (cpt == 4 ? cols8_threads<4>() : cols8_threads<8>())
+                        : 128;
+  constexpr size_t smem = N == 8 ? COLS8_BOX_BYTES + 8
+                                 : FGeo<N>::BOX * sizeof(double);
+  auto kern = N == 8 ? (cpt == 4 ? k_step_cols8<4, DEV_IDS>
+                                 : k_step_cols8<8, DEV_IDS>)
+                     : k_step_fused<N, 128, DEV_IDS>;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(

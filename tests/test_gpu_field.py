@@ -28,6 +28,26 @@ def test_field_iteration_matches_reference(cuda, grid, n, vel, A, E):
     assert np.array_equal(it.owned().cpu().numpy(), HO.reference_step(f, vel))
 
 
+@pytest.mark.parametrize("vel", [(1.0, 1.0, 1.0), (-1.0, 0.5, -0.25),
+                                 (0.7, -1.3, 0.0), (-0.2, -0.9, 1.1)])
+def test_field_step_one_large_launch(cuda, vel):
+    """One launch over >= 4096 sub-grids takes the one-thread-per-column
+    kernel shape (k_step_cols8<8>); team-sized launches take <4>.  Both
+    bit-identical, every sign combination of the velocity (the swizzled box
+    origin shifts against the flow)."""
+    import torch
+    from paper_2210_06438_b200.field import FieldIteration
+    f = HO.stress_field(128)
+    it = FieldIteration(128, 8, vel, max_team=128, executors=1)
+    it.load(torch.from_numpy(f).to(cuda))
+    for _ in range(3):
+        it.halo(True)
+        it.step_ids(None, it.S)      # one launch, 4096 sub-grids
+        it.swap()
+    torch.cuda.synchronize()
+    assert np.array_equal(it.owned().cpu().numpy(), HO.reference_step(f, vel))
+
+
 def test_field_iteration_golden(cuda, hydro_golden):
     import torch
     from paper_2210_06438_b200.field import FieldIteration
