@@ -57,11 +57,13 @@ def b_step(n: int) -> int:
     return 8 * (c ** 3 + 6 * c ** 2 + n ** 3)
 
 
-def ncu_traffic_per_launch(team: int):
-    """DRAM bytes (read + write) per team launch of T slices, from the
-    committed ncu capture of the recon+flux kernel (one launch over 4096
-    slices; writes still resident in L2 at kernel end are not counted)."""
-    path = os.path.join(ROOT, "profiles", "r01_ncu_recon_flux_single.txt")
+def ncu_traffic_per_launch(team: int,
+                           capture: str = "r01_ncu_recon_flux_single.txt"):
+    """DRAM bytes (read + write) per launch of `team` slices / sub-grids,
+    scaled from a committed ncu --set full capture (the recon+flux kernel
+    over 4096 slices by default; writes still resident in L2 at kernel end
+    are not counted)."""
+    path = os.path.join(ROOT, "profiles", capture)
     try:
         vals = {}
         with open(path) as fh:
@@ -574,10 +576,15 @@ def cfg5_leg(args, world, rank, local, peak):
             "bound": "hbm", "unit": "GB/s", "peak": peak,
             "achieved": fused_bytes / (ms * 1e-3) / 1e9,
             "frac": fused_bytes / (ms * 1e-3) / 1e9 / peak,
-            "traffic": None,
+            "traffic": ncu_traffic_per_launch(
+                part.subgrids, "r01_ncu_step_fused_cfg5g256.txt"),
             "note": "fused step, SURVEY §8(d) B_step = 8[(n+2)^3 + "
                     "6(n+2)^2 + n^3] = 16 896 B per 8^3 sub-grid; halo "
-                    "refresh and exchange inside the step"},
+                    "refresh and exchange inside the step. frac can exceed "
+                    "1: B_step counts each sub-grid's halo reads, which the "
+                    "padded-field layout serves from L2 (traffic = DRAM "
+                    "bytes per step-kernel launch from the ncu capture at "
+                    "grid 256, scaled: ~7.2 KB per sub-grid)"},
         "materialising_path": {
             "ms_per_step": ms_pool,
             "value": rate(S_total, n, ms_pool),
