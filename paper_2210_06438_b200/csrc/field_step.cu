@@ -16,9 +16,9 @@
 // is just the box overlapping its neighbours), then every owned cell's six
 // face fluxes with the reference's arithmetic (face_flux, kernels.py:73-93)
 // and the no-FMA update (kernels.py:100-111) into the next padded field.
-// n = 8 uses k_step_cols8 (swizzled 11 x 11 x 16 box, threads own z
-// columns, 16-B shared loads); n = 16 uses k_step_fused (full box, one
-// cell per thread-iteration).  Algorithmic bytes per 8^3 sub-grid (SURVEY
+// n = 8 uses k_step_cols8s (swizzled 11 x 11 x 16 box, threads own z
+// columns, 16-B shared loads, each face formed once); n = 16 uses
+// k_step_fused (full box, one cell per thread-iteration).  Algorithmic bytes per 8^3 sub-grid (SURVEY
 // B_step): 8 * [(n+2)^3 + 6 (n+2)^2 + n^3] = 16.9 KB, vs 84.8 KB + 36 KB
 // ghost fill + 28 KB update for the materialising path.
 #include <cuda.h>
@@ -26,6 +26,7 @@
 #include <cudaTypedefs.h>
 #include <stdint.h>
 
+#include <cstdlib>
 #include <mutex>
 #include <unordered_map>
 
@@ -163,30 +164,16 @@ __global__ void __launch_bounds__(THREADS)
 // Each of the CTA's 64 threads owns one (x, y) column of 8 cells and reads
 // whole 16-B z pairs: its own column once (z halo included, kept in
 // registers; each z face flux is formed once and carried to the next
-// cell), and the three neighbour columns along x and along y that the
-// upwind faces need.  A quarter warp (8 threads, consecutive y) touches 8
-// consecutive box rows — 8 distinct swizzled chunks, no bank conflict —
-// and every load moves 16 B: 30 vector loads per 8 cells instead of ~10
-// scalar, 2-way-conflicted loads per cell.  The x/y extent of the box is
-// 11, not 12: an upwind face reads 2 cells upstream and 1 downstream, so
-// the box origin shifts by one cell against the flow (a < 0); 15.5 KB per
-// sub-grid keeps 13 CTAs resident.  Same arithmetic, same order as
-// face_flux / update_body: bit-identical.
+// cell) and the two neighbour columns along x and along y that its +1/2
+// faces need.  A quarter warp (8 threads, consecutive y) touches 8
+// consecutive box rows — 8 distinct swizzled chunks, no bank conflict.
+// The x/y extent of the box is 11, not 12: an upwind face reads 2 cells
+// upstream and 1 downstream, so the box origin shifts by one cell against
+// the flow (a < 0); 15.5 KB per sub-grid.
 __device__ __forceinline__ double2 ld_swz(const unsigned char* box, int r,
                                           int c) {
   return *reinterpret_cast<const double2*>(box + r * 128 +
                                            ((c ^ (r & 7)) << 4));
-}
-
-// Flux through the face between cells u0 and up1 (face_flux, kernels.py:
-// 73-93): upwind a*(u0 + sigma0/2) for a >= 0, a*(up1 - sigma1/2) for a < 0.
-__device__ __forceinline__ double face(double um1, double u0, double up1,
-                                       double up2, double a) {
-  if (a >= 0.0)
-    return __dmul_rn(a, __dadd_rn(u0, __dmul_rn(0.5, minmod(__dsub_rn(up1, u0),
-                                                          __dsub_rn(u0, um1)))));
-  return __dmul_rn(a, __dsub_rn(up1, __dmul_rn(0.5, minmod(__dsub_rn(up2, up1),
-                                                         __dsub_rn(up1, u0)))));
 }
 
 constexpr int COLS8_BXY = 11;                                    // box x, y
@@ -197,20 +184,168 @@ constexpr int COLS8_BOX_BYTES = COLS8_BXY * COLS8_BXY * 16 * 8;  // 15 488
 // per sub-grid for small team launches).
 template <int CPT>
 constexpr int cols8_threads() { return 64 * (8 / CPT); }
+// ---- each x / y face formed ONCE -------------------------------------------
+// Forming both x faces and both y faces of every owned cell computes every
+// interior x / y face twice (44 FP64 instructions per cell).  Here a thread
+// forms only the +1/2 face of its cell along x and y and takes the -1/2
+// face from the lane that owns the neighbouring column (__shfl_up: a warp
+// holds a 4 (x) x 8 (y) block of columns, so -x is lane-8 and -y is
+// lane-1).  The faces a warp cannot get from its own lanes — x faces of
+// column i0-1 and y faces of row j=-1 — are formed in a prologue, three per
+// lane, into a per-warp shared strip: 33 FP64 instructions per cell
+// (config 5: 0.649 -> 0.634 ms per iteration; the kernel is latency-bound,
+// ~25% of warp time waits on the box — a persistent double-buffered
+// variant (6 CTAs/SM) ran 0.726 ms and an L2 prefetch of later CTAs'
+// boxes 0.764 ms).  Same arithmetic, same operation order per
+// face and per update as face_flux / update_body: bit-identical.
+//
+// Face between cells with box values (v0, v1, v2) taken upwind-first:
+// v = (u_{c-1}, u_c, u_{c+1}) for a >= 0, (u_c, u_{c+1}, u_{c+2}) for a < 0
+// (face_flux, kernels.py:73-93).  Thanks to the flow-shifted box, the +1/2
+// face of owned cell c always uses box indices c+1, c+2, c+3 along x / y.
+template <bool POS>
+__device__ __forceinline__ double face3(double v0, double v1, double v2,
+                                        double a) {
+  const double h = __dmul_rn(0.5, minmod(__dsub_rn(v2, v1), __dsub_rn(v1, v0)));
+  return __dmul_rn(a, POS ? __dadd_rn(v1, h) : __dsub_rn(v1, h));
+}
+__device__ __forceinline__ double ld_swz1(const unsigned char* box, int r,
+                                          int z) {
+  return *reinterpret_cast<const double*>(
+      box + r * 128 + (((z >> 1) ^ (r & 7)) << 4) + ((z & 1) << 3));
+}
+constexpr int COLS8S_HALO_OFF = 15504;  // after the box and the mbarrier
+constexpr int COLS8S_SMEM = COLS8S_HALO_OFF + 2 * 96 * 8;  // 17 040 B
+
+template <int CPT, bool PX, bool PY, bool PZ>
+__device__ __forceinline__ void cols8s_body(
+    const unsigned char* box, double* halo, int i, int j, int k0, int i0,
+    double ax, double ay, double az, double dt_dx, double* o, bool lo,
+    bool hi, double* plo, double* phi) {
+  constexpr int BY = COLS8_BXY, HXF = 8 * CPT, HALO = 12 * CPT;
+  constexpr int sx = PX ? 0 : 1, sy = PY ? 0 : 1;
+  const int lane = threadIdx.x & 31;
+  // prologue: the warp's boundary faces (x: column i0-1, every j; y: row
+  // j=-1, every i of the warp), 12*CPT of them, spread over the lanes
+#pragma unroll
+  for (int f = lane; f < HALO; f += 32) {
+    double v0, v1, v2;
+    if (f < HXF) {
+      const int jj = f & 7, z = k0 + (f >> 3) + 4;
+      const int r = i0 * BY + jj + 2 - sy;
+      v0 = ld_swz1(box, r, z);
+      v1 = ld_swz1(box, r + BY, z);
+      v2 = ld_swz1(box, r + 2 * BY, z);
+      halo[f] = face3<PX>(v0, v1, v2, ax);
+    } else {
+      const int g = f - HXF, ii = g & 3, z = k0 + (g >> 2) + 4;
+      const int r = (i0 + ii + 2 - sx) * BY;
+      v0 = ld_swz1(box, r, z);
+      v1 = ld_swz1(box, r + 1, z);
+      v2 = ld_swz1(box, r + 2, z);
+      halo[f] = face3<PY>(v0, v1, v2, ay);
+    }
+  }
+  __syncwarp();
+  const int r0 = (i + 2 - sx) * BY + (j + 2 - sy);  // own box row
+  double u[CPT + 4];  // own column, box z k0+2 .. k0+CPT+5
+#pragma unroll
+  for (int q = 0; q < CPT / 2 + 2; ++q) {
+    const double2 v = ld_swz(box, r0, k0 / 2 + 1 + q);
+    u[2 * q] = v.x;
+    u[2 * q + 1] = v.y;
+  }
+  // z face below owned cell k0 (u index 2): PZ (u1,u2,u3) / !PZ (u2,u3,u4)
+  double fz = PZ ? face3<true>(u[0], u[1], u[2], az)
+                 : face3<false>(u[1], u[2], u[3], az);
+  // the two x / y rows besides the own one that the +1/2 faces need
+  const int xa = PX ? r0 - BY : r0 + BY, xb = PX ? r0 + BY : r0 + 2 * BY;
+  const int ya = PY ? r0 - 1 : r0 + 1, yb = PY ? r0 + 1 : r0 + 2;
+#pragma unroll
+  for (int q = 0; q < CPT / 2; ++q) {
+    const int c = k0 / 2 + 2 + q;
+    const double2 XA = ld_swz(box, xa, c), XB = ld_swz(box, xb, c);
+    const double2 YA = ld_swz(box, ya, c), YB = ld_swz(box, yb, c);
+    double v[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int z = 2 * q + h + 2;  // index into u
+      const int zz = 2 * q + h;     // owned z - k0
+      const double u0 = u[z];
+      const double xa_ = h ? XA.y : XA.x, xb_ = h ? XB.y : XB.x;
+      const double ya_ = h ? YA.y : YA.x, yb_ = h ? YB.y : YB.x;
+      const double fx = PX ? face3<true>(xa_, u0, xb_, ax)
+                           : face3<false>(u0, xa_, xb_, ax);
+      const double fy = PY ? face3<true>(ya_, u0, yb_, ay)
+                           : face3<false>(u0, ya_, yb_, ay);
+      double fxm = __shfl_up_sync(0xffffffffu, fx, 8);
+      double fym = __shfl_up_sync(0xffffffffu, fy, 1);
+      if (i == i0) fxm = halo[zz * 8 + j];
+      if (j == 0) fym = halo[HXF + zz * 4 + (i - i0)];
+      const double fz_up = PZ ? face3<true>(u[z - 1], u0, u[z + 1], az)
+                              : face3<false>(u0, u[z + 1], u[z + 2], az);
+      // update_body order: ((dFx + dFy) + dFz), kernels.py:100-111
+      double div = __dsub_rn(fx, fxm);
+      div = __dadd_rn(div, __dsub_rn(fy, fym));
+      div = __dadd_rn(div, __dsub_rn(fz_up, fz));
+      fz = fz_up;
+      v[h] = __dsub_rn(u0, __dmul_rn(dt_dx, div));
+    }
+    const double2 w = make_double2(v[0], v[1]);
+    const int k = k0 + 2 * q;
+    *reinterpret_cast<double2*>(o + k) = w;
+    if (lo) *reinterpret_cast<double2*>(plo + k) = w;
+    if (hi) *reinterpret_cast<double2*>(phi + k) = w;
+  }
+}
+
 template <int CPT>
-constexpr int cols8_min_blocks() { return CPT == 8 ? 13 : 8; }
+constexpr int cols8s_min_blocks() { return CPT == 8 ? 12 : 8; }
+
+// one sub-grid g whose box is staged at `box`: coordinates, peer targets,
+// and the sign-specialised body
+template <int CPT>
+__device__ __forceinline__ void cols8s_subgrid(
+    const unsigned char* box, double* halo, int g, int m, double ax,
+    double ay, double az, double dt_dx, double* out, int64_t pyz, int pz,
+    double* peer_lo, double* peer_hi, int X, int mx) {
+  constexpr int N = 8;
+  const int bx = g / (m * m), by = (g / m) % m, bz = g % m;
+  const int col = threadIdx.x & 63, part = threadIdx.x >> 6;
+  const int i = col >> 3, j = col & 7, i0 = i & 4;
+  const int k0 = part * CPT;
+  const int64_t x = (int64_t)bx * N + i + HX, y = (int64_t)by * N + j + HY;
+  double* o = out + x * pyz + y * pz + (int64_t)bz * N + HZ;
+  const bool lo = peer_lo != nullptr && bx == 0 && i < HX;
+  const bool hi = peer_hi != nullptr && bx == mx - 1 && i >= N - HX;
+  double* plo = lo ? peer_lo + ((int64_t)X + HX + i) * pyz + y * pz +
+                         (int64_t)bz * N + HZ
+                   : nullptr;
+  double* phi = hi ? peer_hi + (int64_t)(i - (N - HX)) * pyz + y * pz +
+                         (int64_t)bz * N + HZ
+                   : nullptr;
+  const int sg = (ax >= 0.0 ? 1 : 0) | (ay >= 0.0 ? 2 : 0) | (az >= 0.0 ? 4 : 0);
+#define TF_COLS8S(S)                                                        \
+  case S:                                                                   \
+    cols8s_body<CPT, (S & 1) != 0, (S & 2) != 0, (S & 4) != 0>(             \
+        box, halo, i, j, k0, i0, ax, ay, az, dt_dx, o, lo, hi, plo, phi);   \
+    break;
+  switch (sg) {
+    TF_COLS8S(0) TF_COLS8S(1) TF_COLS8S(2) TF_COLS8S(3)
+    TF_COLS8S(4) TF_COLS8S(5) TF_COLS8S(6) TF_COLS8S(7)
+  }
+#undef TF_COLS8S
+}
 
 template <int CPT, bool DEV_IDS>
-__global__ void __launch_bounds__(cols8_threads<CPT>(), cols8_min_blocks<CPT>())
-    k_step_cols8(const __grid_constant__ CUtensorMap tmap,
-                 const int32_t* __restrict__ dev_ids,
-                 const __grid_constant__ TeamIds team, int m, double ax,
-                 double ay, double az, double dt_dx, double* __restrict__ out,
-                 int64_t pyz, int pz, double* peer_lo, double* peer_hi, int X,
-                 int mx) {
-  constexpr int N = 8, BY = COLS8_BXY;
-  // no static shared memory: the dynamic window starts 1024-B aligned, as
-  // the 128-B swizzle requires; the mbarrier sits after the box
+__global__ void __launch_bounds__(cols8_threads<CPT>(), cols8s_min_blocks<CPT>())
+    k_step_cols8s(const __grid_constant__ CUtensorMap tmap,
+                  const int32_t* __restrict__ dev_ids,
+                  const __grid_constant__ TeamIds team, int m, double ax,
+                  double ay, double az, double dt_dx, double* __restrict__ out,
+                  int64_t pyz, int pz, double* peer_lo, double* peer_hi, int X,
+                  int mx) {
+  constexpr int N = 8;
   extern __shared__ __align__(1024) unsigned char box[];
   uint64_t* bar = reinterpret_cast<uint64_t*>(box + COLS8_BOX_BYTES);
 
@@ -218,7 +353,6 @@ __global__ void __launch_bounds__(cols8_threads<CPT>(), cols8_min_blocks<CPT>())
   const int s = blockIdx.x;
   const int g = DEV_IDS ? (dev_ids ? dev_ids[s] : s) : team.id[s];
   const int bx = g / (m * m), by = (g / m) % m, bz = g % m;
-  // against the flow the box needs 2 cells, with it 1 (+1 origin if a < 0)
   const int sx = ax >= 0.0 ? 0 : 1, sy = ay >= 0.0 ? 0 : 1;
   if (threadIdx.x == 0) {
     mbar_init(bar);
@@ -227,62 +361,10 @@ __global__ void __launch_bounds__(cols8_threads<CPT>(), cols8_min_blocks<CPT>())
   }
   __syncthreads();
   mbar_wait(bar);
-
-  const int col = threadIdx.x & 63, part = threadIdx.x >> 6;
-  const int i = col >> 3, j = col & 7;
-  const int r0 = (i + 2 - sx) * BY + (j + 2 - sy);  // own box row
-  const int k0 = part * CPT;                        // first owned z
-  // own column, box z k0+2 .. k0+CPT+5 (chunks k0/2+1 ..): u[z - k0 - 2]
-  double u[CPT + 4];
-#pragma unroll
-  for (int q = 0; q < CPT / 2 + 2; ++q) {
-    const double2 v = ld_swz(box, r0, k0 / 2 + 1 + q);
-    u[2 * q] = v.x;
-    u[2 * q + 1] = v.y;
-  }
-  // the far neighbour an upwind face needs: -2 for a >= 0, +2 for a < 0
-  const int fx = ax >= 0.0 ? -2 : 2, fy = ay >= 0.0 ? -2 : 2;
-  const int64_t x = (int64_t)bx * N + i + HX, y = (int64_t)by * N + j + HY;
-  double* o = out + x * pyz + y * pz + (int64_t)bz * N + HZ;
-  // z flux through the face below owned cell k0
-  double fz = face(u[0], u[1], u[2], u[3], az);
-#pragma unroll
-  for (int q = 0; q < CPT / 2; ++q) {  // owned z pair k0+2q, k0+2q+1
-    const int c = k0 / 2 + 2 + q;      // its box chunk
-    const double2 xm = ld_swz(box, r0 - BY, c), xp = ld_swz(box, r0 + BY, c),
-                  xf = ld_swz(box, r0 + fx * BY, c);
-    const double2 ym = ld_swz(box, r0 - 1, c), yp = ld_swz(box, r0 + 1, c),
-                  yf = ld_swz(box, r0 + fy, c);
-    double v[2];
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int z = 2 * q + h + 2;  // index into u
-      const double u0 = u[z];
-      const double xmv = h ? xm.y : xm.x, xpv = h ? xp.y : xp.x,
-                   xfv = h ? xf.y : xf.x;
-      const double ymv = h ? ym.y : ym.x, ypv = h ? yp.y : yp.x,
-                   yfv = h ? yf.y : yf.x;
-      // update_body order: ((dFx + dFy) + dFz), kernels.py:100-111; the far
-      // value serves as um2 (a >= 0) or up2 (a < 0) — face() reads only one
-      double div = __dsub_rn(face(xmv, u0, xpv, xfv, ax),
-                             face(xfv, xmv, u0, xpv, ax));
-      div = __dadd_rn(div, __dsub_rn(face(ymv, u0, ypv, yfv, ay),
-                                     face(yfv, ymv, u0, ypv, ay)));
-      const double fz_up = face(u[z - 1], u0, u[z + 1], u[z + 2], az);
-      div = __dadd_rn(div, __dsub_rn(fz_up, fz));
-      fz = fz_up;
-      v[h] = __dsub_rn(u0, __dmul_rn(dt_dx, div));
-    }
-    const double2 w = make_double2(v[0], v[1]);
-    const int k = k0 + 2 * q;  // owned z of this pair
-    *reinterpret_cast<double2*>(o + k) = w;
-    if (peer_lo != nullptr && bx == 0 && i < HX)
-      *reinterpret_cast<double2*>(peer_lo + ((int64_t)X + HX + i) * pyz +
-                                  y * pz + (int64_t)bz * N + HZ + k) = w;
-    if (peer_hi != nullptr && bx == mx - 1 && i >= N - HX)
-      *reinterpret_cast<double2*>(peer_hi + (int64_t)(i - (N - HX)) * pyz +
-                                  y * pz + (int64_t)bz * N + HZ + k) = w;
-  }
+  double* halo = reinterpret_cast<double*>(box + COLS8S_HALO_OFF) +
+                 (threadIdx.x >> 5) * 12 * CPT;
+  cols8s_subgrid<CPT>(box, halo, g, m, ax, ay, az, dt_dx, out, pyz, pz,
+                      peer_lo, peer_hi, X, mx);
 }
 
 // Periodic y and z halo of every x layer (z after y so corners are right).
@@ -396,14 +478,14 @@ int field_map(const double* P, int X, int Gy, int Gz, int n, CUtensorMap* out) {
   const cuuint64_t pz = Gz + 2 * HZ, py = Gy + 2 * HY, px = X + 2 * HX;
   cuuint64_t dims[3] = {pz, py, px};
   cuuint64_t strides[2] = {pz * 8, pz * py * 8};
-  // n = 8: 11 x 11 x 16 (k_step_cols8); n = 16: the full (n+4)^2 (n+8)
+  // n = 8: 11 x 11 x 16 (k_step_cols8s); n = 16: the full (n+4)^2 (n+8)
   const cuuint32_t bxy = n == 8 ? COLS8_BXY : (cuuint32_t)(n + 4);
   cuuint32_t box[3] = {(cuuint32_t)(n + 8), bxy, bxy};
   cuuint32_t es[3] = {1, 1, 1};
   CUtensorMap m;
   if (fn(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(P), dims,
          strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-         // n = 8: z rows of exactly 128 B -> swizzled for k_step_cols8
+         // n = 8: z rows of exactly 128 B -> swizzled for k_step_cols8s
          n == 8 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
          CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
@@ -420,7 +502,7 @@ int launch_step(const CUtensorMap& map, const int32_t* dev_ids,
                 double az, double dt_dx, double* out, int X, int Gy, int Gz,
                 cudaStream_t st, int flags, double* peer_lo = nullptr,
                 double* peer_hi = nullptr) {
-  // n = 8: k_step_cols8 — one thread per column (CPT 8) for launches that
+  // n = 8: k_step_cols8s — one thread per column (CPT 8) for launches that
   // fill the GPU many times over (config 5: 206 vs 191 G cell-updates/s),
   // two per column (CPT 4) for team-sized launches, where per-sub-grid
   // latency decides (config 2 team plan: 41 vs 45 us).  n = 16: 128
@@ -428,17 +510,24 @@ int launch_step(const CUtensorMap& map, const int32_t* dev_ids,
   const int cpt = T >= 4096 ? 8 : 4;
   const int TH = N == 8 ? (cpt == 4 ? cols8_threads<4>() : cols8_threads<8>())
                         : 128;
-  constexpr size_t smem = N == 8 ? COLS8_BOX_BYTES + 8
-                                 : FGeo<N>::BOX * sizeof(double);
-  auto kern = N == 8 ? (cpt == 4 ? k_step_cols8<4, DEV_IDS>
-                                 : k_step_cols8<8, DEV_IDS>)
+  const size_t smem = N == 8 ? COLS8S_SMEM : FGeo<N>::BOX * sizeof(double);
+  auto kern = N == 8 ? (cpt == 4 ? k_step_cols8s<4, DEV_IDS>
+                                 : k_step_cols8s<8, DEV_IDS>)
                      : k_step_fused<N, 128, DEV_IDS>;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(
-        kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    attr = true;
+  {
+    // > 48 KB of dynamic shared memory (n = 16) needs the opt-in attribute;
+    // set once per kernel
+    static const void* done[4] = {};
+    const void* k = reinterpret_cast<const void*>(kern);
+    bool seen = false;
+    for (const void* d : done) seen |= d == k;
+    if (!seen) {
+      cudaError_t e = cudaFuncSetAttribute(
+          kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+      for (auto& d : done)
+        if (!d) { d = k; break; }
+    }
   }
   const int64_t pz = Gz + 2 * HZ, pyz = (int64_t)(Gy + 2 * HY) * pz;
   cudaLaunchConfig_t cfg = {};

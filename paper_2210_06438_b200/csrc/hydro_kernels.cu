@@ -565,7 +565,10 @@ int pool_map(const double* pool, int64_t slices, int n, CUtensorMap* out,
   CUresult r = fn(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4,
                   const_cast<double*>(pool), dims, strides, box, estr,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  // 64-B L2 promotion: each x plane of the box is one
+                  // contiguous 1.3 KB run, and 256-B promotion over-fetched
+                  // its ends (A/B on B200: +0.8% HBM fraction, 64 vs 256)
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_64B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return TF_E_INVALID;
   if (cache.size() > 256) cache.clear();

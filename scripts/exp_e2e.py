@@ -77,8 +77,8 @@ print("bit-exact:", np.array_equal(hout.numpy(), HO.advect_once(hin.numpy())))
 if len(sys.argv) > 1 and sys.argv[1] == "trace":
     import json
     from torch.profiler import ProfilerActivity, profile
-    for ch in (8, [1, 2, 3, 4, 3, 2, 1]):
-        p = HostPipeline(it, hin, hout, chunks=ch, down_ctas=32)
+    for ch in ("taper", [1, 2, 3, 4, 3, 2, 1]):
+        p = HostPipeline(it, hin, hout, chunks=ch, down_ctas=16)
         for _ in range(3):
             p.run()
         torch.cuda.synchronize()

@@ -28,11 +28,15 @@ def test_field_iteration_matches_reference(cuda, grid, n, vel, A, E):
     assert np.array_equal(it.owned().cpu().numpy(), HO.reference_step(f, vel))
 
 
-@pytest.mark.parametrize("vel", [(1.0, 1.0, 1.0), (-1.0, 0.5, -0.25),
-                                 (0.7, -1.3, 0.0), (-0.2, -0.9, 1.1)])
+SIGNED_VELOCITIES = [(1.0, 1.0, 1.0), (-1.0, 0.5, -0.25), (0.7, -1.3, 0.0),
+                     (-0.2, -0.9, 1.1), (0.6, 0.8, -1.0), (-0.5, -0.4, -0.3),
+                     (0.9, -0.1, -0.7), (-0.0, 1.2, 0.5)]
+
+
+@pytest.mark.parametrize("vel", SIGNED_VELOCITIES)
 def test_field_step_one_large_launch(cuda, vel):
     """One launch over >= 4096 sub-grids takes the one-thread-per-column
-    kernel shape (k_step_cols8<8>); team-sized launches take <4>.  Both
+    kernel shape (k_step_cols8s<8>); team-sized launches take <4>.  Both
     bit-identical, every sign combination of the velocity (the swizzled box
     origin shifts against the flow)."""
     import torch
@@ -44,6 +48,21 @@ def test_field_step_one_large_launch(cuda, vel):
         it.halo(True)
         it.step_ids(None, it.S)      # one launch, 4096 sub-grids
         it.swap()
+    torch.cuda.synchronize()
+    assert np.array_equal(it.owned().cpu().numpy(), HO.reference_step(f, vel))
+
+
+@pytest.mark.parametrize("vel", SIGNED_VELOCITIES)
+def test_field_step_team_launches_every_sign(cuda, vel):
+    """Team-sized launches (two threads per column) for all eight velocity
+    sign combinations; strided teams so warps see scattered sub-grids."""
+    import torch
+    from paper_2210_06438_b200.field import FieldIteration
+    f = HO.stress_field(64)
+    it = FieldIteration(64, 8, vel, max_team=64, executors=3)
+    it.load(torch.from_numpy(f).to(cuda))
+    for _ in range(3):
+        it.step()
     torch.cuda.synchronize()
     assert np.array_equal(it.owned().cpu().numpy(), HO.reference_step(f, vel))
 
