@@ -330,6 +330,15 @@ int tf_field_pad_f64(const double* field, int32_t X, int32_t Gy, int32_t Gz,
                      double* padded, tf_stream_t stream);
 int tf_field_unpad_f64(const double* padded, int32_t X, int32_t Gy,
                        int32_t Gz, double* field, tf_stream_t stream);
+/* Padded layers [first, first+count) (x in padded coordinates, the x halo
+ * included) written in full — interior AND periodic y/z halos — straight
+ * from a dense (X, Gy, Gz) field: padded (px, py, pz) = field((px-2) mod X,
+ * (py-2) mod Gy, (pz-4) mod Gz).  One launch in place of pad + y/z halo +
+ * x wrap for a chunk of the host pipeline (scenario.py:124-142 periodic
+ * ghosts).  Gy, Gz even.                                                    */
+int tf_field_pad_halo_f64(const double* field, int32_t X, int32_t Gy,
+                          int32_t Gz, double* padded, int32_t first,
+                          int32_t count, tf_stream_t stream);
 /* Zero-copy download of the interior into a PINNED host field (cudaHostAlloc /
  * torch pin_memory; TF_E_INVALID otherwise): the kernel's own posted PCIe
  * writes, `ctas` CTAs of 256 threads, Gz even, host_field 16-B aligned.

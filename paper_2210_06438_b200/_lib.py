@@ -106,6 +106,8 @@ SIGNATURES = {
                                            _p]),
     "tf_field_halo_xwrap_f64": (C.c_int, [_p, _i32, _i32, _i32, _i32, _p]),
     "tf_field_pad_f64": (C.c_int, [_p, _i32, _i32, _i32, _p, _p]),
+    "tf_field_pad_halo_f64": (C.c_int, [_p, _i32, _i32, _i32, _p, _i32, _i32,
+                                        _p]),
     "tf_field_unpad_f64": (C.c_int, [_p, _i32, _i32, _i32, _p, _p]),
     "tf_field_unpad_host_f64": (C.c_int, [_p, _i32, _i32, _i32, _p, _i32,
                                           _p]),

@@ -413,6 +413,28 @@ __global__ void k_pad_io(double* __restrict__ field, double* __restrict__ P,
   }
 }
 
+// Whole padded layers (interior + periodic y/z halos, x wrapped) from a
+// dense field, two cells per thread (HZ and Gz even: a pair never straddles
+// the z wrap).
+__global__ void k_pad_halo(const double* __restrict__ field,
+                           double* __restrict__ P, int X, int Gy, int Gz,
+                           int first, int count) {
+  const int py = Gy + 2 * HY, pz = Gz + 2 * HZ, hz = pz / 2;
+  const int64_t total = (int64_t)count * py * hz;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int px = first + (int)(t / ((int64_t)py * hz));
+    const int y = (int)((t / hz) % py), z = 2 * (int)(t % hz);
+    int fx = (px - HX) % X, fy = (y - HY) % Gy, fz = (z - HZ) % Gz;
+    fx += fx < 0 ? X : 0;
+    fy += fy < 0 ? Gy : 0;
+    fz += fz < 0 ? Gz : 0;
+    const double2 v = *reinterpret_cast<const double2*>(
+        field + ((int64_t)fx * Gy + fy) * Gz + fz);
+    *reinterpret_cast<double2*>(P + ((int64_t)px * py + y) * pz + z) = v;
+  }
+}
+
 // Zero-copy download: owned cells of the padded field straight into a
 // pinned host field over PCIe (GPU-initiated posted writes, 16 B per
 // thread, z rows contiguous on both sides).  A small grid on its own stream
@@ -723,6 +745,19 @@ int tf_field_pad_f64(const double* field, int32_t X, int32_t Gy, int32_t Gz,
   if (!field || !padded || X < 1 || Gy < 1 || Gz < 1) return TF_E_INVALID;
   k_pad_io<<<grid_for((int64_t)X * Gy * Gz), 256, 0, (cudaStream_t)stream>>>(
       const_cast<double*>(field), padded, X, Gy, Gz, 0);
+  return cudaGetLastError();
+}
+
+int tf_field_pad_halo_f64(const double* field, int32_t X, int32_t Gy,
+                          int32_t Gz, double* padded, int32_t first,
+                          int32_t count, tf_stream_t stream) {
+  if (!field || !padded || X < 1 || Gy < HY || Gz < HZ || (Gy & 1) ||
+      (Gz & 1) || first < 0 || count < 0 || first + count > X + 2 * HX)
+    return TF_E_INVALID;
+  if (count == 0) return 0;
+  const int64_t work = (int64_t)count * (Gy + 2 * HY) * ((Gz + 2 * HZ) / 2);
+  k_pad_halo<<<grid_for(work), 256, 0, (cudaStream_t)stream>>>(
+      field, padded, X, Gy, Gz, first, count);
   return cudaGetLastError();
 }
 

@@ -252,17 +252,17 @@ class FieldIteration(_FieldBase):
         launches = 0
         for i, rs in enumerate(ranges):
             comp.wait_event(ev_up[i])
-            for lo, hi in rs:
-                _lib.check(lib.tf_field_pad_f64(
-                    dev_in.data_ptr() + 8 * lo * plane, hi - lo, G, G,
-                    P.data_ptr() + 8 * lo * lay_elems, cs), "tf_field_pad_f64")
-                _lib.check(lib.tf_field_halo_layers_f64(
-                    P.data_ptr(), X, G, G, lo + HX, hi - lo, cs),
-                    "tf_field_halo_layers_f64")
-                launches += 3
-            if i == 0:   # periodic x halos: both sources landed with upload 0
-                _lib.check(lib.tf_field_halo_xwrap_f64(P.data_ptr(), X, G, G,
-                                                       3, cs), "xwrap")
+            # the chunk's padded layers in full (interior, periodic y/z
+            # halos, and for chunk 0 both periodic x halos: their sources,
+            # the first and last HX planes, landed with upload 0)
+            lo, hi = rs[-1]
+            spans = [(0, hi + HX), (X, 2 * HX)] if i == 0 else \
+                [(lo + HX, hi - lo)]
+            for first, count in spans:
+                _lib.check(lib.tf_field_pad_halo_f64(
+                    dev_in.data_ptr(), X, G, G, P.data_ptr(), first, count,
+                    cs), "tf_field_pad_halo_f64")
+                launches += 1
             a, b = start[i], start[i + 1]
             ids = pipe["ids"].get((a, b))
             if ids is None:
