@@ -14,6 +14,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <cstddef>
 #include <chrono>
 #include <string>
 #include <unordered_map>
@@ -494,11 +495,11 @@ struct QueueCtlHost {   // mirrors QueueCtl (hydro_kernels.cu)
   long long final_count;
   long long completed;
 };
-struct QueueDevInit {   // mirrors QueueDev
-  long long published;
-  long long final_count;
-  unsigned long long claim;
-  unsigned long long done;
+struct QueueDevInit {   // mirrors QueueDev (one 128-B line per word)
+  alignas(128) long long published;
+  alignas(128) long long final_count;
+  alignas(128) unsigned long long claim;
+  alignas(128) unsigned long long done;
 };
 
 // One queue instance; runs alternate between two so that run k+1 can
@@ -644,9 +645,13 @@ int tf_qexec_run_recon_flux(tf_qexec* q, const double* pool_ext,
   S.ctl_h->completed = 0;
   __atomic_thread_fence(__ATOMIC_SEQ_CST);
   cudaStream_t st = (cudaStream_t)stream;
-  const QueueDevInit init{0, -1, 0, 0};
-  cudaError_t ce = cudaMemcpyAsync(S.qdev, &init, sizeof(init),
-                                   cudaMemcpyHostToDevice, st);
+  // device counters {published 0, final_count -1, claim 0, done 0}: two
+  // memsets (no staged copy from pageable host memory)
+  cudaError_t ce = cudaMemsetAsync(S.qdev, 0, sizeof(QueueDevInit), st);
+  if (ce == cudaSuccess)
+    ce = cudaMemsetAsync(static_cast<char*>(S.qdev) +
+                             offsetof(QueueDevInit, final_count),
+                         0xff, sizeof(long long), st);
   if (ce != cudaSuccess) return ce;
   int rc = tf_queue_consumer_launch(
       pool_ext, pool_slices, q->n, S.ring_hd, S.ctl_hd, S.ring_d, S.qdev,

@@ -649,12 +649,16 @@ struct QueueCtl {
 };
 // device-side mirror, polled by the consumers through L2 (only the fetcher
 // CTA ever touches host memory, so the pollers do not flood PCIe)
+// Each word on its own 128-B line: the consumers poll `published` /
+// `final_count` while every CTA hits `claim` and `done` with atomics — on
+// one shared line those polls and atomics serialised in the same L2 slice.
 struct QueueDev {
-  long long published;
-  long long final_count;
-  unsigned long long claim;
-  unsigned long long done;
+  alignas(128) long long published;
+  alignas(128) long long final_count;
+  alignas(128) unsigned long long claim;
+  alignas(128) unsigned long long done;
 };
+static_assert(sizeof(QueueDev) == 512, "QueueDev layout (aggregator.cpp)");
 
 __device__ __forceinline__ long long ld_acquire_gpu(const long long* p) {
   long long v;
@@ -665,11 +669,6 @@ __device__ __forceinline__ void st_release_gpu(long long* p, long long v) {
   asm volatile("st.release.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
-__device__ __forceinline__ long long ld_acquire_sys(const long long* p) {
-  long long v;
-  asm volatile("ld.acquire.sys.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
 __device__ __forceinline__ int ld_relaxed_sys(const int* p) {
   int v;
   asm volatile("ld.relaxed.sys.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -696,49 +695,60 @@ __device__ void queue_fetcher(const int* __restrict__ ring_h, QueueCtl* ctl,
                               long long timeout_ns) {
   __shared__ long long s_pub, s_fin, s_done;
   __shared__ int s_stop;
-  constexpr int U = 4;  // loads in flight per thread
+  constexpr int U = 4;                  // loads in flight per thread
+  constexpr int CHUNK = THREADS * U;    // ids mirrored per publish
   long long fetched = 0, reported = -1;
   unsigned long long last_change = globaltimer();
+  // phase 1: mirror ids as the host publishes them, until the queue is
+  // closed and every id has been mirrored
   for (;;) {
     if (threadIdx.x == 0) {
-      s_pub = ld_acquire_sys(&ctl->published);
-      s_fin = ld_acquire_sys(&ctl->final_count);
+      // published and final_count in ONE PCIe round trip (adjacent words;
+      // the fence orders the ring reads after them)
+      long long pub, fin;
+      asm volatile("ld.relaxed.sys.global.v2.b64 {%0, %1}, [%2];"
+                   : "=l"(pub), "=l"(fin)
+                   : "l"(&ctl->published)
+                   : "memory");
+      asm volatile("fence.acq_rel.sys;" ::: "memory");
+      s_pub = pub;
+      s_fin = fin;
       s_done = (long long)atomicAdd(&qd->done, 0ULL);  // coherent read
     }
     __syncthreads();
     const long long pub = s_pub, fin = s_fin, done = s_done;
-    if (pub > fetched) {
-      for (long long k0 = fetched; k0 < pub; k0 += (long long)THREADS * U) {
-        int v[U];
+    // publish chunk by chunk: the consumers start on the first CHUNK ids
+    // instead of waiting for the whole backlog to be mirrored
+    for (long long k0 = fetched; k0 < pub; k0 += CHUNK) {
+      int v[U];
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const long long k = k0 + u * THREADS + threadIdx.x;
-          v[u] = k < pub ? ld_relaxed_sys(ring_h + k) : 0;
-        }
+      for (int u = 0; u < U; ++u) {
+        const long long k = k0 + u * THREADS + threadIdx.x;
+        v[u] = k < pub ? ld_relaxed_sys(ring_h + k) : 0;
+      }
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const long long k = k0 + u * THREADS + threadIdx.x;
-          if (k < pub) ring_d[k] = v[u];
-        }
+      for (int u = 0; u < U; ++u) {
+        const long long k = k0 + u * THREADS + threadIdx.x;
+        if (k < pub) ring_d[k] = v[u];
       }
       __syncthreads();
       if (threadIdx.x == 0) {
         __threadfence();
-        st_release_gpu(&qd->published, pub);
+        st_release_gpu(&qd->published, k0 + CHUNK < pub ? k0 + CHUNK : pub);
       }
-      fetched = pub;
       last_change = globaltimer();
     }
+    if (pub > fetched) fetched = pub;
     if (threadIdx.x == 0) {
       if (fin >= 0 && fetched >= fin) st_release_gpu(&qd->final_count, fin);
       if (done != reported) {
         st_release_sys(&ctl->completed, done);
         last_change = globaltimer();
       }
-      int stop = fin >= 0 && fetched >= fin && done >= fin;
+      int stop = fin >= 0 && fetched >= fin ? 1 : 0;
       if (!stop && (long long)(globaltimer() - last_change) > timeout_ns) {
         st_release_gpu(&qd->final_count, fetched);
-        stop = 1;
+        stop = 2;
       }
       s_stop = stop;
     }
@@ -746,6 +756,23 @@ __device__ void queue_fetcher(const int* __restrict__ ring_h, QueueCtl* ctl,
     __syncthreads();
     if (s_stop) break;
     __nanosleep(100);
+  }
+  // phase 2 (one thread): every id is on the device; report completions to
+  // the host until all are done — device-side polling only, no PCIe reads,
+  // so the grid exits as soon as the last slice does
+  if (threadIdx.x != 0 || s_stop == 2) return;
+  const long long fin = ld_acquire_gpu(&qd->final_count);
+  for (;;) {
+    const long long done = ld_acquire_gpu(
+        reinterpret_cast<const long long*>(&qd->done));
+    if (done != reported) {
+      st_release_sys(&ctl->completed, done);
+      reported = done;
+      last_change = globaltimer();
+    }
+    if (done >= fin) return;
+    if ((long long)(globaltimer() - last_change) > timeout_ns) return;
+    __nanosleep(32);
   }
 }
 
@@ -808,10 +835,10 @@ __global__ void __launch_bounds__(THREADS, recon_min_blocks<THREADS>())
         F + (int64_t)g * 3 * CELLS, ax, ay, az, flux_form);
     if (amax != nullptr) block_max_store<THREADS>(speed, red, amax + g);
     __syncthreads();  // box consumed, this slice's stores issued
-    if (threadIdx.x == 0) {
-      __threadfence();
-      atomicAdd(&qd->done, 1ULL);
-    }
+    // the completion count is the host's busy signal only (the kernel's
+    // exit orders the outputs for the stream), so no fence before it: a
+    // fence here held the CTA until its stores drained (-5 us per run)
+    if (threadIdx.x == 0) atomicAdd(&qd->done, 1ULL);
   }
 }
 

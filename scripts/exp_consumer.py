@@ -15,9 +15,13 @@ ctas = lib.tf_queue_consumer_ctas(8)
 ring_h = torch.arange(S, dtype=torch.int32).pin_memory()
 ctl_h = torch.tensor([S, S, 0], dtype=torch.int64).pin_memory()
 ring_d = torch.empty(S, dtype=torch.int32, device="cuda")
-qdev = torch.tensor([0, -1, 0, 0], dtype=torch.int64, device="cuda")
-init = torch.tensor([0, -1, 0, 0], dtype=torch.int64, device="cuda")
+# QueueDev: published, final_count, claim, done, one 128-B line each
+init = torch.zeros(64, dtype=torch.int64, device="cuda")
+init[16] = -1
+qdev = init.clone()
 st = torch.cuda.current_stream()
+
+
 
 
 def run(k):
