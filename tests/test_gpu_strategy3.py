@@ -162,3 +162,29 @@ def test_realtime_executor_bit_exact(cuda, cfg2, A, E):
     assert max(st["size_histogram"]) <= A
     assert np.array_equal(F.cpu().numpy(), oF)
     assert np.array_equal(um.cpu().numpy(), oum)
+
+
+@pytest.mark.parametrize("n,vel", [(16, (-0.7, 1.3, 0.2)),
+                                   (8, (0.4, -0.9, -1.1))])
+def test_queue_executor_other_shapes(cuda, n, vel):
+    """The device queue for 16^3 sub-grids (single-buffered consumer) and
+    for negative velocity components, stress field, scattered arrivals."""
+    import torch
+    from paper_2210_06438_b200.strategy3 import QueueExecutor, default_parents
+    grid = 64
+    hp = HO.make_pool(HO.stress_field(grid), n)
+    HO.exchange_ghosts_pool(hp, n, grid // n)
+    oum, oup, oF = HO.recon_flux_batch(hp, n, vel)
+    pool = torch.from_numpy(hp).to(cuda)
+    S = pool.shape[0]
+    q = QueueExecutor("flux", 8, default_parents(S, 8), n)
+    um, up, F = _outs(S, n, cuda)
+    amax = torch.zeros(S, dtype=torch.float64, device=cuda)
+    q.run(pool, vel, np.random.default_rng(3).permutation(S), um, up, F,
+          amax=amax)
+    torch.cuda.synchronize()
+    assert q.completed() == S
+    assert np.array_equal(um.cpu().numpy(), oum)
+    assert np.array_equal(up.cpu().numpy(), oup)
+    assert np.array_equal(F.cpu().numpy(), oF)
+    assert bool((amax == max(abs(v) for v in vel)).all())
