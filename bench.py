@@ -578,13 +578,20 @@ def cfg5_leg(args, world, rank, local, peak):
             "frac": fused_bytes / (ms * 1e-3) / 1e9 / peak,
             "traffic": ncu_traffic_per_launch(
                 part.subgrids, "r01_ncu_step_fused_cfg5g256.txt"),
+            # the field itself read once and written once (16 B per cell):
+            # the DRAM floor of the fused step if every halo re-read hits L2
+            "unique_dram_frac": part.subgrids * 16 * n ** 3
+            / (ms * 1e-3) / 1e9 / peak,
             "note": "fused step, SURVEY §8(d) B_step = 8[(n+2)^3 + "
                     "6(n+2)^2 + n^3] = 16 896 B per 8^3 sub-grid; halo "
                     "refresh and exchange inside the step. frac can exceed "
                     "1: B_step counts each sub-grid's halo reads, which the "
                     "padded-field layout serves from L2 (traffic = DRAM "
                     "bytes per step-kernel launch from the ncu capture at "
-                    "grid 256, scaled: ~7.2 KB per sub-grid)"},
+                    "grid 256, scaled: ~7.2 KB per sub-grid). "
+                    "unique_dram_frac = 16 B per cell (field in + out) / "
+                    "step time / peak: the DRAM floor's fraction; the "
+                    "kernel is latency / L2-bound, DESIGN.md §4"},
         "materialising_path": {
             "ms_per_step": ms_pool,
             "value": rate(S_total, n, ms_pool),
