@@ -47,6 +47,45 @@ k(const double2* __restrict__ in, double2* __restrict__ out, int S,
     slice(in, out, blockIdx.x, s);
   } else if (MODE == 1) {
     for (int b = blockIdx.x; b < S; b += gridDim.x) slice(in, out, b, s);
+  } else if (MODE == 5) {
+    // dynamic claim, double-buffered read: the next slice's 16 KB is read
+    // (cp.async into the other buffer) while this slice's 72 KB are written
+    __shared__ double2 s2[R2];
+    double2* buf[2] = {s, s2};
+    __shared__ int nxt2;
+    if (threadIdx.x == 0) next = (int)atomicAdd(claim, 1u);
+    __syncthreads();
+    int b = next, t = 0;
+    if (b < S)
+      for (int i = threadIdx.x; i < R2; i += 512) buf[0][i] = in[(int64_t)b * R2 + i];
+    while (b < S) {
+      if (threadIdx.x == 0) nxt2 = (int)atomicAdd(claim, 1u);
+      __syncthreads();
+      const int bn = nxt2;
+      double2* cur = buf[t & 1];
+      double2* nb = buf[(t + 1) & 1];
+      if (bn < S)
+        for (int i = threadIdx.x; i < R2; i += 512) {
+          const double2* src = in + (int64_t)bn * R2 + i;
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                           (unsigned)__cvta_generic_to_shared(nb + i)),
+                       "l"(src)
+                       : "memory");
+        }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+      const double2 acc = cur[threadIdx.x];
+      double2* o = out + (int64_t)b * W2;
+      for (int i = threadIdx.x; i < W2; i += 512) {
+        const double2 v = make_double2(acc.x + i, acc.y - i);
+        asm volatile("st.global.cs.v2.f64 [%0], {%1, %2};" ::"l"(o + i),
+                     "d"(v.x), "d"(v.y)
+                     : "memory");
+      }
+      asm volatile("cp.async.wait_all;" ::: "memory");
+      __syncthreads();
+      b = bn;
+      ++t;
+    }
   } else if (MODE == 2) {
     for (;;) {
       if (threadIdx.x == 0) next = (int)atomicAdd(claim, 1u);
@@ -119,6 +158,12 @@ int main() {
   printf("one CTA per slice (4096 CTAs): %.2f us\n", 1e3 * run<0>(in, out, S, S, claim));
   printf("persistent static (%d CTAs): %.2f us\n", P, 1e3 * run<1>(in, out, S, P, claim));
   printf("persistent claim  (%d CTAs): %.2f us\n", P, 1e3 * run<2>(in, out, S, P, claim));
+  printf("claim + double-buffered read (%d CTAs): %.2f us\n", P, 1e3 * run<5>(in, out, S, P, claim));
+  {
+    int ps = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, k<5>, 512, 0);
+    printf("  (mode 5 occupancy %d CTAs/SM)\n", ps);
+  }
   printf("claim+acquire poll+ring (%d CTAs): %.2f us\n", P, 1e3 * run<3>(in, out, S, P, claim));
   printf("claim+relaxed poll+cg ring (%d CTAs): %.2f us\n", P, 1e3 * run<4>(in, out, S, P, claim));
   printf("err: %s\n", cudaGetErrorString(cudaDeviceSynchronize()));
