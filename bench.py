@@ -710,6 +710,8 @@ def main():
                     "the committed ncu --set full capture of the same kernel "
                     "(profiles/r01_ncu_recon_flux_single.txt), per slice x "
                     "team size",
+            # also against the 8 TB/s HBM3e spec figure
+            "spec_frac_8tbs": achieved / 8000.0,
             "kernel_alone": {
                 "ms": ms_single,
                 "achieved": bytes_step / (ms_single * 1e-3) / 1e9,
