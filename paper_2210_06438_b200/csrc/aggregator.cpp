@@ -509,7 +509,8 @@ struct QueueSlot {
   void* ctl_hd = nullptr;          // its device alias
   int32_t* ring_h = nullptr;       // mapped pinned
   int32_t* ring_hd = nullptr;      // its device alias
-  int32_t* ring_d = nullptr;       // device mirror
+  int64_t* ring_d = nullptr;       // device mirror, tagged (epoch << 32 | id)
+  int32_t epoch = 0;               // last epoch launched on this slot
   int64_t ring_cap = 0;
   void* qdev = nullptr;            // QueueDevInit on the device
   cudaEvent_t done_ev = nullptr;
@@ -634,7 +635,10 @@ int tf_qexec_run_recon_flux(tf_qexec* q, const double* pool_ext,
       e = cudaHostGetDevicePointer(reinterpret_cast<void**>(&S.ring_hd),
                                    S.ring_h, 0);
     if (e == cudaSuccess)
-      e = cudaMalloc(reinterpret_cast<void**>(&S.ring_d), sizeof(int32_t) * cap);
+      e = cudaMalloc(reinterpret_cast<void**>(&S.ring_d), sizeof(int64_t) * cap);
+    // no stale entry may carry a live epoch
+    if (e == cudaSuccess) e = cudaMemset(S.ring_d, 0, sizeof(int64_t) * cap);
+    S.epoch = 0;
     if (e != cudaSuccess) return e;
     S.ring_cap = cap;
   }
@@ -655,7 +659,7 @@ int tf_qexec_run_recon_flux(tf_qexec* q, const double* pool_ext,
   if (ce != cudaSuccess) return ce;
   int rc = tf_queue_consumer_launch(
       pool_ext, pool_slices, q->n, S.ring_hd, S.ctl_hd, S.ring_d, S.qdev,
-      q->ctas, ax, ay, az, um, up, F, amax, flux_form,
+      q->ctas, ++S.epoch, ax, ay, az, um, up, F, amax, flux_form,
       /*timeout_ns=*/2000000000LL, stream);
   if (rc) return rc;
   ce = cudaEventRecord(S.done_ev, st);

@@ -660,6 +660,17 @@ struct QueueDev {
 };
 static_assert(sizeof(QueueDev) == 512, "QueueDev layout (aggregator.cpp)");
 
+__device__ __forceinline__ long long ld_relaxed_gpu(const long long* p) {
+  long long v;
+  asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned long long ld_relaxed_gpu_u64(
+    const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
 __device__ __forceinline__ long long ld_acquire_gpu(const long long* p) {
   long long v;
   asm volatile("ld.acquire.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
@@ -691,7 +702,8 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 // device mirror.
 template <int THREADS>
 __device__ void queue_fetcher(const int* __restrict__ ring_h, QueueCtl* ctl,
-                              int* __restrict__ ring_d, QueueDev* qd,
+                              unsigned long long* __restrict__ ring_d,
+                              QueueDev* qd, unsigned epoch,
                               long long timeout_ns) {
   __shared__ long long s_pub, s_fin, s_done;
   __shared__ int s_stop;
@@ -729,7 +741,10 @@ __device__ void queue_fetcher(const int* __restrict__ ring_h, QueueCtl* ctl,
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const long long k = k0 + u * THREADS + threadIdx.x;
-        if (k < pub) ring_d[k] = v[u];
+        // tagged entry: a consumer that sees its run's epoch in the slot
+        // has the id — no acquire (and no L1 invalidation) needed
+        if (k < pub)
+          ring_d[k] = ((unsigned long long)epoch << 32) | (unsigned)v[u];
       }
       __syncthreads();
       if (threadIdx.x == 0) {
@@ -780,7 +795,8 @@ template <int N, int THREADS>
 __global__ void __launch_bounds__(THREADS, recon_min_blocks<THREADS>())
     k_queue_consumer(const __grid_constant__ CUtensorMap tmap,
                      const int* __restrict__ ring_h, QueueCtl* ctl,
-                     int* __restrict__ ring_d, QueueDev* qd, double ax,
+                     unsigned long long* __restrict__ ring_d, QueueDev* qd,
+                     unsigned epoch, double ax,
                      double ay, double az, double* __restrict__ um,
                      double* __restrict__ up, double* __restrict__ F,
                      double* __restrict__ amax, int flux_form,
@@ -788,7 +804,7 @@ __global__ void __launch_bounds__(THREADS, recon_min_blocks<THREADS>())
   using G = Geo<N>;
   constexpr int CELLS = G::CELLS;
   if (blockIdx.x == 0) {
-    queue_fetcher<THREADS>(ring_h, ctl, ring_d, qd, timeout_ns);
+    queue_fetcher<THREADS>(ring_h, ctl, ring_d, qd, epoch, timeout_ns);
     return;
   }
   extern __shared__ __align__(128) double sbox[];
@@ -804,11 +820,14 @@ __global__ void __launch_bounds__(THREADS, recon_min_blocks<THREADS>())
       const unsigned long long t0 = globaltimer();
       int g;
       for (;;) {
-        if (k < ld_acquire_gpu(&qd->published)) {
-          g = ring_d[k];
+        // relaxed polls only: an acquire would invalidate the SM's L1
+        // (CCTL.IVALL) once per slice, under every CTA's spilled registers
+        const unsigned long long v = ld_relaxed_gpu_u64(ring_d + k);
+        if ((unsigned)(v >> 32) == epoch) {
+          g = (int)(unsigned)v;
           break;
         }
-        const long long fin = ld_acquire_gpu(&qd->final_count);
+        const long long fin = ld_relaxed_gpu(&qd->final_count);
         if (fin >= 0 && k >= fin) {
           g = -1;  // queue closed and drained
           break;
@@ -1073,13 +1092,14 @@ int tf_queue_consumer_ctas(int32_t n) {
 
 int tf_queue_consumer_launch(const double* pool_ext, int64_t pool_slices,
                              int32_t n, const int32_t* ring_h, void* ctl_h,
-                             int32_t* ring_d, void* qdev, int32_t ctas,
+                             int64_t* ring_d, void* qdev, int32_t ctas,
+                             int32_t epoch,
                              double ax, double ay, double az, double* um,
                              double* up, double* F, double* amax,
                              int32_t flux_form, int64_t timeout_ns,
                              tf_stream_t stream) {
   if (!valid_n(n) || !pool_ext || !ring_h || !ctl_h || !ring_d || !qdev ||
-      ctas < 1 || !um || !up || !F)
+      ctas < 1 || epoch < 1 || !um || !up || !F)
     return TF_E_INVALID;
   CUtensorMap map;
   int rc = pool_map(pool_ext, pool_slices, n, &map);
@@ -1091,12 +1111,13 @@ int tf_queue_consumer_launch(const double* pool_ext, int64_t pool_slices,
   // grid: the fetcher block + `ctas` consumers
   if (n == 8)
     k_queue_consumer<8, TH><<<ctas + 1, TH, Geo<8>::BOX * sizeof(double), st>>>(
-        map, ring_h, c, ring_d, q, ax, ay, az, um, up, F, amax, flux_form,
-        timeout_ns);
+        map, ring_h, c, reinterpret_cast<unsigned long long*>(ring_d), q,
+        (unsigned)epoch, ax, ay, az, um, up, F, amax, flux_form, timeout_ns);
   else
     k_queue_consumer<16, TH>
         <<<ctas + 1, TH, Geo<16>::BOX * sizeof(double), st>>>(
-            map, ring_h, c, ring_d, q, ax, ay, az, um, up, F, amax, flux_form,
+            map, ring_h, c, reinterpret_cast<unsigned long long*>(ring_d), q,
+            (unsigned)epoch, ax, ay, az, um, up, F, amax, flux_form,
             timeout_ns);
   return cudaGetLastError();
 }

@@ -14,7 +14,7 @@ S = wl.S
 ctas = lib.tf_queue_consumer_ctas(8)
 ring_h = torch.arange(S, dtype=torch.int32).pin_memory()
 ctl_h = torch.tensor([S, S, 0], dtype=torch.int64).pin_memory()
-ring_d = torch.empty(S, dtype=torch.int32, device="cuda")
+ring_d = torch.zeros(S, dtype=torch.int64, device="cuda")  # tagged entries
 # QueueDev: published, final_count, claim, done, one 128-B line each
 init = torch.zeros(64, dtype=torch.int64, device="cuda")
 init[16] = -1
@@ -29,7 +29,7 @@ def run(k):
     ctl_h[2] = 0
     rc = lib.tf_queue_consumer_launch(
         wl.pools[k % 2].data_ptr(), S, 8, ring_h.data_ptr(), ctl_h.data_ptr(),
-        ring_d.data_ptr(), qdev.data_ptr(), ctas, 1.0, 1.0, 1.0,
+        ring_d.data_ptr(), qdev.data_ptr(), ctas, k + 1, 1.0, 1.0, 1.0,
         wl.um.data_ptr(), wl.up.data_ptr(), wl.F.data_ptr(),
         wl.amax.data_ptr(), 0, 2_000_000_000, st.cuda_stream)
     assert rc == 0, rc
