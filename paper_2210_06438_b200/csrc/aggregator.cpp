@@ -26,20 +26,22 @@ namespace {
 
 // zlib crc32 (IEEE 802.3, reflected 0xEDB88320) — the reference derives each
 // region's lead executor from crc32(name) (aggregator.py:273).
-uint32_t crc32_ieee(const char* s) {
-  static uint32_t table[256];
-  static bool init = false;
-  if (!init) {
+struct Crc32Table {
+  uint32_t t[256];
+  Crc32Table() {
     for (uint32_t i = 0; i < 256; ++i) {
       uint32_t c = i;
       for (int k = 0; k < 8; ++k) c = (c & 1) ? 0xEDB88320u ^ (c >> 1) : c >> 1;
-      table[i] = c;
+      t[i] = c;
     }
-    init = true;
   }
+};
+
+uint32_t crc32_ieee(const char* s) {
+  static const Crc32Table table;  // thread-safe one-time init
   uint32_t c = 0xFFFFFFFFu;
   for (const unsigned char* p = (const unsigned char*)s; *p; ++p)
-    c = table[(c ^ *p) & 0xFFu] ^ (c >> 8);
+    c = table.t[(c ^ *p) & 0xFFu] ^ (c >> 8);
   return c ^ 0xFFFFFFFFu;
 }
 

@@ -518,6 +518,21 @@ int field_map(const double* P, int X, int Gy, int Gz, int n, CUtensorMap* out) {
   return 0;
 }
 
+// cudaFuncAttributeMaxDynamicSharedMemorySize, set once per kernel
+// (thread-safe: host threads may launch concurrently)
+int ensure_smem(const void* kern, size_t smem) {
+  static std::mutex mu;
+  static std::unordered_map<const void*, size_t> set;
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = set.find(kern);
+  if (it != set.end() && it->second >= smem) return 0;
+  const cudaError_t e = cudaFuncSetAttribute(
+      kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  set[kern] = smem;
+  return 0;
+}
+
 template <int N, bool DEV_IDS>
 int launch_step(const CUtensorMap& map, const int32_t* dev_ids,
                 const TeamIds& team, int T, int m, double ax, double ay,
@@ -536,21 +551,9 @@ int launch_step(const CUtensorMap& map, const int32_t* dev_ids,
   auto kern = N == 8 ? (cpt == 4 ? k_step_cols8s<4, DEV_IDS>
                                  : k_step_cols8s<8, DEV_IDS>)
                      : k_step_fused<N, 128, DEV_IDS>;
-  {
-    // > 48 KB of dynamic shared memory (n = 16) needs the opt-in attribute;
-    // set once per kernel
-    static const void* done[4] = {};
-    const void* k = reinterpret_cast<const void*>(kern);
-    bool seen = false;
-    for (const void* d : done) seen |= d == k;
-    if (!seen) {
-      cudaError_t e = cudaFuncSetAttribute(
-          kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      if (e != cudaSuccess) return e;
-      for (auto& d : done)
-        if (!d) { d = k; break; }
-    }
-  }
+  // > 48 KB of dynamic shared memory (n = 16) needs the opt-in attribute
+  int rc = ensure_smem(reinterpret_cast<const void*>(kern), smem);
+  if (rc) return rc;
   const int64_t pz = Gz + 2 * HZ, pyz = (int64_t)(Gy + 2 * HY) * pz;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)T);

@@ -592,13 +592,10 @@ int launch_recon(const CUtensorMap& map, const int32_t* dev_ids,
   constexpr int TH = recon_threads<N>();
   constexpr size_t smem = Geo<N>::BOX * sizeof(double);
   auto kern = k_recon_flux<N, TH, MODE, DEV_IDS>;
-  static bool attr_done = false;  // benign race: idempotent attribute set
-  if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(
-        kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    attr_done = true;
-  }
+  // set once per instantiation (a function-local static: thread-safe init)
+  static const cudaError_t attr = cudaFuncSetAttribute(
+      kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (attr != cudaSuccess) return attr;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)T);
   cfg.blockDim = dim3(TH);
@@ -1050,14 +1047,10 @@ int tf_recon_flux_ppm_f64(const double* pool_ext, int64_t pool_slices,
         map, ids, out_mode, ax, ay, az, um, up, F, amax, flux_form);
   } else {
     constexpr size_t smem = Geo<16>::EXT3 * sizeof(double);
-    static bool attr = false;
-    if (!attr) {
-      cudaError_t e = cudaFuncSetAttribute(
-          k_recon_flux_ppm<16, TH, true>,
-          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      if (e != cudaSuccess) return e;
-      attr = true;
-    }
+    static const cudaError_t attr = cudaFuncSetAttribute(
+        k_recon_flux_ppm<16, TH, true>,
+        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (attr != cudaSuccess) return attr;
     k_recon_flux_ppm<16, TH, true><<<T, TH, smem, st>>>(
         map, ids, out_mode, ax, ay, az, um, up, F, amax, flux_form);
   }
