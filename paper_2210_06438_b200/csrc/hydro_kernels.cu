@@ -593,9 +593,9 @@ int launch_recon(const CUtensorMap& map, const int32_t* dev_ids,
   constexpr size_t smem = Geo<N>::BOX * sizeof(double);
   auto kern = k_recon_flux<N, TH, MODE, DEV_IDS>;
   // set once per instantiation (a function-local static: thread-safe init)
-  static const cudaError_t attr = cudaFuncSetAttribute(
+  static const cudaError_t smem_attr = cudaFuncSetAttribute(
       kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (attr != cudaSuccess) return attr;
+  if (smem_attr != cudaSuccess) return smem_attr;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)T);
   cfg.blockDim = dim3(TH);
@@ -1047,10 +1047,10 @@ int tf_recon_flux_ppm_f64(const double* pool_ext, int64_t pool_slices,
         map, ids, out_mode, ax, ay, az, um, up, F, amax, flux_form);
   } else {
     constexpr size_t smem = Geo<16>::EXT3 * sizeof(double);
-    static const cudaError_t attr = cudaFuncSetAttribute(
+    static const cudaError_t smem_attr = cudaFuncSetAttribute(
         k_recon_flux_ppm<16, TH, true>,
         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (attr != cudaSuccess) return attr;
+    if (smem_attr != cudaSuccess) return smem_attr;
     k_recon_flux_ppm<16, TH, true><<<T, TH, smem, st>>>(
         map, ids, out_mode, ax, ay, az, um, up, F, amax, flux_form);
   }
