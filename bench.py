@@ -189,12 +189,19 @@ def max_over_ranks(world, x: float) -> float:
     return float(t.item())
 
 
-def timed(fn, steps, warmup, world, stream):
-    """W untimed steps, then EXACTLY `steps` steps between barrier+sync on
-    both sides, CUDA events on the launching stream; ms/step (max ranks)."""
+def timed(fn, steps, warmup, world, stream, settle_s: float = 0.02):
+    """W untimed steps (and at least `settle_s` of untimed work, so a short
+    measurement after host-side setup does not start on idle-lowered
+    clocks), then EXACTLY `steps` steps between barrier+sync on both sides,
+    CUDA events on the launching stream; ms/step (max over ranks)."""
     import torch
-    for k in range(warmup):
+    t_end = time.time() + settle_s
+    k = 0
+    while k < warmup or time.time() < t_end:
         fn(k)
+        k += 1
+        if k % 8 == 0:
+            torch.cuda.synchronize()
     torch.cuda.synchronize()
     barrier(world)
     t0 = torch.cuda.Event(enable_timing=True)
@@ -609,9 +616,13 @@ def main():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--max-team", type=int, default=128)
-    # one executor = the paper's strategy-3 configuration (all parents on one
-    # stream); with PDL between consecutive teams it is also the fastest
-    ap.add_argument("--executors", type=int, default=1)
+    # two executor streams, teams alternating between them with PDL inside
+    # each branch: as fast as one stream in a fresh process (33.8 vs 33.7 G)
+    # and robust to the process state a multi-stream program is always in —
+    # once any ordinary kernel has run on a non-default stream, a single
+    # PDL chain of team launches in a graph slows by 12% (33.7 -> 29.6 G)
+    # while two branches hold 33.4 G (scripts/exp_sweep_gap.py)
+    ap.add_argument("--executors", type=int, default=2)
     ap.add_argument("--mode", choices=("plan", "realtime", "single"),
                     default="plan")
     ap.add_argument("--no-sweep", action="store_true")
