@@ -289,11 +289,13 @@ def rate(S, n, ms):
 def run_sweep(wl, args, world, stream, peak):
     """Aggregation sweep 1..128 (plan-graph and real-time executor),
     strategy 2 (A=1 over many streams), strategy 1 (16^3, A=1)."""
-    out = {"aggregation": {}, "aggregation_4_executors": {}, "realtime": {},
+    out = {"aggregation": {}, "aggregation_1_executor": {},
+           "aggregation_4_executors": {}, "realtime": {},
            "strategy2": {}, "strategy1": {}}
     ks, kw = max(5, args.steps // 2), 3
     for A in (1, 4, 16, 64, 128):
         for key, E in (("aggregation", args.executors),
+                       ("aggregation_1_executor", 1),
                        ("aggregation_4_executors", 4)):
             step, nk, hist, _ = plan_runner(
                 wl, A, E, team_buffers=args.outputs == "team")
