@@ -304,7 +304,10 @@ def run_sweep(wl, args, world, stream, peak):
                 "cell_updates_per_s": rate(wl.S, wl.n, ms), "ms_per_iter": ms,
                 "launches": nk, "executors": E,
                 "hbm_frac": wl.S * b_alg(wl.n) / (ms * 1e-3) / (peak * 1e9)}
-        rstep, launches, ex = realtime_runner(wl, A, args.executors)
+        # the real-time launch-per-team executor on ONE stream (the paper's
+        # strategy-3 configuration; with more streams the starvation rule
+        # fires on every idle stream and most teams close solo)
+        rstep, launches, ex = realtime_runner(wl, A, 1)
         ms = timed(rstep, ks, kw, world, stream)
         st = ex.stats()
         out["realtime"][A] = {
