@@ -36,7 +36,8 @@ def _stale() -> bool:
     if not LIB.exists():
         return True
     built = LIB.stat().st_mtime
-    deps = [CSRC / s for s in SOURCES] + [ROOT / "include" / "taskfuse_b200.h"]
+    deps = [CSRC / s for s in SOURCES] + [ROOT / "include" / "taskfuse_b200.h",
+                                          CSRC / "sm100_common.cuh"]
     return any(p.stat().st_mtime > built for p in deps)
 
 

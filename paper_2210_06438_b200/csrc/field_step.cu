@@ -31,32 +31,12 @@
 #include <unordered_map>
 
 #include "../../include/taskfuse_b200.h"
+#include "sm100_common.cuh"
 
 namespace {
 
 constexpr int HX = 2, HY = 2, HZ = 4;  // halo widths of the padded field
 
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar))
-               : "memory");
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
-                   smem_u32(bar)),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar) {
-  asm volatile(
-      "{\n.reg .pred P1;\nLAB_WAIT:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], 0;\n"
-      "@P1 bra DONE;\nbra LAB_WAIT;\nDONE:\n}\n" ::"r"(smem_u32(bar))
-      : "memory");
-}
 __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map,
                                             int c0, int c1, int c2,
                                             uint64_t* bar) {
@@ -68,13 +48,6 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map,
       : "memory");
 }
 
-__device__ __forceinline__ double minmod(double a, double b) {
-  return (__dmul_rn(a, b) <= 0.0) ? 0.0 : ((fabs(a) < fabs(b)) ? a : b);
-}
-__device__ __forceinline__ double slope(const double* s, int b, int st) {
-  const double base = s[b];
-  return minmod(__dsub_rn(s[b + st], base), __dsub_rn(base, s[b - st]));
-}
 // flux of one face (kernels.py:73-93 for one axis): upwind F = a*up (a>=0)
 // or a*um of the next cell along the axis (a<0).  The update never reads
 // the np.roll wrap layer, so the "next" cell always exists in the box.
@@ -88,10 +61,6 @@ __device__ __forceinline__ double face_flux(const double* s, int b, int st,
   const double half = __dmul_rn(0.5, slope(s, bn, st));
   return __dmul_rn(a, __dsub_rn(s[bn], half));
 }
-
-struct TeamIds {
-  int32_t id[TF_MAX_TEAM];
-};
 
 template <int N>
 struct FGeo {
@@ -119,13 +88,13 @@ __global__ void __launch_bounds__(THREADS)
   const int g = DEV_IDS ? (dev_ids ? dev_ids[s] : s) : team.id[s];
   const int bx = g / (m * m), by = (g / m) % m, bz = g % m;
   if (threadIdx.x == 0) {
-    mbar_init(&bar);
+    mbar_init(&bar, 1);
     mbar_expect_tx(&bar, G::BOX * (uint32_t)sizeof(double));
     // padded coords of the box origin: global (b*n-2, b*n-2, b*n-4)
     tma_load_3d(sbox, &tmap, bz * N, by * N, bx * N, &bar);
   }
   __syncthreads();
-  mbar_wait(&bar);
+  mbar_wait(&bar, 0);
 
   // Each thread: its owned cells' 6 face fluxes straight from the box, then
   // update_body (kernels.py:100-111: x, y, z accumulation order, no FMA).
@@ -355,12 +324,12 @@ __global__ void __launch_bounds__(cols8_threads<CPT>(), cols8s_min_blocks<CPT>()
   const int bx = g / (m * m), by = (g / m) % m, bz = g % m;
   const int sx = ax >= 0.0 ? 0 : 1, sy = ay >= 0.0 ? 0 : 1;
   if (threadIdx.x == 0) {
-    mbar_init(bar);
+    mbar_init(bar, 1);
     mbar_expect_tx(bar, COLS8_BOX_BYTES);
     tma_load_3d(box, &tmap, bz * N, by * N + sy, bx * N + sx, bar);
   }
   __syncthreads();
-  mbar_wait(bar);
+  mbar_wait(bar, 0);
   double* halo = reinterpret_cast<double*>(box + COLS8S_HALO_OFF) +
                  (threadIdx.x >> 5) * 12 * CPT;
   cols8s_subgrid<CPT>(box, halo, g, m, ax, ay, az, dt_dx, out, pyz, pz,
@@ -455,20 +424,6 @@ __global__ void k_unpad_host(const double* __restrict__ P,
     const double2 v = *reinterpret_cast<const double2*>(P + p);
     *reinterpret_cast<double2*>(host + 2 * t) = v;
   }
-}
-
-PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-  static std::once_flag once;
-  std::call_once(once, [] {
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault,
-                                &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-  });
-  return fn;
 }
 
 struct Key {

@@ -30,6 +30,7 @@
 #include <unordered_map>
 
 #include "../../include/taskfuse_b200.h"
+#include "sm100_common.cuh"
 
 namespace {
 
@@ -47,40 +48,7 @@ struct Geo {
   static constexpr int OWN = N * N * N;
 };
 
-struct TeamIds {
-  int32_t id[TF_MAX_TEAM];
-};
-
 // ---------------------------------------------------------------- PTX glue
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)),
-               "r"(count)
-               : "memory");
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile(
-      "mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
-          smem_u32(bar)),
-      "r"(bytes)
-      : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
-  asm volatile(
-      "{\n"
-      ".reg .pred P1;\n"
-      "LAB_WAIT:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
-      "@P1 bra DONE;\n"
-      "bra LAB_WAIT;\n"
-      "DONE:\n"
-      "}\n" ::"r"(smem_u32(bar)),
-      "r"(phase)
-      : "memory");
-}
 __device__ __forceinline__ void tma_load_box(void* dst, const CUtensorMap* map,
                                              int c0, int c1, int c2, int c3,
                                              uint64_t* bar) {
@@ -94,20 +62,6 @@ __device__ __forceinline__ void tma_load_box(void* dst, const CUtensorMap* map,
 }
 
 // --------------------------------------------------------------- numerics
-// kernels.py:58-60 — product test first, then strict |a|<|b|.  NaN in the
-// product fails `<= 0` and NaN in |a| fails `<`, both yielding b, as numpy.
-__device__ __forceinline__ double minmod(double a, double b) {
-  return (__dmul_rn(a, b) <= 0.0) ? 0.0 : ((fabs(a) < fabs(b)) ? a : b);
-}
-
-// Slope at stencil-box index b along stride st (kernels.py:76-79):
-// sigma = minmod(w[+e] - base, base - w[-e]).
-__device__ __forceinline__ double slope(const double* __restrict__ s, int b,
-                                        int st) {
-  const double base = s[b];
-  return minmod(__dsub_rn(s[b + st], base), __dsub_rn(base, s[b - st]));
-}
-
 __device__ __forceinline__ double warp_max(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
@@ -511,20 +465,6 @@ __global__ void k_reduce(const int32_t* __restrict__ ids, int T, int out_mode,
 }
 
 // ------------------------------------------------------------ host side
-PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-  static std::once_flag once;
-  std::call_once(once, [] {
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault,
-                                &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-  });
-  return fn;
-}
-
 struct MapKey {
   const void* ptr;
   int64_t slices;
