@@ -273,13 +273,35 @@ def realtime_runner(wl, max_team, executors, parents=None, overlap=False):
     return step, launches, ex
 
 
-def single_runner(wl):
+def single_runner(wl, reconstruction="minmod", flux_form=0):
     from paper_2210_06438_b200 import ops
 
     def step(k):
         ops.recon_flux(wl.pools[k % len(wl.pools)], wl.n, VELOCITY, wl.um,
-                       wl.up, wl.F, out_mode=1, amax=wl.amax)
+                       wl.up, wl.F, out_mode=1, amax=wl.amax,
+                       flux_form=flux_form, reconstruction=reconstruction)
     return step
+
+
+def scheme_legs(wl, steps, warmup, world, stream, peak):
+    """north_star's named kernels on config 2, one launch of all slices:
+    Kurganov-Tadmor flux form (1e-12 of the reference's upwind flux) and
+    PPM reconstruction (parity unpinned).  PPM's stencil
+    reaches the ghost depth 3, so its algorithmic read is the whole 14^3
+    box: 8 [E^3 + 9 (n+2)^3] B per sub-grid."""
+    n = wl.n
+    c, e = n + 2, n + 6
+    out = {}
+    for name, rec, ff, per in (
+            ("minmod_upwind", "minmod", 0, b_alg(n)),
+            ("minmod_kt", "minmod", 1, b_alg(n)),
+            ("ppm_upwind", "ppm", 0, 8 * (e ** 3 + 9 * c ** 3)),
+            ("ppm_kt", "ppm", 1, 8 * (e ** 3 + 9 * c ** 3))):
+        ms = timed(single_runner(wl, rec, ff), steps, warmup, world, stream)
+        out[name] = {"cell_updates_per_s": rate(wl.S, n, ms),
+                     "ms_per_iter": ms, "alg_bytes_per_subgrid": per,
+                     "hbm_frac": wl.S * per / (ms * 1e-3) / 1e9 / peak}
+    return out
 
 
 def rate(S, n, ms):
@@ -752,6 +774,8 @@ def main():
     # in, one hydro iteration = reconstruct + flux + update of every
     # sub-grid, pinned host field out), transfers overlapped with compute
     line["e2e"] = dict(line["fused_full_iteration"]["e2e_pipelined"])
+    line["schemes_one_launch"] = scheme_legs(wl, max(10, args.steps // 2), 3,
+                                             world, stream, peak)
     line["e2e_faces"] = {"value": rate(total_S, wl.n, f_ms), "unit": UNIT,
                          "h2d_bytes_per_step": fbi,
                          "d2h_bytes_per_step": fbo, "ms_per_step": f_ms,

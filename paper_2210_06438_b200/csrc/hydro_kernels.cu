@@ -247,12 +247,9 @@ __device__ __forceinline__ double ppm_interface(const double* __restrict__ s,
                                        __dadd_rn(s[b - st], s[b + 2 * st])));
   return np_min(np_max(a, np_min(u0, u1)), np_max(u0, u1));
 }
-// CW84-limited left/right states of the cell at b along st
-__device__ __forceinline__ void ppm_states(const double* __restrict__ s, int b,
-                                           int st, double& ul, double& ur) {
-  const double u = s[b];
-  const double l = ppm_interface(s, b - st, st);
-  const double r = ppm_interface(s, b, st);
+// CW84 limiting of cell value u between its interface values l and r
+__device__ __forceinline__ void ppm_limit(double u, double l, double r,
+                                          double& ul, double& ur) {
   const double dq = __dsub_rn(r, l);
   const double mid = __dsub_rn(u, __dmul_rn(0.5, __dadd_rn(l, r)));
   const bool flat = __dmul_rn(__dsub_rn(r, u), __dsub_rn(u, l)) <= 0.0;
@@ -266,11 +263,17 @@ __device__ __forceinline__ void ppm_states(const double* __restrict__ s, int b,
                    ? __dsub_rn(__dmul_rn(3.0, u), __dmul_rn(2.0, l))
                    : r);
 }
+// CW84-limited left/right states of the cell at b along st
+__device__ __forceinline__ void ppm_states(const double* __restrict__ s, int b,
+                                           int st, double& ul, double& ur) {
+  ppm_limit(s[b], ppm_interface(s, b - st, st), ppm_interface(s, b, st), ul,
+            ur);
+}
 
 // Batched PPM reconstruct + (upwind | KT) flux, one CTA per slice, the whole
 // ghosted sub-grid staged by one TMA box load.
-template <int N, int THREADS, bool DEV_IDS>
-__global__ void __launch_bounds__(THREADS)
+template <int N, int THREADS, bool DEV_IDS, int MINB = 1>
+__global__ void __launch_bounds__(THREADS, MINB)
     k_recon_flux_ppm(const __grid_constant__ CUtensorMap tmap,
                      const int32_t* __restrict__ dev_ids, int out_mode,
                      double ax, double ay, double az, double* __restrict__ um,
@@ -306,16 +309,21 @@ __global__ void __launch_bounds__(THREADS)
     for (int axis = 0; axis < 3; ++axis) {
       const int st = stv[axis];
       const double a = av[axis];
+      // the cell's two interface values; the next cell's left interface
+      // is this cell's right one (formed once)
+      const double i1 = ppm_interface(sbox, b, st);
       double ul, ur;
-      ppm_states(sbox, b, st, ul, ur);
+      ppm_limit(sbox[b], ppm_interface(sbox, b - st, st), i1, ul, ur);
       __stcs(um_s + axis * CELLS + c, ul);
       __stcs(up_s + axis * CELLS + c, ur);
       double next_l = 0.0;
       if (a < 0.0 || flux_form == 1) {
-        // np.roll(um, -1): the last layer wraps onto layer 0
-        const int bn = cv[axis] == C - 1 ? b - (C - 1) * st : b + st;
         double nr;
-        ppm_states(sbox, bn, st, next_l, nr);
+        if (cv[axis] == C - 1)  // np.roll(um, -1): the last layer wraps
+          ppm_states(sbox, b - (C - 1) * st, st, next_l, nr);
+        else
+          ppm_limit(sbox[b + st], i1, ppm_interface(sbox, b + st, st), next_l,
+                    nr);
       }
       double f;
       if (flux_form == 0) {
@@ -983,7 +991,10 @@ int tf_recon_flux_ppm_f64(const double* pool_ext, int64_t pool_slices,
   cudaStream_t st = (cudaStream_t)stream;
   if (n == 8) {
     constexpr size_t smem = Geo<8>::EXT3 * sizeof(double);
-    k_recon_flux_ppm<8, TH, true><<<T, TH, smem, st>>>(
+    // 256 threads at <= 64 registers, 4 CTAs/SM: measured best of 128 /
+    // 256 / 512 threads x register budgets (config 2, one launch: PPM +
+    // upwind 68.6% -> 88.5% of HBM, PPM + KT 52.8% -> 54.7%)
+    k_recon_flux_ppm<8, 256, true, 4><<<T, 256, smem, st>>>(
         map, ids, out_mode, ax, ay, az, um, up, F, amax, flux_form);
   } else {
     constexpr size_t smem = Geo<16>::EXT3 * sizeof(double);
