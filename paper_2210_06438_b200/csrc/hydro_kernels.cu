@@ -284,6 +284,7 @@ __global__ void __launch_bounds__(THREADS, MINB)
   extern __shared__ __align__(128) double sbox[];  // E^3
   __shared__ __align__(8) uint64_t bar;
   __shared__ double red[THREADS / 32];
+  __shared__ double s_ul[CELLS];  // one axis' left states (KT / a < 0)
   const int s = blockIdx.x;
   const int g = dev_ids ? dev_ids[s] : s;
   if (threadIdx.x == 0) {
@@ -299,43 +300,79 @@ __global__ void __launch_bounds__(THREADS, MINB)
   double* F_s = F + slot * 3 * CELLS;
   const double av[3] = {ax, ay, az};
   const int stv[3] = {E * E, E, 1};
+  const int cst[3] = {C * C, C, 1};  // cube strides
+  constexpr int PER = (CELLS + THREADS - 1) / THREADS;
   double speed = 0.0;
-  for (int c = threadIdx.x; c < CELLS; c += THREADS) {
-    const int ci = c / (C * C), cj = (c / C) % C, ck = c % C;
-    const int cv[3] = {ci, cj, ck};
-    // cube c = extended index c + 2 in every axis
-    const int b = ((ci + 2) * E + (cj + 2)) * E + (ck + 2);
+  if (flux_form == 0 && ax >= 0.0 && ay >= 0.0 && az >= 0.0) {
+    // upwind with a >= 0 on every axis: F = a * up needs no neighbour, so
+    // one cell-major pass (measured faster than the axis phases below)
+    for (int c = threadIdx.x; c < CELLS; c += THREADS) {
+      const int ci = c / (C * C), cj = (c / C) % C, ck = c % C;
+      const int b = ((ci + 2) * E + (cj + 2)) * E + (ck + 2);
 #pragma unroll
-    for (int axis = 0; axis < 3; ++axis) {
-      const int st = stv[axis];
-      const double a = av[axis];
-      // the cell's two interface values; the next cell's left interface
-      // is this cell's right one (formed once)
-      const double i1 = ppm_interface(sbox, b, st);
+      for (int axis = 0; axis < 3; ++axis) {
+        double ul, ur;
+        ppm_states(sbox, b, stv[axis], ul, ur);
+        __stcs(um_s + axis * CELLS + c, ul);
+        __stcs(up_s + axis * CELLS + c, ur);
+        __stcs(F_s + axis * CELLS + c, __dmul_rn(av[axis], ur));
+      }
+    }
+    speed = fmax(fmax(fabs(ax), fabs(ay)), fabs(az));
+    if (amax != nullptr) block_max_store<THREADS>(speed, red, amax + slot);
+    return;
+  }
+#pragma unroll 1
+  for (int axis = 0; axis < 3; ++axis) {
+    const int st = stv[axis];
+    const double a = av[axis];
+    // KT form or a < 0: F needs the NEXT cell's limited left state.  Every
+    // cell's left state is formed once (phase 1, into s_ul) and the flux
+    // read from there (phase 2) — instead of each cell re-limiting its
+    // neighbour.
+    const bool next = a < 0.0 || flux_form == 1;
+    double urk[PER];
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+      const int c = threadIdx.x + k * THREADS;
+      if (c >= CELLS) break;
+      const int ci = c / (C * C), cj = (c / C) % C, ck = c % C;
+      // cube c = extended index c + 2 in every axis
+      const int b = ((ci + 2) * E + (cj + 2)) * E + (ck + 2);
       double ul, ur;
-      ppm_limit(sbox[b], ppm_interface(sbox, b - st, st), i1, ul, ur);
+      ppm_states(sbox, b, st, ul, ur);
       __stcs(um_s + axis * CELLS + c, ul);
       __stcs(up_s + axis * CELLS + c, ur);
-      double next_l = 0.0;
-      if (a < 0.0 || flux_form == 1) {
-        double nr;
-        if (cv[axis] == C - 1)  // np.roll(um, -1): the last layer wraps
-          ppm_states(sbox, b - (C - 1) * st, st, next_l, nr);
-        else
-          ppm_limit(sbox[b + st], i1, ppm_interface(sbox, b + st, st), next_l,
-                    nr);
-      }
-      double f;
-      if (flux_form == 0) {
-        f = a >= 0.0 ? __dmul_rn(a, ur) : __dmul_rn(a, next_l);
-      } else {
-        const double fl = __dmul_rn(a, ur), fr = __dmul_rn(a, next_l);
-        f = __dsub_rn(__dmul_rn(0.5, __dadd_rn(fl, fr)),
-                      __dmul_rn(__dmul_rn(0.5, fabs(a)), __dsub_rn(next_l, ur)));
-      }
-      __stcs(F_s + axis * CELLS + c, f);
-      speed = fmax(speed, fabs(a));
+      urk[k] = ur;
+      if (next) s_ul[c] = ul;
+      else __stcs(F_s + axis * CELLS + c, __dmul_rn(a, ur));
     }
+    if (next) {
+      __syncthreads();
+#pragma unroll
+      for (int k = 0; k < PER; ++k) {
+        const int c = threadIdx.x + k * THREADS;
+        if (c >= CELLS) break;
+        const int ci = c / (C * C), cj = (c / C) % C, ck = c % C;
+        const int pos = axis == 0 ? ci : (axis == 1 ? cj : ck);
+        // np.roll(um, -1): the last layer wraps onto layer 0
+        const double next_l =
+            s_ul[pos == C - 1 ? c - (C - 1) * cst[axis] : c + cst[axis]];
+        const double ur = urk[k];
+        double f;
+        if (flux_form == 0) {
+          f = __dmul_rn(a, next_l);
+        } else {
+          const double fl = __dmul_rn(a, ur), fr = __dmul_rn(a, next_l);
+          f = __dsub_rn(__dmul_rn(0.5, __dadd_rn(fl, fr)),
+                        __dmul_rn(__dmul_rn(0.5, fabs(a)),
+                                  __dsub_rn(next_l, ur)));
+        }
+        __stcs(F_s + axis * CELLS + c, f);
+      }
+      __syncthreads();  // s_ul is rewritten for the next axis
+    }
+    speed = fmax(speed, fabs(a));
   }
   if (amax != nullptr) block_max_store<THREADS>(speed, red, amax + slot);
 }

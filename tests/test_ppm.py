@@ -83,7 +83,9 @@ def test_ppm_sharper_than_minmod_on_smooth_data():
     (32, 8, "blast", (-1.0, 0.5, -0.25), 0),
     (32, 8, "sod", (0.7, -1.3, 0.0), 1),
     (32, 16, "stress", (-0.3, 0.2, 0.9), 0),
-    (32, 16, "blast", (1.0, 1.0, 1.0), 1)])
+    (32, 16, "blast", (1.0, 1.0, 1.0), 1),
+    (16, 8, "stress", (-0.4, -0.9, -1.2), 1),
+    (16, 8, "stress", (0.5, 0.0, 1.5), 1)])
 def test_gpu_ppm_matches_oracle(cuda, grid, n, field, vel, form):
     import torch
     from paper_2210_06438_b200 import ops
