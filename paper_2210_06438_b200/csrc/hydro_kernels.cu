@@ -443,20 +443,47 @@ __global__ void __launch_bounds__(256)
   constexpr int E = G::E;
   const int s = blockIdx.x;
   const int g = ids ? ids[s] : s;
-  const int m = per_axis, grid = per_axis * N;
-  const int bx = g / (m * m), by = (g / m) % m, bz = g % m;
+  // the 27 periodic neighbours' base offsets, once per CTA (no division or
+  // wrap arithmetic per cell); a ghost cell (i,j,k) of direction
+  // d = (di,dj,dk) in {-1,0,1}^3 is the neighbour's ext cell (i,j,k) - d*N
+  __shared__ int64_t nbase[27];
+  if (threadIdx.x < 27) {
+    const int m = per_axis;
+    const int bx = g / (m * m), by = (g / m) % m, bz = g % m;
+    const int t = threadIdx.x;
+    const int di = t / 9 - 1, dj = (t / 3) % 3 - 1, dk = t % 3 - 1;
+    const int nx = (bx + di + m) % m, ny = (by + dj + m) % m,
+              nz = (bz + dk + m) % m;
+    nbase[t] = ((int64_t)(nx * m + ny) * m + nz) * G::EXT3 -
+               (int64_t)((di * E + dj) * E + dk) * N;
+  }
+  __syncthreads();
   double* __restrict__ dst = pool + (int64_t)g * G::EXT3;
-  for (int c = threadIdx.x; c < G::EXT3; c += blockDim.x) {
-    const int i = c / (E * E), j = (c / E) % E, k = c % E;
-    const bool owned = i >= 3 && i < N + 3 && j >= 3 && j < N + 3 && k >= 3 &&
-                       k < N + 3;
-    if (owned) continue;
-    const int gi = (bx * N + i - 3 + grid) % grid;
-    const int gj = (by * N + j - 3 + grid) % grid;
-    const int gk = (bz * N + k - 3 + grid) % grid;
-    const int src = ((gi / N) * m + (gj / N)) * m + (gk / N);
-    const int e = ((gi % N + 3) * E + (gj % N + 3)) * E + (gk % N + 3);
-    dst[c] = pool[(int64_t)src * G::EXT3 + e];
+  // every load issued before any store: sources are neighbours' OWNED
+  // cells, destinations this sub-grid's GHOST cells, so they never overlap
+  // — but through one pointer the compiler would otherwise serialise each
+  // load behind the previous store
+  constexpr int TH = 256, PER = (G::EXT3 + TH - 1) / TH;
+  constexpr int GRP = PER < 12 ? PER : 12;  // loads in flight per thread
+#pragma unroll 1
+  for (int q0 = 0; q0 < PER; q0 += GRP) {
+    double v[GRP];
+#pragma unroll
+    for (int q = 0; q < GRP; ++q) {
+      const int c = threadIdx.x + (q0 + q) * TH;
+      const int i = c / (E * E), j = (c / E) % E, k = c % E;  // constexpr E
+      const int t = (((i >= 3) + (i >= N + 3)) * 3 + (j >= 3) +
+                     (j >= N + 3)) * 3 + (k >= 3) + (k >= N + 3);
+      if (c < G::EXT3 && t != 13) v[q] = pool[nbase[t] + c];  // 13 = owned
+    }
+#pragma unroll
+    for (int q = 0; q < GRP; ++q) {
+      const int c = threadIdx.x + (q0 + q) * TH;
+      const int i = c / (E * E), j = (c / E) % E, k = c % E;
+      const bool owned = i >= 3 && i < N + 3 && j >= 3 && j < N + 3 &&
+                         k >= 3 && k < N + 3;
+      if (c < G::EXT3 && !owned) dst[c] = v[q];
+    }
   }
 }
 
