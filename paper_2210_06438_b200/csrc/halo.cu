@@ -52,24 +52,43 @@ __global__ void __launch_bounds__(256)
   const int g = first + blockIdx.x;
   const int bx = g / (m * m), by = (g / m) % m, bz = g % m;
   double* __restrict__ dst = pool + (int64_t)g * E * E * E;
-  for (int c = threadIdx.x; c < E * E * E; c += blockDim.x) {
-    const int i = c / (E * E), j = (c / E) % E, k = c % E;
-    if (i >= 3 && i < N + 3 && j >= 3 && j < N + 3 && k >= 3 && k < N + 3)
-      continue;
-    const int lx = bx * N + i - 3;  // slab-local x, in [-3, X+3)
-    const int gy = (by * N + j - 3 + G) % G;
-    const int gz = (bz * N + k - 3 + G) % G;
-    double v;
-    if (lx < 0) {
-      v = halo_lo[((int64_t)(lx + 3) * G + gy) * G + gz];
-    } else if (lx >= X) {
-      v = halo_hi[((int64_t)(lx - X) * G + gy) * G + gz];
-    } else {
-      const int64_t src = ((int64_t)(lx / N) * m + gy / N) * m + gz / N;
-      v = pool[src * E * E * E +
-               ((int64_t)(lx % N + 3) * E + (gy % N + 3)) * E + (gz % N + 3)];
+  // loads issued in groups before their stores: sources (neighbours' owned
+  // cells, halo planes) never overlap destinations (this sub-grid's ghost
+  // cells), but through one pointer the compiler would serialise each load
+  // behind the previous store (the same fix as k_ghost_fill)
+  constexpr int TH = 256, PER = (E * E * E + TH - 1) / TH;
+  constexpr int GRP = PER < 12 ? PER : 12;
+#pragma unroll 1
+  for (int q0 = 0; q0 < PER; q0 += GRP) {
+    double v[GRP];
+#pragma unroll
+    for (int q = 0; q < GRP; ++q) {
+      const int c = threadIdx.x + (q0 + q) * TH;
+      const int i = c / (E * E), j = (c / E) % E, k = c % E;
+      if (c >= E * E * E ||
+          (i >= 3 && i < N + 3 && j >= 3 && j < N + 3 && k >= 3 && k < N + 3))
+        continue;
+      const int lx = bx * N + i - 3;  // slab-local x, in [-3, X+3)
+      const int gy = (by * N + j - 3 + G) % G;
+      const int gz = (bz * N + k - 3 + G) % G;
+      if (lx < 0) {
+        v[q] = halo_lo[((int64_t)(lx + 3) * G + gy) * G + gz];
+      } else if (lx >= X) {
+        v[q] = halo_hi[((int64_t)(lx - X) * G + gy) * G + gz];
+      } else {
+        const int64_t src = ((int64_t)(lx / N) * m + gy / N) * m + gz / N;
+        v[q] = pool[src * E * E * E + ((int64_t)(lx % N + 3) * E +
+                                      (gy % N + 3)) * E + (gz % N + 3)];
+      }
     }
-    dst[c] = v;
+#pragma unroll
+    for (int q = 0; q < GRP; ++q) {
+      const int c = threadIdx.x + (q0 + q) * TH;
+      const int i = c / (E * E), j = (c / E) % E, k = c % E;
+      if (c < E * E * E &&
+          !(i >= 3 && i < N + 3 && j >= 3 && j < N + 3 && k >= 3 && k < N + 3))
+        dst[c] = v[q];
+    }
   }
 }
 
