@@ -229,13 +229,14 @@ int64_t tf_qexec_completed(const tf_qexec* q);
 int tf_queue_consumer_ctas(int32_t n);
 /* ring_h/ctl_h: mapped pinned host ring + control block {published,
  * final_count, completed}; ring_d: device mirror of tagged entries
- * (epoch << 32 | id), zeroed once at allocation; epoch >= 1, new for every
- * launch on that ring; qdev: {published, final_count, claim, done}, one
- * 128-B line each (zeroed, final_count = -1, before launch).               */
+ * (epoch << 32 | id), ring_cap of them (the most this launch may publish),
+ * zeroed once at allocation; epoch >= 1, new for every launch on that ring;
+ * qdev: {published, final_count, claim, done}, one 128-B line each (zeroed,
+ * final_count = -1, before launch).                                        */
 int tf_queue_consumer_launch(const double* pool_ext, int64_t pool_slices,
                              int32_t n, const int32_t* ring_h, void* ctl_h,
-                             int64_t* ring_d, void* qdev, int32_t ctas,
-                             int32_t epoch,
+                             int64_t* ring_d, int64_t ring_cap, void* qdev,
+                             int32_t ctas, int32_t epoch,
                              double ax, double ay, double az, double* um,
                              double* up, double* F, double* amax,
                              int32_t flux_form, int64_t timeout_ns,

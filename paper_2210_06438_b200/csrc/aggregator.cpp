@@ -660,8 +660,8 @@ int tf_qexec_run_recon_flux(tf_qexec* q, const double* pool_ext,
                          0xff, sizeof(long long), st);
   if (ce != cudaSuccess) return ce;
   int rc = tf_queue_consumer_launch(
-      pool_ext, pool_slices, q->n, S.ring_hd, S.ctl_hd, S.ring_d, S.qdev,
-      q->ctas, ++S.epoch, ax, ay, az, um, up, F, amax, flux_form,
+      pool_ext, pool_slices, q->n, S.ring_hd, S.ctl_hd, S.ring_d, count,
+      S.qdev, q->ctas, ++S.epoch, ax, ay, az, um, up, F, amax, flux_form,
       /*timeout_ns=*/2000000000LL, stream);
   if (rc) return rc;
   ce = cudaEventRecord(S.done_ev, st);

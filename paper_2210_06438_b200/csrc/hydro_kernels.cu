@@ -804,8 +804,9 @@ template <int N, int THREADS>
 __global__ void __launch_bounds__(THREADS, recon_min_blocks<THREADS>())
     k_queue_consumer(const __grid_constant__ CUtensorMap tmap,
                      const int* __restrict__ ring_h, QueueCtl* ctl,
-                     unsigned long long* __restrict__ ring_d, QueueDev* qd,
-                     unsigned epoch, double ax,
+                     unsigned long long* __restrict__ ring_d,
+                     long long ring_cap, QueueDev* qd, unsigned epoch,
+                     double ax,
                      double ay, double az, double* __restrict__ um,
                      double* __restrict__ up, double* __restrict__ F,
                      double* __restrict__ amax, int flux_form,
@@ -829,6 +830,12 @@ __global__ void __launch_bounds__(THREADS, recon_min_blocks<THREADS>())
       const unsigned long long t0 = globaltimer();
       int g;
       for (;;) {
+        // this run publishes at most ring_cap ids: a slot beyond them is
+        // never filled (and lies outside the ring)
+        if (k >= ring_cap) {
+          g = -1;
+          break;
+        }
         // relaxed polls only: an acquire would invalidate the SM's L1
         // (CCTL.IVALL) once per slice, under every CTA's spilled registers
         const unsigned long long v = ld_relaxed_gpu_u64(ring_d + k);
@@ -1100,14 +1107,14 @@ int tf_queue_consumer_ctas(int32_t n) {
 
 int tf_queue_consumer_launch(const double* pool_ext, int64_t pool_slices,
                              int32_t n, const int32_t* ring_h, void* ctl_h,
-                             int64_t* ring_d, void* qdev, int32_t ctas,
-                             int32_t epoch,
+                             int64_t* ring_d, int64_t ring_cap, void* qdev,
+                             int32_t ctas, int32_t epoch,
                              double ax, double ay, double az, double* um,
                              double* up, double* F, double* amax,
                              int32_t flux_form, int64_t timeout_ns,
                              tf_stream_t stream) {
   if (!valid_n(n) || !pool_ext || !ring_h || !ctl_h || !ring_d || !qdev ||
-      ctas < 1 || epoch < 1 || !um || !up || !F)
+      ring_cap < 0 || ctas < 1 || epoch < 1 || !um || !up || !F)
     return TF_E_INVALID;
   CUtensorMap map;
   int rc = pool_map(pool_ext, pool_slices, n, &map);
@@ -1119,14 +1126,15 @@ int tf_queue_consumer_launch(const double* pool_ext, int64_t pool_slices,
   // grid: the fetcher block + `ctas` consumers
   if (n == 8)
     k_queue_consumer<8, TH><<<ctas + 1, TH, Geo<8>::BOX * sizeof(double), st>>>(
-        map, ring_h, c, reinterpret_cast<unsigned long long*>(ring_d), q,
-        (unsigned)epoch, ax, ay, az, um, up, F, amax, flux_form, timeout_ns);
+        map, ring_h, c, reinterpret_cast<unsigned long long*>(ring_d),
+        (long long)ring_cap, q, (unsigned)epoch, ax, ay, az, um, up, F, amax,
+        flux_form, timeout_ns);
   else
     k_queue_consumer<16, TH>
         <<<ctas + 1, TH, Geo<16>::BOX * sizeof(double), st>>>(
-            map, ring_h, c, reinterpret_cast<unsigned long long*>(ring_d), q,
-            (unsigned)epoch, ax, ay, az, um, up, F, amax, flux_form,
-            timeout_ns);
+            map, ring_h, c, reinterpret_cast<unsigned long long*>(ring_d),
+            (long long)ring_cap, q, (unsigned)epoch, ax, ay, az, um, up, F,
+            amax, flux_form, timeout_ns);
   return cudaGetLastError();
 }
 
