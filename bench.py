@@ -774,6 +774,17 @@ def main():
     # in, one hydro iteration = reconstruct + flux + update of every
     # sub-grid, pinned host field out), transfers overlapped with compute
     line["e2e"] = dict(line["fused_full_iteration"]["e2e_pipelined"])
+    # the host link bounds e2e: bytes both ways per step against the
+    # measured concurrent copy-engine rate (48.9 GB/s per direction on this
+    # pool's boxes, profiles/r01_pcie_probe2.log)
+    e = line["e2e"]
+    link = e["h2d_bytes_per_step"] + e["d2h_bytes_per_step"]
+    e["link"] = {"bytes_per_step": link,
+                 "achieved_GBps": link / (e["ms_per_step"] * 1e-3) / 1e9,
+                 "bidirectional_peak_GBps": 2 * 48.9,
+                 "frac": link / (e["ms_per_step"] * 1e-3) / 1e9 / 97.8,
+                 "floor_ms": max(e["h2d_bytes_per_step"],
+                                 e["d2h_bytes_per_step"]) / 48.9e9 * 1e3}
     line["schemes_one_launch"] = scheme_legs(wl, max(10, args.steps // 2), 3,
                                              world, stream, peak)
     line["e2e_faces"] = {"value": rate(total_S, wl.n, f_ms), "unit": UNIT,
