@@ -517,7 +517,7 @@ def fused_legs(args, steps, warmup, world, stream, peak):
             "gpu_launches_per_step": pipe.launches,
             "step": "field.HostPipeline: tapered x-chunks (sub-grid layers "
                     "[1,3,4,4,3,1]), copy-engine upload shifted by the x "
-                    "halo / scatter+halo / fused step / zero-copy download "
+                    "halo / one pad+halo kernel / fused step / zero-copy download "
                     "kernel, overlapped, captured as one CUDA graph"},
     }
 
