@@ -232,11 +232,12 @@ int tf_queue_consumer_ctas(int32_t n);
  * (epoch << 32 | id), ring_cap of them (the most this launch may publish),
  * zeroed once at allocation; epoch >= 1, new for every launch on that ring;
  * qdev: {published, final_count, claim, done}, one 128-B line each (zeroed,
- * final_count = -1, before launch).                                        */
+ * final_count = -1, before launch); qdev_next (or NULL): another such block
+ * the kernel resets on its way out, for the next launch.                    */
 int tf_queue_consumer_launch(const double* pool_ext, int64_t pool_slices,
                              int32_t n, const int32_t* ring_h, void* ctl_h,
                              int64_t* ring_d, int64_t ring_cap, void* qdev,
-                             int32_t ctas, int32_t epoch,
+                             void* qdev_next, int32_t ctas, int32_t epoch,
                              double ax, double ay, double az, double* um,
                              double* up, double* F, double* amax,
                              int32_t flux_form, int64_t timeout_ns,

@@ -120,8 +120,8 @@ SIGNATURES = {
     "tf_qexec_completed": (_i64, [_p]),
     "tf_queue_consumer_ctas": (C.c_int, [_i32]),
     "tf_queue_consumer_launch": (C.c_int, [_p, _i64, _i32, _p, _p, _p, _i64,
-                                           _p, _i32, _i32, _f64, _f64, _f64,
-                                           _p, _p, _p, _p, _i32, _i64,
+                                           _p, _p, _i32, _i32, _f64, _f64,
+                                           _f64, _p, _p, _p, _p, _i32, _i64,
                                            _p]),  # noqa
     "tf_version": (C.c_char_p, []),
     "tf_check_device": (C.c_int, [_i32]),

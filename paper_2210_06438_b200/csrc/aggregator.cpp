@@ -582,6 +582,11 @@ int tf_qexec_create(tf_region* region, int32_t n, tf_qexec** out) {
       e = cudaHostAlloc(&S.ctl_h, sizeof(QueueCtlHost), cudaHostAllocMapped);
     if (e == cudaSuccess) e = cudaHostGetDevicePointer(&S.ctl_hd, S.ctl_h, 0);
     if (e == cudaSuccess) e = cudaMalloc(&S.qdev, sizeof(QueueDevInit));
+    if (e == cudaSuccess) {  // {0, -1, 0, 0}; later runs reset it on device
+      QueueDevInit init{};
+      init.final_count = -1;
+      e = cudaMemcpy(S.qdev, &init, sizeof(init), cudaMemcpyHostToDevice);
+    }
     if (e == cudaSuccess)
       e = cudaEventCreateWithFlags(&S.done_ev, cudaEventDisableTiming);
   }
@@ -651,20 +656,15 @@ int tf_qexec_run_recon_flux(tf_qexec* q, const double* pool_ext,
   S.ctl_h->completed = 0;
   __atomic_thread_fence(__ATOMIC_SEQ_CST);
   cudaStream_t st = (cudaStream_t)stream;
-  // device counters {published 0, final_count -1, claim 0, done 0}: two
-  // memsets (no staged copy from pageable host memory)
-  cudaError_t ce = cudaMemsetAsync(S.qdev, 0, sizeof(QueueDevInit), st);
-  if (ce == cudaSuccess)
-    ce = cudaMemsetAsync(static_cast<char*>(S.qdev) +
-                             offsetof(QueueDevInit, final_count),
-                         0xff, sizeof(long long), st);
-  if (ce != cudaSuccess) return ce;
+  // the slot's device counters were reset by the previous run's kernel on
+  // its way out (qdev_next), or at creation
   int rc = tf_queue_consumer_launch(
       pool_ext, pool_slices, q->n, S.ring_hd, S.ctl_hd, S.ring_d, count,
-      S.qdev, q->ctas, ++S.epoch, ax, ay, az, um, up, F, amax, flux_form,
+      S.qdev, q->slots[q->cur ^ 1].qdev, q->ctas, ++S.epoch, ax, ay, az, um,
+      up, F, amax, flux_form,
       /*timeout_ns=*/2000000000LL, stream);
   if (rc) return rc;
-  ce = cudaEventRecord(S.done_ev, st);
+  const cudaError_t ce = cudaEventRecord(S.done_ev, st);
   if (ce != cudaSuccess) return ce;
   S.in_flight = true;
   tf_region* r = q->region;

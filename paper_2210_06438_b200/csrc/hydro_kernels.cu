@@ -712,7 +712,7 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 template <int THREADS>
 __device__ void queue_fetcher(const int* __restrict__ ring_h, QueueCtl* ctl,
                               unsigned long long* __restrict__ ring_d,
-                              QueueDev* qd, unsigned epoch,
+                              QueueDev* qd, QueueDev* qd_next, unsigned epoch,
                               long long timeout_ns) {
   __shared__ long long s_pub, s_fin, s_done;
   __shared__ int s_stop;
@@ -781,22 +781,33 @@ __device__ void queue_fetcher(const int* __restrict__ ring_h, QueueCtl* ctl,
     if (s_stop) break;
     __nanosleep(100);
   }
+  if (threadIdx.x != 0) return;
   // phase 2 (one thread): every id is on the device; report completions to
   // the host until all are done — device-side polling only, no PCIe reads,
   // so the grid exits as soon as the last slice does
-  if (threadIdx.x != 0 || s_stop == 2) return;
-  const long long fin = ld_acquire_gpu(&qd->final_count);
-  for (;;) {
-    const long long done = ld_acquire_gpu(
-        reinterpret_cast<const long long*>(&qd->done));
-    if (done != reported) {
-      st_release_sys(&ctl->completed, done);
-      reported = done;
-      last_change = globaltimer();
+  if (s_stop != 2) {
+    const long long fin = ld_acquire_gpu(&qd->final_count);
+    for (;;) {
+      const long long done = ld_acquire_gpu(
+          reinterpret_cast<const long long*>(&qd->done));
+      if (done != reported) {
+        st_release_sys(&ctl->completed, done);
+        reported = done;
+        last_change = globaltimer();
+      }
+      if (done >= fin) break;
+      if ((long long)(globaltimer() - last_change) > timeout_ns) break;
+      __nanosleep(32);
     }
-    if (done >= fin) return;
-    if ((long long)(globaltimer() - last_change) > timeout_ns) return;
-    __nanosleep(32);
+  }
+  // reset the OTHER queue slot's device counters for the next run (it last
+  // ran two launches ago and runs next, both stream-ordered around this
+  // kernel): the host then needs no memset launches between runs
+  if (qd_next != nullptr) {
+    qd_next->published = 0;
+    qd_next->final_count = -1;
+    qd_next->claim = 0;
+    qd_next->done = 0;
   }
 }
 
@@ -805,8 +816,8 @@ __global__ void __launch_bounds__(THREADS, recon_min_blocks<THREADS>())
     k_queue_consumer(const __grid_constant__ CUtensorMap tmap,
                      const int* __restrict__ ring_h, QueueCtl* ctl,
                      unsigned long long* __restrict__ ring_d,
-                     long long ring_cap, QueueDev* qd, unsigned epoch,
-                     double ax,
+                     long long ring_cap, QueueDev* qd, QueueDev* qd_next,
+                     unsigned epoch, double ax,
                      double ay, double az, double* __restrict__ um,
                      double* __restrict__ up, double* __restrict__ F,
                      double* __restrict__ amax, int flux_form,
@@ -814,7 +825,8 @@ __global__ void __launch_bounds__(THREADS, recon_min_blocks<THREADS>())
   using G = Geo<N>;
   constexpr int CELLS = G::CELLS;
   if (blockIdx.x == 0) {
-    queue_fetcher<THREADS>(ring_h, ctl, ring_d, qd, epoch, timeout_ns);
+    queue_fetcher<THREADS>(ring_h, ctl, ring_d, qd, qd_next, epoch,
+                           timeout_ns);
     return;
   }
   extern __shared__ __align__(128) double sbox[];
@@ -1108,7 +1120,7 @@ int tf_queue_consumer_ctas(int32_t n) {
 int tf_queue_consumer_launch(const double* pool_ext, int64_t pool_slices,
                              int32_t n, const int32_t* ring_h, void* ctl_h,
                              int64_t* ring_d, int64_t ring_cap, void* qdev,
-                             int32_t ctas, int32_t epoch,
+                             void* qdev_next, int32_t ctas, int32_t epoch,
                              double ax, double ay, double az, double* um,
                              double* up, double* F, double* amax,
                              int32_t flux_form, int64_t timeout_ns,
@@ -1127,14 +1139,15 @@ int tf_queue_consumer_launch(const double* pool_ext, int64_t pool_slices,
   if (n == 8)
     k_queue_consumer<8, TH><<<ctas + 1, TH, Geo<8>::BOX * sizeof(double), st>>>(
         map, ring_h, c, reinterpret_cast<unsigned long long*>(ring_d),
-        (long long)ring_cap, q, (unsigned)epoch, ax, ay, az, um, up, F, amax,
-        flux_form, timeout_ns);
+        (long long)ring_cap, q, static_cast<QueueDev*>(qdev_next),
+        (unsigned)epoch, ax, ay, az, um, up, F, amax, flux_form, timeout_ns);
   else
     k_queue_consumer<16, TH>
         <<<ctas + 1, TH, Geo<16>::BOX * sizeof(double), st>>>(
             map, ring_h, c, reinterpret_cast<unsigned long long*>(ring_d),
-            (long long)ring_cap, q, (unsigned)epoch, ax, ay, az, um, up, F,
-            amax, flux_form, timeout_ns);
+            (long long)ring_cap, q, static_cast<QueueDev*>(qdev_next),
+            (unsigned)epoch, ax, ay, az, um, up, F, amax, flux_form,
+            timeout_ns);
   return cudaGetLastError();
 }
 

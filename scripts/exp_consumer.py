@@ -29,7 +29,8 @@ def run(k):
     ctl_h[2] = 0
     rc = lib.tf_queue_consumer_launch(
         wl.pools[k % 2].data_ptr(), S, 8, ring_h.data_ptr(), ctl_h.data_ptr(),
-        ring_d.data_ptr(), S, qdev.data_ptr(), ctas, k + 1, 1.0, 1.0, 1.0,
+        ring_d.data_ptr(), S, qdev.data_ptr(), None, ctas, k + 1, 1.0, 1.0,
+        1.0,
         wl.um.data_ptr(), wl.up.data_ptr(), wl.F.data_ptr(),
         wl.amax.data_ptr(), 0, 2_000_000_000, st.cuda_stream)
     assert rc == 0, rc
