@@ -188,3 +188,28 @@ def test_queue_executor_other_shapes(cuda, n, vel):
     assert np.array_equal(up.cpu().numpy(), oup)
     assert np.array_equal(F.cpu().numpy(), oF)
     assert bool((amax == max(abs(v) for v in vel)).all())
+
+
+def test_queue_executor_back_to_back_runs_of_varying_size(cuda, cfg2):
+    """Consecutive real-time runs alternate the two queue slots; each run's
+    ring entries carry a new epoch and the previous kernel resets the next
+    slot's counters.  Runs of very different sizes (a full iteration, then a
+    handful of arrivals, then a large random subset ...) must each process
+    exactly their own arrivals — stale entries of a longer earlier run are
+    never taken — and leave every other output slot untouched."""
+    import torch
+    from paper_2210_06438_b200.strategy3 import QueueExecutor, default_parents
+    pool, n, vel, oum, oup, oF = cfg2
+    S = pool.shape[0]
+    rng = np.random.default_rng(2210)
+    q = QueueExecutor("flux", 32, default_parents(S, 32), n)
+    for size in (S, 7, 1500, 1, S, 333):
+        ids = rng.choice(S, size=size, replace=False).astype(np.int32)
+        um, up, F = _outs(S, n, cuda)
+        q.run(pool, vel, ids, um, up, F)
+        torch.cuda.synchronize()
+        assert q.completed() == size
+        Fh = F.cpu().numpy()
+        assert np.array_equal(Fh[ids], oF[ids]), size
+        rest = np.setdiff1d(np.arange(S), ids)
+        assert np.isnan(Fh[rest]).all(), size
