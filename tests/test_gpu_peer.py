@@ -78,3 +78,31 @@ def test_peer_two_processes_one_gpu(cuda, world):
     whole = np.concatenate([got[r] for r in range(world)], axis=0)
     assert np.array_equal(whole, HO.reference_step(HO.stress_field(grid),
                                                    vel))
+
+
+def test_peer_barrier_times_out_instead_of_hanging(cuda):
+    """A neighbour that never arrives: the device barrier gives up after its
+    timeout and raises the error flag (the host then raises) — it never
+    hangs the GPU."""
+    import torch
+    from paper_2210_06438_b200 import _lib
+    lib = _lib.load()
+    mine = torch.zeros(2, dtype=torch.int64, device=cuda)
+    left = torch.zeros(2, dtype=torch.int64, device=cuda)
+    right = torch.zeros(2, dtype=torch.int64, device=cuda)
+    err = torch.zeros(1, dtype=torch.int32, device=cuda)
+    st = torch.cuda.current_stream().cuda_stream
+    # neighbours arrived: both of my flags already at the epoch
+    mine.fill_(1)
+    _lib.check(lib.tf_peer_barrier(mine.data_ptr(), left.data_ptr(),
+                                   right.data_ptr(), 1, 10_000_000,
+                                   err.data_ptr(), st), "tf_peer_barrier")
+    torch.cuda.synchronize()
+    assert int(err.item()) == 0
+    assert left.tolist()[1] == 1 and right.tolist()[0] == 1  # I told them
+    # epoch 2: nobody writes my flags -> timeout (1 ms), error flag set
+    _lib.check(lib.tf_peer_barrier(mine.data_ptr(), left.data_ptr(),
+                                   right.data_ptr(), 2, 1_000_000,
+                                   err.data_ptr(), st), "tf_peer_barrier")
+    torch.cuda.synchronize()
+    assert int(err.item()) == 1
