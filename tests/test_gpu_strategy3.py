@@ -213,3 +213,34 @@ def test_queue_executor_back_to_back_runs_of_varying_size(cuda, cfg2):
         assert np.array_equal(Fh[ids], oF[ids]), size
         rest = np.setdiff1d(np.arange(S), ids)
         assert np.isnan(Fh[rest]).all(), size
+
+
+def test_queue_consumer_gives_the_gpu_back_when_nothing_arrives(cuda):
+    """A queue that is never published to and never closed: the resident
+    consumer grid exits after its timeout instead of holding the GPU."""
+    import time
+    import torch
+    from paper_2210_06438_b200 import _lib
+    lib = _lib.load()
+    n, S = 8, 64
+    c = n + 2
+    pool = torch.zeros((S, n + 6, n + 6, n + 6), dtype=torch.float64,
+                       device=cuda)
+    um, up, F = (torch.empty((S, 3, c, c, c), dtype=torch.float64,
+                             device=cuda) for _ in range(3))
+    ring_h = torch.zeros(S, dtype=torch.int32).pin_memory()
+    ctl_h = torch.tensor([0, -1, 0], dtype=torch.int64).pin_memory()
+    ring_d = torch.zeros(S, dtype=torch.int64, device=cuda)
+    qdev = torch.zeros(64, dtype=torch.int64, device=cuda)
+    qdev[16] = -1                       # final_count: not closed
+    ctas = lib.tf_queue_consumer_ctas(n)
+    t0 = time.time()
+    _lib.check(lib.tf_queue_consumer_launch(
+        pool.data_ptr(), S, n, ring_h.data_ptr(), ctl_h.data_ptr(),
+        ring_d.data_ptr(), S, qdev.data_ptr(), None, ctas, 1, 1.0, 1.0, 1.0,
+        um.data_ptr(), up.data_ptr(), F.data_ptr(), None, 0,
+        5_000_000, torch.cuda.current_stream().cuda_stream),
+        "tf_queue_consumer_launch")
+    torch.cuda.synchronize()
+    assert time.time() - t0 < 5.0
+    assert int(ctl_h[2]) == 0           # nothing completed
