@@ -141,3 +141,26 @@ def test_random_kt_and_ppm(cuda, case):
         assert np.array_equal(_bits(up), _bits(pup)), (case, form)
         assert np.array_equal(_bits(F), _bits(flux(pum, pup, vel))), \
             (case, form)
+
+
+@pytest.mark.parametrize("n,grid", [(8, 32), (8, 64), (16, 64), (8, 8)])
+def test_ghost_fill_subsets(cuda, n, grid):
+    """exchange_ghosts for a random subset of sub-grids (the per-task path
+    fills one sub-grid at a time): listed sub-grids match the oracle, every
+    other sub-grid keeps its NaN ghosts; a one-sub-grid lattice wraps onto
+    itself."""
+    import torch
+    from paper_2210_06438_b200 import ops
+    rng = np.random.default_rng(grid * n)
+    m = grid // n
+    f = 1.0 + rng.random((grid, grid, grid))
+    hp = HO.make_pool(f, n)            # ghosts NaN
+    S = hp.shape[0]
+    ids = np.sort(rng.choice(S, size=max(1, S // 3), replace=False))
+    pool = torch.from_numpy(hp.copy()).to(cuda)
+    ops.ghost_fill(pool, n, m, ids=torch.from_numpy(ids.astype(np.int32))
+                   .to(cuda))
+    torch.cuda.synchronize()
+    HO.exchange_ghosts_pool(hp, n, m, ids=[int(i) for i in ids])
+    got = pool.cpu().numpy()
+    assert np.array_equal(_bits(got), _bits(hp))
