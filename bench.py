@@ -566,8 +566,9 @@ def cfg5_leg(args, world, rank, local, peak):
     # (the step measured for `value`)
     from paper_2210_06438_b200.field import PeerSlabFieldIteration
     peer = PeerSlabFieldIteration(part, slab, VELOCITY, device=dev)
-    ms = timed(lambda k: peer.iteration(), args.steps, args.warmup, world,
-               stream)
+    with ClockSampler(local) as clk:
+        ms = timed(lambda k: peer.iteration(), args.steps, args.warmup,
+                   world, stream)
     peer.check()
     del peer
     torch.cuda.empty_cache()
@@ -622,10 +623,11 @@ def cfg5_leg(args, world, rank, local, peak):
                     "1: B_step counts each sub-grid's halo reads, which the "
                     "padded-field layout serves from L2 (traffic = DRAM "
                     "bytes per step-kernel launch from the ncu capture at "
-                    "grid 256, scaled: ~7.2 KB per sub-grid). "
+                    "grid 256, scaled: ~7.4 KB per sub-grid). "
                     "unique_dram_frac = 16 B per cell (field in + out) / "
                     "step time / peak: the DRAM floor's fraction; the "
                     "kernel is latency / L2-bound, DESIGN.md §4"},
+        "clocks": clk.summary(),
         "materialising_path": {
             "ms_per_step": ms_pool,
             "value": rate(S_total, n, ms_pool),

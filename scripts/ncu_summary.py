@@ -23,6 +23,11 @@ KEYS = [
     "launch__occupancy_limit_registers", "launch__occupancy_limit_shared_mem",
     "lts__t_sector_hit_rate.pct", "smsp__inst_executed.sum",
     "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum",
+    "l1tex__throughput.avg.pct_of_peak_sustained_active",
+    "l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed",
+    "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum",
+    "l1tex__t_sectors_pipe_lsu_mem_global_op_st.sum",
+    "smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio",
 ]
 
 
