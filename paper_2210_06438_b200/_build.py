@@ -51,7 +51,9 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     log = []
     for src in SOURCES:
         obj = tmp / (src + ".o")
-        cmd = [nvcc(), *NVCC_FLAGS, "-x", "cu", "-c", str(CSRC / src),
+        # TASKFUSE_NVCC_EXTRA: extra -D tuning flags for experiment builds
+        extra = os.environ.get("TASKFUSE_NVCC_EXTRA", "").split()
+        cmd = [nvcc(), *NVCC_FLAGS, *extra, "-x", "cu", "-c", str(CSRC / src),
                "-o", str(obj)]
         res = subprocess.run(cmd, capture_output=True, text=True)
         log.append(res.stdout + res.stderr)
