@@ -1,6 +1,8 @@
 """e2e experiment: download CTA count per chunk (0 = copy engine) in the
 tapered host pipeline — does throttling the zero-copy download while the
-last uploads are in flight shorten the tail?"""
+last uploads are in flight shorten the tail?  (Ran against a
+run_host_pipelined that took a per-chunk CTA list; no variant beat a
+uniform 16, so that option was not kept — lists fail on the current code.)"""
 import sys
 
 import torch
