@@ -503,8 +503,9 @@ def fused_legs(args, steps, warmup, world, stream, peak):
                    "ms_per_step": ms_dev,
                    "hbm_frac": fused_bytes / (ms_dev * 1e-3) / 1e9 / peak,
                    "launches_per_step": it.launches_per_step,
-                   "step": "halo refresh + one fused recon+flux+update "
-                           "kernel per team (CUDA graph)"},
+                   "step": "one fused recon+flux+update kernel per team, "
+                           "each also writing its sub-grids' share of the "
+                           "next field's periodic halos (CUDA graph)"},
         "e2e": {"value": rate(S * world, n, ms_e2e), "unit": UNIT,
                 "ms_per_step": ms_e2e,
                 "h2d_bytes_per_step": host_in.numel() * 8,

@@ -298,9 +298,16 @@ int tf_ghost_fill_slab_f64(double* pool_ext, int32_t n, int32_t mx, int32_t m,
  * reconstruct+flux+update per sub-grid (kernels.py:73-111, bit-identical):
  * reads the stencil box from padded_in, writes the owned cells of
  * padded_out.  Halo of padded_in must be current.
+ * flags: TF_LAUNCH_OVERLAP_PREV as above; n = 8 only, TF_STEP_HALO_YZ /
+ * TF_STEP_HALO_X: the step also writes the periodic y/z / x halo layers of
+ * padded_out that copy its sub-grids' owned cells (the halo kernel is then
+ * unnecessary after a step over every sub-grid; halo edges and corners,
+ * which the 6-point stencil never reads, are left as they were).
  * tf_field_halo_f64: periodic y/z halo of every layer; periodic_x != 0 also
  * fills the x halo periodically (one GPU; multi-GPU receives it instead).
  * tf_field_pad_f64 / tf_field_unpad_f64: (X, Gy, Gz) field <-> interior.    */
+#define TF_STEP_HALO_YZ 4
+#define TF_STEP_HALO_X 8
 int tf_field_step_f64(const double* padded_in, int32_t X, int32_t Gy,
                       int32_t Gz, int32_t n, const int32_t* ids,
                       const int32_t* host_ids, int32_t T, double ax, double ay,

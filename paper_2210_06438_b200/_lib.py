@@ -26,6 +26,8 @@ TF_E_NO_TMA = 1002
 MAX_TEAM = 128
 TF_LAUNCH_OVERLAP_PREV = 1
 TF_PLAN_TEAM_BUFFERS = 2
+TF_STEP_HALO_YZ = 4
+TF_STEP_HALO_X = 8
 
 
 class EnterResult(C.Structure):

@@ -748,7 +748,8 @@ int capture_teams(const int32_t* ids, const int64_t* team_offsets,
       const int64_t lo = team_offsets[t];
       const int T = (int)(team_offsets[t + 1] - lo);
       const int e = team_executor[t];
-      const int f = started[e] ? (flags & TF_LAUNCH_OVERLAP_PREV) : 0;
+      const int f = (started[e] ? (flags & TF_LAUNCH_OVERLAP_PREV) : 0) |
+                    (flags & (TF_STEP_HALO_YZ | TF_STEP_HALO_X));
       crc = launch(ids + lo, T, f, (tf_stream_t)br[e]);
       started[e] = 1;
       plan->kernels += 1;

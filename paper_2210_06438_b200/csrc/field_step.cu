@@ -188,11 +188,12 @@ __device__ __forceinline__ double ld_swz1(const unsigned char* box, int r,
 constexpr int COLS8S_HALO_OFF = 15504;  // after the box and the mbarrier
 constexpr int COLS8S_SMEM = COLS8S_HALO_OFF + 2 * 96 * 8;  // 17 040 B
 
-template <int CPT, bool PX, bool PY, bool PZ>
+template <int CPT, bool WH, bool PX, bool PY, bool PZ>
 __device__ __forceinline__ void cols8s_body(
     const unsigned char* box, double* halo, int i, int j, int k0, int i0,
     double ax, double ay, double az, double dt_dx, bool lo, bool hi,
-    double* plo, double* phi, double2* res) {
+    double* plo, double* phi, bool yl, double* pyl, bool zl, double* pzl,
+    double2* res) {
   constexpr int BY = COLS8_BXY, HXF = 8 * CPT, HALO = 12 * CPT;
   constexpr int sx = PX ? 0 : 1, sy = PY ? 0 : 1;
   const int lane = threadIdx.x & 31;
@@ -267,6 +268,10 @@ __device__ __forceinline__ void cols8s_body(
     res[q] = w;
     if (lo) *reinterpret_cast<double2*>(plo + k) = w;
     if (hi) *reinterpret_cast<double2*>(phi + k) = w;
+    if constexpr (WH) {     // low periodic y / z halo of the next field
+      if (yl) *reinterpret_cast<double2*>(pyl + k) = w;
+      if (zl && k >= 8 - HZ) *reinterpret_cast<double2*>(pzl + k) = w;
+    }
   }
 }
 
@@ -289,11 +294,12 @@ __device__ __forceinline__ void tma_store_3d(const CUtensorMap* map,
 // store: 16-B st.global per thread touched 32 rows of the next field per
 // warp store (half-used sectors, ~35% of the kernel's L1 wavefronts; config
 // 5: 0.634 -> 0.54 ms per iteration)
-template <int CPT>
+template <int CPT, bool WH>
 __device__ __forceinline__ void cols8s_subgrid(
     const unsigned char* box, double* halo, int g, int m, double ax,
-    double ay, double az, double dt_dx, int64_t pyz, int pz, double* peer_lo,
-    double* peer_hi, int X, int mx, const CUtensorMap* omap) {
+    double ay, double az, double dt_dx, double* out, int64_t pyz, int pz,
+    double* peer_lo, double* peer_hi, int X, int mx,
+    const CUtensorMap* omap) {
   constexpr int N = 8;
   const int bx = g / (m * m), by = (g / m) % m, bz = g % m;
   const int col = threadIdx.x & 63, part = threadIdx.x >> 6;
@@ -308,12 +314,22 @@ __device__ __forceinline__ void cols8s_subgrid(
   double* phi = hi ? peer_hi + (int64_t)(i - (N - HX)) * pyz + y * pz +
                          (int64_t)bz * N + HZ
                    : nullptr;
+  // WH: the last HY rows / HZ z cells of the field's last sub-grids
+  // also go to the next field's low y / z halo (the stencil reads only the
+  // 6-point star: halo edges and corners are not needed)
+  const int64_t xo = (int64_t)bx * N + i + HX;
+  const bool yl = WH && by == m - 1 && j >= N - HY;
+  const bool zl = WH && bz == m - 1;
+  double* pyl = out + xo * pyz + (int64_t)(j - (N - HY)) * pz +
+                (int64_t)bz * N + HZ;
+  double* pzl = out + xo * pyz + y * pz - (N - HZ);  // + owned local k
   const int sg = (ax >= 0.0 ? 1 : 0) | (ay >= 0.0 ? 2 : 0) | (az >= 0.0 ? 4 : 0);
   double2 res[CPT / 2];
 #define TF_COLS8S(S)                                                        \
   case S:                                                                   \
-    cols8s_body<CPT, (S & 1) != 0, (S & 2) != 0, (S & 4) != 0>(             \
-        box, halo, i, j, k0, i0, ax, ay, az, dt_dx, lo, hi, plo, phi, res); \
+    cols8s_body<CPT, WH, (S & 1) != 0, (S & 2) != 0, (S & 4) != 0>(       \
+        box, halo, i, j, k0, i0, ax, ay, az, dt_dx, lo, hi, plo, phi, yl,   \
+        pyl, zl, pzl, res);                                                 \
     break;
   switch (sg) {
     TF_COLS8S(0) TF_COLS8S(1) TF_COLS8S(2) TF_COLS8S(3)
@@ -336,7 +352,19 @@ __device__ __forceinline__ void cols8s_subgrid(
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncthreads();
     if (threadIdx.x == 0) {
-      tma_store_3d(omap, stage, bz * N + HZ, by * N + HY, bx * N + HX);
+      const int z0 = bz * N + HZ, y0 = by * N + HY, x0 = bx * N + HX;
+      tma_store_3d(omap, stage, z0, y0, x0);
+      // high periodic y / z halos of the next field: the same tile stored
+      // again one period up, the TMA clipping everything past the padded
+      // array — exactly the HY / HZ halo layers stay.  (A TMA store may
+      // run off the high end only: negative coordinates are an illegal
+      // instruction, scripts/tma_store_probe.cu — the low halos are plain
+      // stores in cols8s_body.)
+      if constexpr (WH) {
+        const int Gy = m * N;
+        if (by == 0) tma_store_3d(omap, stage, z0, y0 + Gy, x0);
+        if (bz == 0) tma_store_3d(omap, stage, z0 + Gy, y0, x0);
+      }
       asm volatile("cp.async.bulk.commit_group;" ::: "memory");
       // the tile must be read out of shared memory before the CTA retires
       asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
@@ -344,13 +372,13 @@ __device__ __forceinline__ void cols8s_subgrid(
   }
 }
 
-template <int CPT, bool DEV_IDS>
+template <int CPT, bool DEV_IDS, bool WH>
 __global__ void __launch_bounds__(cols8_threads<CPT>(), cols8s_min_blocks<CPT>())
     k_step_cols8s(const __grid_constant__ CUtensorMap tmap,
                   const __grid_constant__ CUtensorMap omap,
                   const int32_t* __restrict__ dev_ids,
                   const __grid_constant__ TeamIds team, int m, double ax,
-                  double ay, double az, double dt_dx, double* /*out: via omap*/,
+                  double ay, double az, double dt_dx, double* __restrict__ out,
                   int64_t pyz, int pz, double* peer_lo, double* peer_hi, int X,
                   int mx) {
   constexpr int N = 8;
@@ -371,8 +399,8 @@ __global__ void __launch_bounds__(cols8_threads<CPT>(), cols8s_min_blocks<CPT>()
   mbar_wait(bar, 0);
   double* halo = reinterpret_cast<double*>(box + COLS8S_HALO_OFF) +
                  (threadIdx.x >> 5) * 12 * CPT;
-  cols8s_subgrid<CPT>(box, halo, g, m, ax, ay, az, dt_dx, pyz, pz, peer_lo,
-                      peer_hi, X, mx, &omap);
+  cols8s_subgrid<CPT, WH>(box, halo, g, m, ax, ay, az, dt_dx, out, pyz, pz,
+                            peer_lo, peer_hi, X, mx, &omap);
 }
 
 // Periodic y and z halo of every x layer (z after y so corners are right).
@@ -554,8 +582,20 @@ int launch_step(const CUtensorMap& map, const int32_t* dev_ids,
     const int rc = field_map(out, X, Gy, Gz, N, &omap, true);
     if (rc) return rc;
   }
-  auto kern = N == 8 ? (cpt == 4 ? k_step_cols8s<4, DEV_IDS>
-                                 : k_step_cols8s<8, DEV_IDS>)
+  // TF_STEP_HALO_YZ: the variant that also writes the next field's
+  // periodic y/z halos; TF_STEP_HALO_X: the x halo layers are exactly the
+  // multi-GPU neighbour stores with both neighbours = this field
+  const int hflags = flags & (TF_STEP_HALO_YZ | TF_STEP_HALO_X);
+  if (hflags && N != 8) return TF_E_INVALID;
+  if (hflags & TF_STEP_HALO_X) {
+    if (peer_lo || peer_hi) return TF_E_INVALID;
+    peer_lo = peer_hi = out;
+  }
+  const bool halo = (hflags & TF_STEP_HALO_YZ) != 0;
+  auto kern = N == 8 ? (cpt == 4 ? (halo ? k_step_cols8s<4, DEV_IDS, true>
+                                         : k_step_cols8s<4, DEV_IDS, false>)
+                                 : (halo ? k_step_cols8s<8, DEV_IDS, true>
+                                         : k_step_cols8s<8, DEV_IDS, false>))
                      : k_step_fused<N, 128, DEV_IDS>;
   // > 48 KB of dynamic shared memory (n = 16) needs the opt-in attribute
   int rc = ensure_smem(reinterpret_cast<const void*>(kern), smem);
@@ -698,6 +738,9 @@ int tf_field_step_peer_f64(const double* padded_in, int32_t X, int32_t Gy,
   if (rc) return rc;
   TeamIds team{};
   cudaStream_t st = (cudaStream_t)stream;
+  // (the y/z halos stay with the caller's halo kernels: at config 5 the
+  // halo-writing step variant spills and costs more than they do, 0.57 vs
+  // 0.54 ms per iteration)
   return n == 8 ? launch_step<8, true>(map, ids, team, T, m, ax, ay, az, dt_dx,
                                        padded_out, X, Gy, Gz, st, 0, peer_lo,
                                        peer_hi)

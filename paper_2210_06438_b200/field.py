@@ -117,10 +117,12 @@ class _FieldBase:
 
 
 class FieldPlan:
-    """A formed team plan of the fused step captured as a CUDA graph."""
+    """A formed team plan of the fused step captured as a CUDA graph.
+    halo_flags: TF_STEP_HALO_YZ / TF_STEP_HALO_X (n = 8) — the team kernels
+    also write the next field's periodic halos."""
 
     def __init__(self, teams: list[Team], fi: _FieldBase, src: int,
-                 executors: int, overlap: bool = True):
+                 executors: int, overlap: bool = True, halo_flags: int = 0):
         lib = fi.lib
         ids = np.concatenate([np.asarray(t.ids, np.int32) for t in teams])
         offs = np.zeros(len(teams) + 1, np.int64)
@@ -135,7 +137,8 @@ class FieldPlan:
             exe.ctypes.data_as(C.POINTER(C.c_int32)), len(teams), executors,
             fi.P[src].data_ptr(), fi.X, fi.G, fi.G, fi.n, ax, ay, az,
             fi.dt_dx, fi.P[1 - src].data_ptr(),
-            _lib.TF_LAUNCH_OVERLAP_PREV if overlap else 0, C.byref(h)),
+            (_lib.TF_LAUNCH_OVERLAP_PREV if overlap else 0) | halo_flags,
+            C.byref(h)),
             "tf_plan_capture_field_step")
         self.lib, self.handle = lib, h
         self.kernels = lib.tf_plan_kernels(h)
@@ -159,15 +162,29 @@ class FieldIteration(_FieldBase):
                  device=None, overlap: bool = True):
         super().__init__(grid_n, grid_n, n, velocity, dt_dx, device)
         self.teams = form_teams(range(self.S), max_team, executors)
-        self.plans = [FieldPlan(self.teams, self, src, executors, overlap)
+        # n = 8: the team kernels write the next field's periodic halos
+        # themselves (every sub-grid is in some team), so only a freshly
+        # loaded field needs the halo kernels
+        self.kernel_halo = n == 8
+        hf = _lib.TF_STEP_HALO_YZ | _lib.TF_STEP_HALO_X \
+            if self.kernel_halo else 0
+        self.plans = [FieldPlan(self.teams, self, src, executors, overlap,
+                                halo_flags=hf)
                       for src in (0, 1)]
+        self.halo_fresh = False
         self.field_dev = torch.empty((grid_n,) * 3, dtype=torch.float64,
                                      device=self.device)
 
+    def load(self, field_dev: torch.Tensor, stream=None) -> None:
+        super().load(field_dev, stream)
+        self.halo_fresh = False
+
     def step(self, stream=None) -> None:
-        self.halo(True, stream)
+        if not self.halo_fresh:
+            self.halo(True, stream)
         self.plans[self.cur].launch(stream)
         self.swap()
+        self.halo_fresh = self.kernel_halo
 
     def run_host(self, field_in, field_out, iterations: int = 1) -> None:
         """Host field (pinned) in -> iterations -> host field out."""
@@ -180,7 +197,8 @@ class FieldIteration(_FieldBase):
 
     @property
     def launches_per_step(self) -> int:
-        return 2 + len(self.teams)   # 2 halo kernels + one per team
+        # one kernel per team (+ 2 halo kernels when n = 16)
+        return len(self.teams) + (0 if self.kernel_halo else 2)
 
     def run_host_pipelined(self, field_in, field_out, chunks="taper",
                            down_ctas: int = 16,
@@ -296,6 +314,7 @@ class FieldIteration(_FieldBase):
             launches += 2
         comp.wait_stream(down)
         self.swap()
+        self.halo_fresh = False     # the chunk steps write no halos
         return launches
 
 
@@ -324,6 +343,7 @@ class HostPipeline:
             self.launches = fi.run_host_pipelined(field_in, field_out, chunks,
                                                   down_ctas, down_stream)
         fi.cur = 0
+        fi.halo_fresh = False
         torch.cuda.synchronize()
 
     def run(self) -> None:

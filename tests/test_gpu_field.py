@@ -174,3 +174,38 @@ def test_slab_field_single_rank_overlap(cuda):
         r.iteration(overlap=True)
     torch.cuda.synchronize()
     assert np.array_equal(r.owned().cpu().numpy(), HO.reference_step(f))
+
+
+@pytest.mark.parametrize("vel", [(1.0, 1.0, 1.0), (-0.6, 1.1, -0.9)])
+def test_step_kernel_writes_the_periodic_halos(cuda, vel):
+    """TF_STEP_HALO_YZ | TF_STEP_HALO_X: a team plan over every sub-grid
+    leaves the next field's periodic halo faces exactly as the halo kernels
+    would (edges and corners — never read by the 6-point stencil — are
+    excluded), and chained steps without halo kernels match the reference."""
+    import torch
+    from paper_2210_06438_b200.field import HX, HY, HZ, FieldIteration
+    f = HO.stress_field(32)
+    it = FieldIteration(32, 8, vel, max_team=8, executors=2)
+    it.load(torch.from_numpy(f).to(cuda))
+    it.step()                     # halo kernels (fresh load), then the plan
+    assert it.halo_fresh
+    got = it.field.clone()
+    it.halo(True)                 # what the halo kernels make of it
+    want = it.field.clone()
+    torch.cuda.synchronize()
+    px, py, pz = got.shape
+    ix = np.arange(px)
+    iy = np.arange(py)
+    iz = np.arange(pz)
+    hx = (ix < HX) | (ix >= px - HX)
+    hy = (iy < HY) | (iy >= py - HY)
+    hz = (iz < HZ) | (iz >= pz - HZ)
+    nh = hx[:, None, None].astype(int) + hy[None, :, None] + hz[None, None, :]
+    face = nh <= 1                # interior or exactly one halo coordinate
+    assert (nh == 1).sum() > 0
+    assert np.array_equal(got.cpu().numpy()[face], want.cpu().numpy()[face])
+    for _ in range(2):
+        it.step()
+    torch.cuda.synchronize()
+    assert np.array_equal(it.owned().cpu().numpy(),
+                          HO.reference_step(f, vel))
