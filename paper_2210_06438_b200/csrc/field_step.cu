@@ -188,12 +188,11 @@ __device__ __forceinline__ double ld_swz1(const unsigned char* box, int r,
 constexpr int COLS8S_HALO_OFF = 15504;  // after the box and the mbarrier
 constexpr int COLS8S_SMEM = COLS8S_HALO_OFF + 2 * 96 * 8;  // 17 040 B
 
-template <int CPT, bool WH, bool PX, bool PY, bool PZ>
+template <int CPT, bool PX, bool PY, bool PZ>
 __device__ __forceinline__ void cols8s_body(
     const unsigned char* box, double* halo, int i, int j, int k0, int i0,
     double ax, double ay, double az, double dt_dx, bool lo, bool hi,
-    double* plo, double* phi, bool yl, double* pyl, bool zl, double* pzl,
-    double2* res) {
+    double* plo, double* phi, double2* res) {
   constexpr int BY = COLS8_BXY, HXF = 8 * CPT, HALO = 12 * CPT;
   constexpr int sx = PX ? 0 : 1, sy = PY ? 0 : 1;
   const int lane = threadIdx.x & 31;
@@ -268,10 +267,6 @@ __device__ __forceinline__ void cols8s_body(
     res[q] = w;
     if (lo) *reinterpret_cast<double2*>(plo + k) = w;
     if (hi) *reinterpret_cast<double2*>(phi + k) = w;
-    if constexpr (WH) {     // low periodic y / z halo of the next field
-      if (yl) *reinterpret_cast<double2*>(pyl + k) = w;
-      if (zl && k >= 8 - HZ) *reinterpret_cast<double2*>(pzl + k) = w;
-    }
   }
 }
 
@@ -314,22 +309,12 @@ __device__ __forceinline__ void cols8s_subgrid(
   double* phi = hi ? peer_hi + (int64_t)(i - (N - HX)) * pyz + y * pz +
                          (int64_t)bz * N + HZ
                    : nullptr;
-  // WH: the last HY rows / HZ z cells of the field's last sub-grids
-  // also go to the next field's low y / z halo (the stencil reads only the
-  // 6-point star: halo edges and corners are not needed)
-  const int64_t xo = (int64_t)bx * N + i + HX;
-  const bool yl = WH && by == m - 1 && j >= N - HY;
-  const bool zl = WH && bz == m - 1;
-  double* pyl = out + xo * pyz + (int64_t)(j - (N - HY)) * pz +
-                (int64_t)bz * N + HZ;
-  double* pzl = out + xo * pyz + y * pz - (N - HZ);  // + owned local k
   const int sg = (ax >= 0.0 ? 1 : 0) | (ay >= 0.0 ? 2 : 0) | (az >= 0.0 ? 4 : 0);
   double2 res[CPT / 2];
 #define TF_COLS8S(S)                                                        \
   case S:                                                                   \
-    cols8s_body<CPT, WH, (S & 1) != 0, (S & 2) != 0, (S & 4) != 0>(       \
-        box, halo, i, j, k0, i0, ax, ay, az, dt_dx, lo, hi, plo, phi, yl,   \
-        pyl, zl, pzl, res);                                                 \
+    cols8s_body<CPT, (S & 1) != 0, (S & 2) != 0, (S & 4) != 0>(             \
+        box, halo, i, j, k0, i0, ax, ay, az, dt_dx, lo, hi, plo, phi, res); \
     break;
   switch (sg) {
     TF_COLS8S(0) TF_COLS8S(1) TF_COLS8S(2) TF_COLS8S(3)
@@ -351,6 +336,33 @@ __device__ __forceinline__ void cols8s_subgrid(
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncthreads();
+    if constexpr (WH) {
+      // low periodic y / z halos of the next field (the last HY rows / HZ
+      // z cells of the field's last sub-grids; the stencil reads only the
+      // 6-point star, so halo edges and corners are not needed): copied
+      // out of the staged tile by the first 64 threads, 16 B each
+      auto tile2 = [&](int r, int c) {
+        return *reinterpret_cast<const double2*>(
+            stage + r * 64 + ((c ^ ((r >> 1) & 3)) << 4));
+      };
+      const int t = threadIdx.x;
+      const int64_t xb = (int64_t)bx * N + HX;
+      if (by == m - 1 && t < 64) {           // rows y = 6, 7 -> halo 0, 1
+        const int xx = t >> 3, yy = N - HY + ((t >> 2) & 1), c = t & 3;
+        *reinterpret_cast<double2*>(
+            out + (xb + xx) * pyz + (int64_t)(yy - (N - HY)) * pz +
+            (int64_t)bz * N + HZ + 2 * c) = tile2(xx * 8 + yy, c);
+      }
+      if (bz == m - 1 && t < 64) {           // z = 4..7 -> halo z 0..3
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int r = t, c = 2 + h;
+          *reinterpret_cast<double2*>(
+              out + (xb + (r >> 3)) * pyz +
+              ((int64_t)by * N + (r & 7) + HY) * pz + 2 * h) = tile2(r, c);
+        }
+      }
+    }
     if (threadIdx.x == 0) {
       const int z0 = bz * N + HZ, y0 = by * N + HY, x0 = bx * N + HX;
       tma_store_3d(omap, stage, z0, y0, x0);
@@ -739,8 +751,8 @@ int tf_field_step_peer_f64(const double* padded_in, int32_t X, int32_t Gy,
   TeamIds team{};
   cudaStream_t st = (cudaStream_t)stream;
   // (the y/z halos stay with the caller's halo kernels: at config 5 the
-  // halo-writing step variant spills and costs more than they do, 0.57 vs
-  // 0.54 ms per iteration)
+  // halo-writing step variant measures the same, 0.550 vs 0.542-0.549 ms
+  // per iteration)
   return n == 8 ? launch_step<8, true>(map, ids, team, T, m, ax, ay, az, dt_dx,
                                        padded_out, X, Gy, Gz, st, 0, peer_lo,
                                        peer_hi)
