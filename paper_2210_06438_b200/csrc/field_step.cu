@@ -580,12 +580,13 @@ int launch_step(const CUtensorMap& map, const int32_t* dev_ids,
                 double az, double dt_dx, double* out, int X, int Gy, int Gz,
                 cudaStream_t st, int flags, double* peer_lo = nullptr,
                 double* peer_hi = nullptr) {
-  // n = 8: k_step_cols8s — one thread per column (CPT 8) for launches that
-  // fill the GPU many times over (config 5: 206 vs 191 G cell-updates/s),
-  // two per column (CPT 4) for team-sized launches, where per-sub-grid
-  // latency decides (config 2 team plan: 41 vs 45 us).  n = 16: 128
-  // threads per sub-grid, measured best of 128/256/512.
-  const int cpt = T >= 4096 ? 8 : 4;
+  // n = 8: k_step_cols8s — one thread per column (CPT 8; config 5: 0.54
+  // vs 0.68 ms per iteration with CPT 4; config-2 team plans of 64-128
+  // since the tile store and the halo-writing step: 16.4 vs 18.3 us), two
+  // per column (CPT 4) only for launches of < 64 sub-grids, where
+  // per-sub-grid latency decides.  n = 16: 128 threads per sub-grid,
+  // measured best of 128/256/512.
+  const int cpt = T >= 64 ? 8 : 4;
   const int TH = N == 8 ? (cpt == 4 ? cols8_threads<4>() : cols8_threads<8>())
                         : 128;
   const size_t smem = N == 8 ? COLS8S_SMEM : FGeo<N>::BOX * sizeof(double);
