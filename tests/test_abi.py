@@ -25,6 +25,24 @@ def test_header_symbols_exported(native_lib):
         assert s in _lib.SIGNATURES, f"{s} not bound in _lib.SIGNATURES"
 
 
+def test_header_constants_match_python_mirror():
+    """Every TF_* #define the Python side uses has the header's value."""
+    from paper_2210_06438_b200 import _lib
+    defs = dict(re.findall(r"#define\s+(TF_[A-Z0-9_]+)\s+(-?\d+)",
+                           HEADER.read_text()))
+    mirrored = [k for k in defs if hasattr(_lib, k)]
+    for k in ("TF_LAUNCH_OVERLAP_PREV", "TF_PLAN_TEAM_BUFFERS",
+              "TF_STEP_HALO_YZ", "TF_STEP_HALO_X"):
+        assert k in mirrored, k
+    for k in mirrored:
+        assert getattr(_lib, k) == int(defs[k]), k
+    # the launch / plan / halo flag bits are distinct
+    bits = [int(defs[k]) for k in ("TF_LAUNCH_OVERLAP_PREV",
+                                   "TF_PLAN_TEAM_BUFFERS", "TF_STEP_HALO_YZ",
+                                   "TF_STEP_HALO_X")]
+    assert sum(bits) == (bits[0] | bits[1] | bits[2] | bits[3])
+
+
 def test_no_cpu_fallback():
     """The product path refuses host tensors instead of computing on the CPU."""
     import pytest
