@@ -161,11 +161,16 @@ int32_t tf_region_parent_executor(const tf_region* r, int32_t parent);
 /* AggregationRegion.enter (aggregator.py:284-326) minus the task guard.    */
 int tf_region_enter(tf_region* r, int64_t tag, tf_busy_fn busy, void* ctx,
                     tf_enter_result* out);
-/* Stream drained (device.py:364-370 -> aggregator.py:328-332): closes every
- * forming team whose parent sits on `executor`, in watch order.  Writes up
- * to cap closed team ids to out_teams; returns the count (or <0 error).    */
+/* Stream drained (device.py:364-370 -> aggregator.py:328-332): closes the
+ * forming teams whose parent sits on `executor`, in watch order, at most
+ * `cap` of them (their ids written to out_teams); teams beyond cap stay
+ * forming and watching, so nothing is closed unreported.  Returns the count
+ * (or <0 error).  Size out_teams with tf_region_watch_count.               */
 int tf_region_stream_idle(tf_region* r, int32_t executor, int64_t* out_teams,
                           int32_t cap);
+/* Number of teams watching `executor`'s stream (an upper bound on what the
+ * next tf_region_stream_idle closes).                                      */
+int32_t tf_region_watch_count(const tf_region* r, int32_t executor);
 /* Team bookkeeping.  release frees a closed team's record. */
 int tf_region_release_team(tf_region* r, int64_t team);
 int tf_region_team_size(const tf_region* r, int64_t team);

@@ -67,6 +67,7 @@ SIGNATURES = {
     "tf_region_enter": (C.c_int, [_p, _i64, BUSY_FN, _p,
                                   C.POINTER(EnterResult)]),
     "tf_region_stream_idle": (C.c_int, [_p, _i32, _pi64, _i32]),
+    "tf_region_watch_count": (_i32, [_p, _i32]),
     "tf_region_release_team": (C.c_int, [_p, _i64]),
     "tf_region_team_size": (C.c_int, [_p, _i64]),
     "tf_region_team_members": (C.c_int, [_p, _i64, _pi64, _i32]),

@@ -207,20 +207,32 @@ int tf_region_enter(tf_region* r, int64_t tag, tf_busy_fn busy, void* ctx,
 int tf_region_stream_idle(tf_region* r, int32_t executor, int64_t* out_teams,
                           int32_t cap) {
   if (!r || executor < 0 || executor >= r->executors) return -TF_E_INVALID;
+  if (cap < 0 || (cap > 0 && !out_teams)) return -TF_E_INVALID;
   std::vector<int64_t>& fire = r->fire_scratch;
   fire.swap(r->watchers[executor]);  // keeps both buffers' capacity
   int32_t n = 0;
   for (int64_t id : fire) {
     Team* t = r->teams.get(id);
     if (!t || t->state != FORMING) continue;
+    if (n == cap) {
+      // no room to report it: it keeps watching, so the caller's next call
+      // (sized by tf_region_watch_count) closes it — a team is never closed
+      // without its id reaching the caller
+      r->watchers[executor].push_back(id);
+      continue;
+    }
     Parent& p = r->parents[t->parent];
     if (p.forming == id) p.forming = -1;  // aggregator.py:328-332
     close_team(r, id, *t, DRAIN);
-    if (out_teams && n < cap) out_teams[n] = id;
-    ++n;
+    out_teams[n++] = id;
   }
   fire.clear();
   return n;
+}
+
+int32_t tf_region_watch_count(const tf_region* r, int32_t executor) {
+  if (!r || executor < 0 || executor >= r->executors) return -TF_E_INVALID;
+  return (int32_t)r->watchers[executor].size();
 }
 
 int tf_region_team_size(const tf_region* r, int64_t team) {

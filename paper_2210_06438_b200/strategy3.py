@@ -36,6 +36,23 @@ from .errors import ValidationError
 _CLOSE = {1: "cap", 2: "solo", 3: "drain"}
 
 
+def _check_recon_args(pool, n, um, up, F, amax, slots=None) -> int:
+    """The checks ops.recon_flux makes (shape, dtype, device, capacity of
+    every output) before a bulk path hands raw pointers to TMA maps and
+    device stores; returns the pool's slice count."""
+    from . import ops
+    ops._check_n(n)
+    S = ops._check_pool(pool, n)
+    slots = S if slots is None else slots
+    for t, nm in ((um, "um"), (up, "up"), (F, "F")):
+        ops._check_faces(t, n, slots, nm)
+    if amax is not None:
+        ops._need_cuda_f64(amax, "amax")
+        if amax.numel() < slots:
+            raise ValidationError(f"amax must hold >= {slots} values")
+    return S
+
+
 def default_parents(subgrids: int, max_team: int) -> int:
     """step.py:61 — one parent per expected team."""
     return max(1, subgrids // max_team)
@@ -73,8 +90,15 @@ class FormationCore:
         return res
 
     def stream_idle(self, executor: int) -> list[int]:
-        buf = (C.c_int64 * 8192)()
-        n = self.lib.tf_region_stream_idle(self.handle, executor, buf, 8192)
+        # sized by the core's own watcher count: every closed team's id is
+        # returned (the core never closes a team it could not report)
+        cap = self.lib.tf_region_watch_count(self.handle, executor)
+        if cap < 0:
+            _lib.check(-cap, "tf_region_watch_count")
+        if cap == 0:
+            return []
+        buf = (C.c_int64 * cap)()
+        n = self.lib.tf_region_stream_idle(self.handle, executor, buf, cap)
         if n < 0:
             _lib.check(-n, "tf_region_stream_idle")
         return list(buf[:n])
@@ -159,12 +183,11 @@ class TeamPlan:
         offs[1:] = np.cumsum([len(t.ids) for t in teams])
         exe = np.asarray([t.executor for t in teams], dtype=np.int32)
         self._keep = (ids, offs, exe, pool, um, up, F, amax)
-        S = pool.shape[0]
+        # per-sub-grid slots, or (team buffers) one slot per flat slice
+        S = _check_recon_args(pool, n, um, up, F, amax,
+                              slots=int(ids.size) if team_buffers else None)
         if ids.size and (ids.min() < 0 or ids.max() >= S):
             raise ValidationError("team id outside the pool")
-        for t, nm in ((um, "um"), (up, "up"), (F, "F")):
-            if t.shape[0] < S:
-                raise ValidationError(f"{nm} must hold one slot per sub-grid")
         ax, ay, az = (float(v) for v in velocity)
         h = C.c_void_p()
         rc = self.lib.tf_plan_capture_recon_flux(
@@ -217,7 +240,7 @@ class RealtimeExecutor:
         """Submit the arrivals; returns the number of team launches.  The
         current torch stream (or join_stream) is made to wait for them."""
         arr = np.ascontiguousarray(np.asarray(ids, dtype=np.int32))
-        S = pool.shape[0]
+        S = _check_recon_args(pool, n, um, up, F, amax)
         if arr.size and (arr.min() < 0 or arr.max() >= S):
             raise ValidationError("arrival id outside the pool")
         launches = C.c_int64()
@@ -267,6 +290,9 @@ class QueueExecutor:
         """Publish the arrivals; returns teams published.  The consumer runs
         on `stream` (default: the current stream)."""
         arr = np.ascontiguousarray(np.asarray(ids, dtype=np.int32))
+        S = _check_recon_args(pool, self.n, um, up, F, amax)
+        if arr.size and (arr.min() < 0 or arr.max() >= S):
+            raise ValidationError("arrival id outside the pool")
         s = stream if stream is not None else torch.cuda.current_stream()
         teams = C.c_int64()
         ax, ay, az = (float(v) for v in velocity)

@@ -147,3 +147,25 @@ def test_native_formation_replays_reference(native_lib, traces_golden):
             st = tr["stats"][name]
             assert stats[name] == (st["teams_formed"], st["solo_fast_path"],
                                    st["histogram"]), (tr["name"], name)
+
+
+def test_stream_idle_reports_every_closed_team(native_lib):
+    """More forming teams than any fixed buffer (10 000 parents on one
+    executor): every team the drain closes reaches the caller, and a short
+    buffer leaves the rest forming instead of closing them unreported."""
+    from paper_2210_06438_b200.strategy3 import FormationCore
+    core = FormationCore("reconstruct", 2, 10_000, 1)
+    for tag in range(10_000):
+        res = core.enter(tag, lambda e: True)
+        assert not res.closed
+    lib = native_lib
+    assert lib.tf_region_watch_count(core.handle, 0) == 10_000
+    buf = (C.c_int64 * 16)()
+    assert lib.tf_region_stream_idle(core.handle, 0, buf, 16) == 16
+    assert lib.tf_region_watch_count(core.handle, 0) == 10_000 - 16
+    assert core.stats()["teams_formed"] == 16
+    rest = core.stream_idle(0)
+    assert len(rest) == 10_000 - 16
+    assert sorted(list(buf) + rest) == sorted(set(list(buf) + rest))
+    assert core.stats()["teams_formed"] == 10_000
+    assert lib.tf_region_watch_count(core.handle, 0) == 0
