@@ -4,7 +4,7 @@
 Metric (BASELINE.json): sub-grid cell-updates/s of the hydro
 reconstruct+flux hot path vs aggregation level, and % of HBM peak.
 
-Workload (BASELINE.json configs[1]): Sod shock tube, 4096 8^3 sub-grids
+N = 1 (BASELINE.json configs[1]): Sod shock tube, 4096 8^3 sub-grids
 (grid 128^3), velocity (1,1,1).  One STEP = one iteration of the aggregated
 reconstruct+flux region over all sub-grids: the 4096 task arrivals are
 formed into teams by the strategy-3 formation core (max_team = 128 by
@@ -12,12 +12,19 @@ default, parents = S/max_team as HydroSim does, step.py:61), each team is one
 launch of the batched TMA kernel, and the iteration's team launches replay as
 one CUDA graph over the executor streams.  Inputs are device-resident; two
 input pools alternate between steps (per-step working set 385 MB, 3x L2).
+The timed outputs are checked against digests of the oracle's result
+(tests/golden/bench_cfg2.json) before the line is printed.
+
+N > 1 (BASELINE.json configs[4]): config 5, 262 144 8^3 sub-grids (grid
+512^3, blast field) slab-partitioned over the N GPUs (strong scaling); one
+STEP = one full iteration per rank with the ghost-layer exchange inside it
+(the step kernel stores its boundary layers into the ring neighbours' fields
+over peer memory; NCCL ring variant timed beside it).
 
     python bench.py [--gpus N --steps K --warmup W] [--impl reference]
 
-Multi-GPU (torchrun): weak scaling, each rank owns its own 4096 sub-grids;
-the step has no data-path collective (the recon+flux region is
-embarrassingly parallel), value = all ranks' cell-updates / max-rank time.
+`--gpus N` with N > 1 outside torchrun re-launches itself under
+torch.distributed.run with N ranks (one process per GPU).
 """
 
 from __future__ import annotations
@@ -149,12 +156,35 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------- dist plumbing
-def dist_setup(gpus: int):
+def self_launch(args) -> int:
+    """`--gpus N` (N > 1) outside torchrun: run this script under
+    torch.distributed.run with N ranks on this node (127.0.0.1
+    rendezvous) and return its exit code.  rank 0 prints the line."""
+    import socket
+    import subprocess
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           "--master-port", str(port), os.path.abspath(__file__),
+           *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
+def dist_setup(gpus: int, init: bool = True):
+    """RANK / LOCAL_RANK / WORLD_SIZE from the torchrun environment; the
+    world must be exactly --gpus (a silent 1-rank run of an N-GPU request
+    would report the wrong n_gpus)."""
     import torch
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
+    if world != gpus:
+        raise SystemExit(f"bench.py: --gpus {gpus} but WORLD_SIZE={world}; "
+                         "launch with torchrun --nproc-per-node {gpus} (or "
+                         "without torchrun, which self-launches)")
+    if world > 1 and init:
         import torch.distributed as dist
         # one process per GPU; the modulo only matters when a test squeezes
         # several ranks onto fewer GPUs (TASKFUSE_DIST_BACKEND=gloo)
@@ -163,13 +193,30 @@ def dist_setup(gpus: int):
             torch.cuda.set_device(local)
         backend = os.environ.get("TASKFUSE_DIST_BACKEND", "nccl")
         if backend == "nccl":
+            # the communicator init (ranks, transports) goes to stderr so
+            # the rank count is checkable; stdout carries only the line
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+            os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
             dist.init_process_group(
                 "nccl", device_id=torch.device("cuda", local))
         else:
             dist.init_process_group(backend)
     elif torch.cuda.is_available():
-        torch.cuda.set_device(0)
+        torch.cuda.set_device(local % max(1, torch.cuda.device_count()))
     return world, rank, local
+
+
+def all_true(world, ok: bool) -> bool:
+    """Logical AND over ranks."""
+    if world == 1:
+        return bool(ok)
+    import torch
+    import torch.distributed as dist
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([1 if ok else 0], dtype=torch.int32, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MIN)
+    return bool(t.item())
 
 
 def barrier(world):
@@ -397,6 +444,46 @@ def config3_sweep(args, world, stream, peak, ks, kw):
     return res
 
 
+# ------------------------------------------------------- workload configs
+# One dict per workload, printed verbatim by BOTH arms (ours and
+# --impl reference), so the driver sees the same config on each line.
+def cfg2_config():
+    S = (GRID // N_SUB) ** 3
+    return {
+        "workload": "config 2: Sod shock tube, 4096 8^3 FP64 sub-grids, one "
+                    "aggregated reconstruct+flux iteration per step (um, up, "
+                    "F and the per-sub-grid max signal speed materialised)",
+        "subgrids": S, "subgrid_n": N_SUB, "grid": GRID, "field": FIELD,
+        "velocity": list(VELOCITY),
+        "l2": "inputs larger than L2: two ghost-filled input pools "
+              "alternate between steps; per-step working set 385 MB vs "
+              "126 MB L2"}
+
+
+CFG5_FIELD = "blast"
+
+
+def cfg5_config(world, grid):
+    S = (grid // N_SUB) ** 3
+    return {
+        "workload": f"config 5: blast wave, {S} 8^3 FP64 sub-grids (grid "
+                    f"{grid}^3) slab-partitioned over the GPUs; one full "
+                    "iteration per step (ghost-layer exchange, reconstruct, "
+                    "flux, update)",
+        "subgrids": S, "subgrid_n": N_SUB, "grid": grid, "field": CFG5_FIELD,
+        "velocity": list(VELOCITY),
+        "parallelism": f"x-slab partition over {world} GPU(s)",
+        "l2": f"inputs larger than L2: the field is {grid ** 3 * 8 / 1e9:.2f}"
+              " GB per copy vs 126 MB L2"}
+
+
+def workload_of(args, world):
+    if args.workload != "auto":
+        return args.workload
+    return "cfg2" if world == 1 else "cfg5"
+
+
+# --------------------------------------------------------- CPU baselines
 def cpu_baseline_leg(S, n, grid, steps=2, min_seconds=10.0):
     from oracle.cpu_baseline import CpuBaseline, cpu_model
     cb = CpuBaseline(FIELD, grid, n, VELOCITY, range(S))
@@ -413,86 +500,133 @@ def cpu_baseline_leg(S, n, grid, steps=2, min_seconds=10.0):
     return {"value": rate(S, n, best * 1e3), "unit": UNIT,
             "cores": cb.workers, "kind": "port",
             "sample": (f"all {S} 8^3 sub-grids of config 2 per pass "
-                       f"(prep+reconstruct+flux bodies, oracle port of "
-                       f"hydro/kernels.py), spawn pool of {cb.workers} "
+                       f"(prep+reconstruct+flux+reduce bodies, oracle port "
+                       f"of hydro/kernels.py), spawn pool of {cb.workers} "
                        f"workers, slowest worker, best of {len(times)} "
                        f"passes; CPU {cpu_model()}")}
 
 
-def reference_arm(args, world, rank):
-    """--impl reference: the reference's CPU path (oracle port; the
-    reference is pure Python and is not present on GPU boxes) on all host
-    cores, same metric/config/unit."""
+CFG5_SAMPLE_GRID = 128
+
+
+def reference_arm(args, world, rank, workload):
+    """--impl reference: the reference's CPU path (oracle port of its task
+    bodies; the reference is pure Python and is not present on GPU boxes)
+    on all host cores, same metric / unit / config as our arm.  Under
+    torchrun only rank 0 works and prints."""
     if rank != 0:
         return
     from oracle.cpu_baseline import CpuBaseline, cpu_model
-    S = (GRID // N_SUB) ** 3
-    cb = CpuBaseline(FIELD, GRID, N_SUB, VELOCITY, range(S))
+    if workload == "cfg2":
+        S_run, grid_run, field, bodies = (GRID // N_SUB) ** 3, GRID, FIELD, \
+            "recon_flux"
+        config = cfg2_config()
+        S_metric = S_run
+        sample = (f"all {S_run} sub-grids per step (prep+reconstruct+flux+"
+                  "reduce bodies)")
+    else:
+        # the per-sub-grid CPU cost does not depend on the lattice size, so
+        # the config-5 rate is measured on a 16^3-sub-grid lattice of the
+        # same blast field and bodies (the full 262 144-sub-grid pool would
+        # need 5.8 GB per worker); cell-updates/s carries over linearly
+        S_run, grid_run, field, bodies = (CFG5_SAMPLE_GRID // N_SUB) ** 3, \
+            CFG5_SAMPLE_GRID, CFG5_FIELD, "iteration"
+        config = cfg5_config(world, args.cfg5_grid)
+        S_metric = (args.cfg5_grid // N_SUB) ** 3
+        sample = (f"{S_run} sub-grids per step (a {CFG5_SAMPLE_GRID}^3 "
+                  "blast lattice; exchange_ghosts + prep + reconstruct + "
+                  "flux + reduce + update per sub-grid, the CPU task "
+                  "iteration of step.py:93-97), rate extrapolated linearly "
+                  f"to {S_metric} sub-grids")
+    cb = CpuBaseline(field, grid_run, N_SUB, VELOCITY, range(S_run),
+                     bodies=bodies)
     try:
         for _ in range(args.warmup):
             cb.step()
         times = [cb.step() for _ in range(args.steps)]
     finally:
         cb.close()
-    ms = 1e3 * sum(times) / len(times)
-    value = rate(S, N_SUB, ms)
+    ms_run = 1e3 * sum(times) / len(times)
+    value = rate(S_run, N_SUB, ms_run)
+    ms = ms_run * S_metric / S_run
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak" if workload == "cfg2" else "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "config 2: Sod shock tube, 4096 8^3 "
-                   "sub-grids, one reconstruct+flux iteration per step",
-                   "subgrids": S, "subgrid_n": N_SUB},
+        "config": config,
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cb.workers,
                          "kind": "port",
-                         "sample": f"all {S} sub-grids per step, spawn pool "
-                                   f"of {cb.workers}, CPU {cpu_model()}"},
+                         "sample": f"{sample}; spawn pool of {cb.workers} "
+                                   f"workers, CPU {cpu_model()}"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
+# --------------------------------------------------------------- e2e legs
 def e2e_leg(args, steps, warmup, world, stream):
-    """Same metric through the public API with HOST buffers
-    (strategy3.AggregatedIteration.run_host): every step copies the global
-    field host->device from pinned memory, scatters it into the sub-grid
-    pool, fills ghosts, runs the aggregated reconstruct+flux team plan and
-    the update, and reads the updated field back device->host.  More work
-    than the recon+flux metric counts (ghost fill + update), so it is a
-    conservative end-to-end rate."""
+    """The headline e2e: the same aggregated reconstruct+flux iteration as
+    `value`, through the public API with HOST buffers
+    (strategy3.AggregatedIteration.recon_flux_host): every step copies the
+    pinned host field host->device, scatters it into the sub-grid pool and
+    fills the ghosts (make_state + exchange_ghosts, which `value` and the
+    CPU arm get for free), runs the captured A-team plan (um / up / F to
+    HBM) and reads the step's result — the per-sub-grid max signal speed,
+    the reduce stage's output — back device->host."""
     import torch
     from paper_2210_06438_b200.hydro import sod_field
     from paper_2210_06438_b200.strategy3 import AggregatedIteration
     it = AggregatedIteration(GRID, N_SUB, VELOCITY, max_team=args.max_team,
                              executors=args.executors)
     host_in = sod_field(GRID, "cpu").pin_memory()
-    host_out = torch.empty_like(host_in).pin_memory()
+    amax = torch.empty(it.S, dtype=torch.float64).pin_memory()
 
     def step(k):
-        it.run_host(host_in, host_out)
+        it.recon_flux_host(host_in, amax)
     ms = timed(step, steps, warmup, world, stream)
     torch.cuda.synchronize()
-    return ms, host_in.numel() * 8, host_out.numel() * 8, \
-        it.launches_per_step + 2
+    ok = bool((amax == max(abs(v) for v in VELOCITY)).all())
+    res = {"value": rate(it.S * world, N_SUB, ms), "unit": UNIT,
+           "ms_per_step": ms, "h2d_bytes_per_step": host_in.numel() * 8,
+           "d2h_bytes_per_step": amax.numel() * 8,
+           "gpu_launches_per_step": it.recon_flux_launches,
+           "result_check": ok,
+           "step": "pinned host field -> device, scatter into the sub-grid "
+                   "pool + ghost fill, aggregated reconstruct+flux teams "
+                   "(um/up/F to HBM, captured plan), per-sub-grid max "
+                   "signal speed -> pinned host "
+                   "(AggregatedIteration.recon_flux_host)"}
+    # the same iteration with the update and the whole field back
+    host_out = torch.empty_like(host_in).pin_memory()
+    ms_it = timed(lambda k: it.run_host(host_in, host_out), steps, warmup,
+                  world, stream)
+    res["full_iteration_host_roundtrip"] = {
+        "value": rate(it.S * world, N_SUB, ms_it), "unit": UNIT,
+        "ms_per_step": ms_it, "h2d_bytes_per_step": host_in.numel() * 8,
+        "d2h_bytes_per_step": host_out.numel() * 8,
+        "step": "host field in -> scatter, ghost fill, aggregated "
+                "recon+flux teams (um/up/F to HBM), update -> host field out "
+                "(AggregatedIteration.run_host)"}
+    return res
 
 
 def fused_legs(args, steps, warmup, world, stream, peak):
     """The fused full iteration (field.FieldIteration, SURVEY §8 f #2) on
-    config 2: device-resident step and the host round trip."""
+    config 2: device-resident step and the host round trip (a different
+    computation from the headline: reconstruct+flux+update without
+    materialising the faces)."""
     import torch
     from paper_2210_06438_b200.hydro import sod_field
-    from paper_2210_06438_b200.field import FieldIteration
+    from paper_2210_06438_b200.field import FieldIteration, HostPipeline
     it = FieldIteration(GRID, N_SUB, VELOCITY, max_team=args.max_team,
                         executors=args.executors)
     it.load(sod_field(GRID, "cuda"))
     ms_dev = timed(lambda k: it.step(), steps, warmup, world, stream)
     host_in = sod_field(GRID, "cpu").pin_memory()
     host_out = torch.empty_like(host_in).pin_memory()
-    ms_e2e = timed(lambda k: it.run_host(host_in, host_out), steps, warmup,
-                   world, stream)
-    from paper_2210_06438_b200.field import HostPipeline
     pipe = HostPipeline(it, host_in, host_out)
     ms_pipe = timed(lambda k: pipe.run(), steps, warmup, world, stream)
     S = (GRID // N_SUB) ** 3
@@ -501,25 +635,20 @@ def fused_legs(args, steps, warmup, world, stream, peak):
     return {
         "device": {"value": rate(S * world, n, ms_dev), "unit": UNIT,
                    "ms_per_step": ms_dev,
-                   "hbm_frac": fused_bytes / (ms_dev * 1e-3) / 1e9 / peak,
+                   "b_step_frac": fused_bytes / (ms_dev * 1e-3) / 1e9 / peak,
                    "launches_per_step": it.launches_per_step,
                    "step": "one fused recon+flux+update kernel per team, "
                            "each also writing its sub-grids' share of the "
                            "next field's periodic halos (CUDA graph)"},
-        "e2e": {"value": rate(S * world, n, ms_e2e), "unit": UNIT,
-                "ms_per_step": ms_e2e,
-                "h2d_bytes_per_step": host_in.numel() * 8,
-                "d2h_bytes_per_step": host_out.numel() * 8},
-        "e2e_pipelined": {
+        "host_pipelined": {
             "value": rate(S * world, n, ms_pipe), "unit": UNIT,
             "ms_per_step": ms_pipe,
             "h2d_bytes_per_step": host_in.numel() * 8,
             "d2h_bytes_per_step": host_out.numel() * 8,
             "gpu_launches_per_step": pipe.launches,
-            "step": "field.HostPipeline: tapered x-chunks (sub-grid layers "
-                    "[1,3,4,4,3,1]), copy-engine upload shifted by the x "
-                    "halo / one pad+halo kernel / fused step / zero-copy download "
-                    "kernel, overlapped, captured as one CUDA graph"},
+            "step": "field.HostPipeline: tapered x-chunks, copy-engine "
+                    "upload / pad+halo kernel / fused step / zero-copy "
+                    "download kernel, overlapped, one CUDA graph"},
     }
 
 
@@ -542,93 +671,206 @@ def e2e_faces_leg(wl, step_fn, steps, warmup, world, stream):
     return ms, host_in.numel() * 8, sum(o.numel() * 8 for o in outs)
 
 
-def cfg5_leg(args, world, rank, local, peak):
-    """BASELINE config 5: 262 144 8^3 sub-grids (grid 512^3, blast field)
-    slab-partitioned over the ranks (strong scaling: fixed total).  One step
-    = one full device iteration per rank: pack halo planes, ring exchange
-    (NCCL P2P), ghost fill (interior layers overlapped with the exchange),
-    aggregated reconstruct+flux, update."""
-    import numpy as np
+# -------------------------------------------------------------- self-checks
+def cfg2_output_check(wl, plans, team_buffers=True):
+    """The timed team plan's outputs against the oracle's digests for this
+    exact workload (tests/golden/bench_cfg2.json; the Sod data are exactly
+    representable, so the digests are machine-independent).  Packed team
+    leases are put back in sub-grid order first."""
+    import hashlib
     import torch
-    from paper_2210_06438_b200.field import SlabFieldIteration
-    from paper_2210_06438_b200.parallel_halo import SlabHydro, SlabPartition
-    grid, n = args.cfg5_grid, N_SUB
-    part = SlabPartition(grid, n, world, rank)
+    path = os.path.join(ROOT, "tests", "golden", "bench_cfg2.json")
+    with open(path) as fh:
+        want = json.load(fh)
+    torch.cuda.synchronize()
+    plans[0].launch()
+    torch.cuda.synchronize()
+    if team_buffers:
+        inv = torch.empty(wl.S, dtype=torch.int64, device="cuda")
+        order = torch.from_numpy(plans[0].order.astype(np.int64)).cuda()
+        inv[order] = torch.arange(wl.S, device="cuda")
+    else:
+        inv = torch.arange(wl.S, device="cuda")
+    got = {}
+    for name, t in (("um", wl.um), ("up", wl.up), ("F", wl.F)):
+        a = t[inv].cpu().numpy()
+        got[name] = hashlib.sha256(
+            np.ascontiguousarray(a, "<f8").tobytes()).hexdigest()
+    amax_ok = bool((wl.amax == want["amax"]).all())
+    ok = all(got[k] == want[k] for k in ("um", "up", "F")) and amax_ok
+    return {"bitexact_vs_oracle_digest": ok,
+            "digests": "tests/golden/bench_cfg2.json (um, up, F sha256)",
+            "amax_ok": amax_ok}
+
+
+# ------------------------------------------------------------ config 5
+def cfg5_slab(part, grid):
+    """The slab of initial_field (scenario.py:30-37) on this rank."""
+    n = N_SUB
     a = part.x0 * n
     x = (np.arange(grid) + 0.5) / grid
-    # the slab of initial_field (scenario.py:30-37), evaluated per slab
     xs = x[a:a + part.mx * n]
     r2 = ((xs - 0.5) ** 2)[:, None, None] + ((x - 0.5) ** 2)[None, :, None] \
         + ((x - 0.5) ** 2)[None, None, :]
-    slab = 1.0 + 1.0 * np.exp(-r2 / (2.0 * 0.1 ** 2))
+    return 1.0 + 1.0 * np.exp(-r2 / (2.0 * 0.1 ** 2))
+
+
+def peer_access_ok(part, local) -> bool:
+    """Can this rank's GPU store into both ring neighbours' memory?  One
+    node, one process per GPU: rank r drives GPU r (mod the device count —
+    ranks sharing a GPU map each other's memory on the same device)."""
+    import torch
+    if part.world == 1:
+        return True
+    ngpu = torch.cuda.device_count()
+    for r in (part.left, part.right):
+        other = r % ngpu
+        if other != local and not torch.cuda.can_device_access_peer(
+                local, other):
+            return False
+    return True
+
+
+def cfg5_leg(args, world, rank, local, peak):
+    """BASELINE config 5: 262 144 8^3 sub-grids (grid 512^3, blast field)
+    slab-partitioned over the ranks (strong scaling: fixed total).  One step
+    = one full device iteration per rank with the ghost-layer exchange
+    inside it.  Headline: the peer-fused step (boundary layers stored into
+    the neighbours' fields by the step kernel); the NCCL-ring exchange and
+    the materialising pool path are timed beside it.  All three paths'
+    first iteration from the initial field must agree bit for bit (each
+    is pinned to the oracle at this size by tests/test_gpu_fullsize.py)."""
+    import torch
+    from paper_2210_06438_b200.field import (PeerSlabFieldIteration,
+                                             SlabFieldIteration)
+    from paper_2210_06438_b200.parallel_halo import SlabHydro, SlabPartition
+    grid, n = args.cfg5_grid, N_SUB
+    part = SlabPartition(grid, n, world, rank)
+    slab = cfg5_slab(part, grid)
     dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream()
-    # fused path with the exchange fused into the compute over peer memory
-    # (the step measured for `value`)
-    from paper_2210_06438_b200.field import PeerSlabFieldIteration
-    peer = PeerSlabFieldIteration(part, slab, VELOCITY, device=dev)
-    with ClockSampler(local) as clk:
-        ms = timed(lambda k: peer.iteration(), args.steps, args.warmup,
-                   world, stream)
-    peer.check()
-    del peer
-    torch.cuda.empty_cache()
-    # fused step with a separate NCCL ring exchange, interior overlapped
-    fused = SlabFieldIteration(part, slab, VELOCITY, device=dev)
-    ms_nccl = timed(lambda k: fused.iteration(overlap=True), args.steps,
+    S_total = (grid // n) ** 3
+    use_peer = all_true(world, peer_access_ok(part, local))
+    checks = {}
+
+    def first_iteration(obj, run):
+        run()
+        torch.cuda.synchronize()
+        return obj.owned()
+
+    # NCCL ring (interior overlapped with the exchange)
+    ring = SlabFieldIteration(part, slab, VELOCITY, device=dev)
+    ref = first_iteration(ring, lambda: ring.iteration(overlap=True))
+    ms_nccl = timed(lambda k: ring.iteration(overlap=True), args.steps,
                     args.warmup, world, stream)
-    del fused
+    del ring
     torch.cuda.empty_cache()
+    ms_peer = None
+    clk = None
+    if use_peer:
+        peer = PeerSlabFieldIteration(part, slab, VELOCITY, device=dev)
+        got = first_iteration(peer, peer.iteration)
+        peer.check()
+        checks["peer_fused_vs_nccl_ring"] = all_true(world,
+                                                     torch.equal(got, ref))
+        del got
+        with ClockSampler(local) as clk:
+            ms_peer = timed(lambda k: peer.iteration(), args.steps,
+                            args.warmup, world, stream)
+        peer.check()
+        # end to end: pinned host slab in, one iteration, host slab out
+        h_in = torch.from_numpy(slab).pin_memory()
+        h_out = torch.empty_like(h_in).pin_memory()
+        ms_e2e = timed(lambda k: peer.run_host(h_in, h_out),
+                       max(3, args.steps // 4), 3, world, stream)
+        peer.check()
+        del peer
+        torch.cuda.empty_cache()
+    else:
+        ring = SlabFieldIteration(part, slab, VELOCITY, device=dev)
+        with ClockSampler(local) as clk:
+            ms_nccl = timed(lambda k: ring.iteration(overlap=True),
+                            args.steps, args.warmup, world, stream)
+        h_in = torch.from_numpy(slab).pin_memory()
+        h_out = torch.empty_like(h_in).pin_memory()
+        dev_f = torch.empty(h_in.shape, dtype=torch.float64, device=dev)
+
+        def ring_host(k):
+            dev_f.copy_(h_in, non_blocking=True)
+            ring.load(dev_f)
+            ring.iteration(overlap=True)
+            ring.store(dev_f)
+            h_out.copy_(dev_f, non_blocking=True)
+        ms_e2e = timed(ring_host, max(3, args.steps // 4), 3, world, stream)
+        del ring, dev_f
+        torch.cuda.empty_cache()
     # materialising path (ghosted sub-grid pool, faces in HBM, update)
     pool = SlabHydro(part, slab, VELOCITY, device=dev)
+    got = first_iteration(pool, lambda: pool.iteration(overlap=True))
+    checks["materialising_vs_nccl_ring"] = all_true(world,
+                                                    torch.equal(got, ref))
+    del got, ref
     ms_pool = timed(lambda k: pool.iteration(overlap=True),
                     max(3, args.steps // 2), args.warmup, world, stream)
     del pool, slab
     torch.cuda.empty_cache()
-    S_total = (grid // n) ** 3
+    if not all(checks.values()):
+        raise SystemExit(f"bench.py cfg5: paths disagree {checks}")
+    ms = ms_peer if use_peer else ms_nccl
     value = rate(S_total, n, ms)
     bytes_alg = part.subgrids * b_alg(n)
-    fused_bytes = part.subgrids * b_step(n)
-    return {
+    unique = part.subgrids * 16 * n ** 3    # field in + out, 16 B per cell
+    # per iteration: 2 halo kernels + the step (+ the peer barrier, or a
+    # second step launch for the boundary layers on the NCCL path; NCCL's
+    # own kernels are not counted)
+    launches = 4
+    line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"config 5: blast wave, {S_total} 8^3 "
-                   f"sub-grids (grid {grid}^3) slab-partitioned over "
-                   f"{world} GPU(s); one full iteration per step (halo "
-                   "exchange, ghost fill, recon+flux, update)",
-                   "subgrids_per_gpu": part.subgrids,
-                   "halo_bytes_per_rank_per_step": 2 * part.plane_bytes,
-                   "parallelism": f"x-slab partition x{world}; boundary "
-                                  "layers stored into the ring neighbours' "
-                                  "fields by the step kernel over CUDA-IPC "
-                                  "peer memory + device peer barrier"},
+        "config": cfg5_config(world, grid),
+        "run": {"path": ("peer-fused: the step kernel stores the slab's "
+                         "boundary layers into the ring neighbours' next "
+                         "fields over CUDA-IPC peer memory, then a device "
+                         "peer barrier" if use_peer else
+                         "NCCL ring exchange of the halo planes, interior "
+                         "layers stepped while they are in flight "
+                         "(no peer access between the GPUs)"),
+                "subgrids_per_gpu": part.subgrids,
+                "halo_bytes_per_rank_per_step": 2 * part.plane_bytes,
+                "dist_backend": (os.environ.get("TASKFUSE_DIST_BACKEND",
+                                                "nccl") if world > 1
+                                 else None)},
+        "self_check": checks,
+        "gpu_launches": launches * args.steps,
         "nccl_exchange_path": {
             "ms_per_step": ms_nccl, "value": rate(S_total, n, ms_nccl),
             "step": "fused step + separate NCCL ring exchange of the halo "
                     "planes, interior layers overlapped"},
         "roofline": {
             "bound": "hbm", "unit": "GB/s", "peak": peak,
-            "achieved": fused_bytes / (ms * 1e-3) / 1e9,
-            "frac": fused_bytes / (ms * 1e-3) / 1e9 / peak,
+            "achieved": unique / (ms * 1e-3) / 1e9,
+            "frac": unique / (ms * 1e-3) / 1e9 / peak,
             "traffic": ncu_traffic_per_launch(
                 part.subgrids, "r01_ncu_step_fused_cfg5g256.txt"),
-            # the field itself read once and written once (16 B per cell):
-            # the DRAM floor of the fused step if every halo re-read hits L2
-            "unique_dram_frac": part.subgrids * 16 * n ** 3
-            / (ms * 1e-3) / 1e9 / peak,
-            "note": "fused step, SURVEY §8(d) B_step = 8[(n+2)^3 + "
-                    "6(n+2)^2 + n^3] = 16 896 B per 8^3 sub-grid; halo "
-                    "refresh and exchange inside the step. frac can exceed "
-                    "1: B_step counts each sub-grid's halo reads, which the "
-                    "padded-field layout serves from L2 (traffic = DRAM "
-                    "bytes per step-kernel launch from the ncu capture at "
-                    "grid 256, scaled: ~7.4 KB per sub-grid). "
-                    "unique_dram_frac = 16 B per cell (field in + out) / "
-                    "step time / peak: the DRAM floor's fraction; the "
-                    "kernel is latency / L2-bound, DESIGN.md §4"},
-        "clocks": clk.summary(),
+            "per_subgrid_alg_bytes": 16 * n ** 3,
+            "note": "fused step; algorithmic bytes = the field read once "
+                    "and written once, 16 B per cell (8 KB per 8^3 "
+                    "sub-grid): every halo re-read is served by L2 in the "
+                    "padded-field layout (DESIGN.md §4), so this is the "
+                    "DRAM floor.  b_step_frac counts SURVEY §8(d)'s B_step "
+                    "= 16 896 B per sub-grid (halo reads included)",
+            "b_step_frac": part.subgrids * b_step(n) / (ms * 1e-3) / 1e9
+            / peak},
+        "clocks": clk.summary() if clk else None,
+        "e2e": {"value": rate(S_total, n, ms_e2e), "unit": UNIT,
+                "ms_per_step": ms_e2e,
+                "h2d_bytes_per_step": part.subgrids * n ** 3 * 8,
+                "d2h_bytes_per_step": part.subgrids * n ** 3 * 8,
+                "step": "per rank: pinned host slab -> device, pad, prime "
+                        "the neighbours' halos, one iteration, slab -> "
+                        "pinned host (PeerSlabFieldIteration.run_host)"},
         "materialising_path": {
             "ms_per_step": ms_pool,
             "value": rate(S_total, n, ms_pool),
@@ -637,8 +879,10 @@ def cfg5_leg(args, world, rank, local, peak):
             "step": "pack+exchange, ghost fill, recon+flux (um/up/F to "
                     "HBM), update"},
     }
+    return line
 
 
+# -------------------------------------------------------------------- main
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -663,16 +907,23 @@ def main():
     ap.add_argument("--no-overlap", action="store_true",
                     help="disable PDL overlap of consecutive team launches")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--workload", choices=("cfg2", "cfg5"), default="cfg2")
+    ap.add_argument("--workload", choices=("auto", "cfg2", "cfg5"),
+                    default="auto",
+                    help="auto: config 2 on one GPU, config 5 (strong "
+                         "scaling with the ghost exchange) on N > 1")
     ap.add_argument("--cfg5-grid", type=int, default=512)
     ap.add_argument("--profile-only", action="store_true",
                     help="just warm-up+timed hot-path steps (for ncu)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
 
-    world, rank, local = dist_setup(args.gpus)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        raise SystemExit(self_launch(args))
+    world, rank, local = dist_setup(args.gpus,
+                                    init=args.impl != "reference")
+    workload = workload_of(args, world)
     if args.impl == "reference":
-        reference_arm(args, world, rank)
+        reference_arm(args, world, rank, workload)
         return
     import torch
     from paper_2210_06438_b200 import _lib
@@ -680,7 +931,7 @@ def main():
     assert lib.tf_check_device(local) == 0, "not an sm_100 device"
     peak, peak_src = peaks()
     stream = torch.cuda.current_stream()
-    if args.workload == "cfg5":
+    if workload == "cfg5":
         line = cfg5_leg(args, world, rank, local, peak)
         if rank == 0:
             print(json.dumps(line), flush=True)
@@ -689,10 +940,11 @@ def main():
             dist.destroy_process_group()
         return
     wl = Workload()
+    plans = None
     if args.mode == "plan":
-        step, nk, hist, _ = plan_runner(wl, args.max_team, args.executors,
-                                        overlap=not args.no_overlap,
-                                        team_buffers=args.outputs == "team")
+        step, nk, hist, plans = plan_runner(
+            wl, args.max_team, args.executors, overlap=not args.no_overlap,
+            team_buffers=args.outputs == "team")
         launches_per_step = nk
     elif args.mode == "realtime":
         step, launches, _ = realtime_runner(wl, args.max_team, args.executors)
@@ -718,6 +970,11 @@ def main():
     value = rate(total_S, wl.n, ms)
     bytes_step = wl.S * b_alg(wl.n)
     achieved = bytes_step / (ms * 1e-3) / 1e9
+    check = cfg2_output_check(wl, plans, args.outputs == "team") \
+        if plans else None
+    if check is not None and not check["bitexact_vs_oracle_digest"]:
+        raise SystemExit(f"bench.py: timed outputs differ from the oracle "
+                         f"digests {check}")
     # the kernel timed alone: one launch over all slices (aggregation limit)
     ms_single = timed(single_runner(wl), args.steps, args.warmup, world,
                       stream)
@@ -726,18 +983,13 @@ def main():
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic",
-        "config": {
-            "workload": "config 2: Sod shock tube, 4096 8^3 FP64 sub-grids "
-                        "per GPU, one aggregated reconstruct+flux iteration "
-                        "per step",
-            "subgrids_per_gpu": wl.S, "subgrid_n": wl.n, "grid": GRID,
-            "max_team": args.max_team, "executors": args.executors,
-            "mode": args.mode, "team_histogram": hist,
-            "outputs": ("packed team leases (slice_alloc layout)"
-                        if args.outputs == "team" else "per-sub-grid slots"),
-            "parallelism": f"sub-grid partition x{world} (no collective)",
-            "l2": "two input pools alternate; per-step working set "
-                  f"{(bytes_step + wl.S * 8 * 2744) / 1e6:.0f} MB vs 126 MB L2"},
+        "config": cfg2_config(),
+        "run": {"max_team": args.max_team, "executors": args.executors,
+                "mode": args.mode, "team_histogram": hist,
+                "outputs": ("packed team leases (slice_alloc layout)"
+                            if args.outputs == "team"
+                            else "per-sub-grid slots")},
+        "self_check": check,
         "gpu_launches": launches_per_step * args.steps,
         "roofline": {
             "bound": "hbm", "achieved": achieved, "peak": peak,
@@ -759,41 +1011,26 @@ def main():
                 "frac": bytes_step / (ms_single * 1e-3) / 1e9 / peak}},
         "clocks": clk.summary(),
     }
-    e_ms, bi, bo, e_launch = e2e_leg(args, max(10, args.steps // 2), 3,
-                                     world, stream)
-    line["e2e_materialising"] = {
-        "value": rate(total_S, wl.n, e_ms), "unit": UNIT,
-        "h2d_bytes_per_step": bi, "d2h_bytes_per_step": bo,
-        "ms_per_step": e_ms,
-        "step": "host field (pinned) -> device scatter -> ghost fill -> "
-                "aggregated recon+flux teams (um/up/F to HBM) -> update -> "
-                "gather -> host field (AggregatedIteration.run_host)",
-        "gpu_launches_per_step": e_launch}
-    f_ms, fbi, fbo = e2e_faces_leg(wl, step, max(5, args.steps // 5), 3,
-                                   world, stream)
-    line["fused_full_iteration"] = fused_legs(args, max(10, args.steps // 2),
-                                              3, world, stream, peak)
-    # headline e2e: the public host->host iteration API (pinned host field
-    # in, one hydro iteration = reconstruct + flux + update of every
-    # sub-grid, pinned host field out), transfers overlapped with compute
-    line["e2e"] = dict(line["fused_full_iteration"]["e2e_pipelined"])
+    line["e2e"] = e2e_leg(args, max(10, args.steps // 2), 3, world, stream)
     # the host link bounds e2e: bytes both ways per step against the
     # measured concurrent copy-engine rate (48.9 GB/s per direction on this
     # pool's boxes, profiles/r01_pcie_probe2.log)
     e = line["e2e"]
-    link = e["h2d_bytes_per_step"] + e["d2h_bytes_per_step"]
-    e["link"] = {"bytes_per_step": link,
-                 "achieved_GBps": link / (e["ms_per_step"] * 1e-3) / 1e9,
-                 "bidirectional_peak_GBps": 2 * 48.9,
-                 "frac": link / (e["ms_per_step"] * 1e-3) / 1e9 / 97.8,
-                 "floor_ms": max(e["h2d_bytes_per_step"],
-                                 e["d2h_bytes_per_step"]) / 48.9e9 * 1e3}
-    line["schemes_one_launch"] = scheme_legs(wl, max(10, args.steps // 2), 3,
-                                             world, stream, peak)
+    e["link"] = {"bytes_per_step": e["h2d_bytes_per_step"]
+                 + e["d2h_bytes_per_step"],
+                 "floor_ms": e["h2d_bytes_per_step"] / 48.9e9 * 1e3,
+                 "frac_of_upload_floor": e["h2d_bytes_per_step"] / 48.9e9
+                 * 1e3 / e["ms_per_step"]}
+    f_ms, fbi, fbo = e2e_faces_leg(wl, step, max(5, args.steps // 5), 3,
+                                   world, stream)
     line["e2e_faces"] = {"value": rate(total_S, wl.n, f_ms), "unit": UNIT,
                          "h2d_bytes_per_step": fbi,
                          "d2h_bytes_per_step": fbo, "ms_per_step": f_ms,
                          "step": "ghosted pool in, um/up/F out"}
+    line["fused_full_iteration"] = fused_legs(args, max(10, args.steps // 2),
+                                              3, world, stream, peak)
+    line["schemes_one_launch"] = scheme_legs(wl, max(10, args.steps // 2), 3,
+                                             world, stream, peak)
     if not args.no_sweep:
         line["sweep"] = run_sweep(wl, args, world, stream, peak)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -425,6 +425,27 @@ class PeerSlabFieldIteration(_FieldBase):
         self._barrier()
         self.swap()
 
+    def run_host(self, slab_in, slab_out) -> None:
+        """End-to-end iteration of this rank's slab through HOST buffers:
+        the pinned (mx*n, G, G) slab goes host->device and is padded, its
+        boundary layers are primed into the neighbours' halos (peer copies
+        + device barrier), one fused iteration runs with the exchange fused
+        into the step, and the updated slab comes back to the pinned
+        `slab_out`.  Every rank calls it once per step."""
+        if not (slab_in.is_pinned() and slab_out.is_pinned()):
+            raise ValidationError("run_host needs pinned host slabs")
+        dev = getattr(self, "_host_dev", None)
+        if dev is None:
+            dev = self._host_dev = torch.empty(
+                (self.X, self.G, self.G), dtype=torch.float64,
+                device=self.device)
+        dev.copy_(slab_in, non_blocking=True)
+        self.load(dev)
+        self._prime()
+        self.iteration()
+        self.store(dev)
+        slab_out.copy_(dev, non_blocking=True)
+
     def check(self) -> None:
         """Raise if a peer barrier timed out."""
         if int(self.err.item()):

@@ -104,6 +104,14 @@ def exchange_halos(part: SlabPartition, lo, hi, halo_lo, halo_hi,
         halo_hi.copy_(lo)
         return
     import torch.distributed as dist
+    if lo.is_cuda and dist.get_backend(group) == "gloo":
+        # gloo moves host tensors only (ranks sharing one GPU in tests):
+        # stage the planes through host memory
+        h = [t.cpu() for t in (lo, hi, halo_lo, halo_hi)]
+        exchange_halos(part, *h, group=group)
+        halo_lo.copy_(h[2])
+        halo_hi.copy_(h[3])
+        return
     ops_ = [dist.P2POp(dist.isend, hi, part.right, group, tag=1),
             dist.P2POp(dist.isend, lo, part.left, group, tag=2),
             dist.P2POp(dist.irecv, halo_lo, part.left, group, tag=1),

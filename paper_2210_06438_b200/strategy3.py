@@ -350,11 +350,13 @@ class AggregatedIteration:
         self.um = torch.empty((S, 3, c, c, c), **f64)
         self.up = torch.empty_like(self.um)
         self.F = torch.empty_like(self.um)
+        self.amax = torch.empty(S, **f64)
         self.field_dev = torch.empty((grid_n,) * 3, **f64)
         self.teams = form_teams(range(S), max_team, executors)
         # one captured plan per pool (the pools swap every iteration)
         self.plans = [TeamPlan(self.teams, p, n, self.velocity, self.um,
-                               self.up, self.F, executors, overlap=overlap)
+                               self.up, self.F, executors, amax=self.amax,
+                               overlap=overlap)
                       for p in self.pools]
         self.cur = 0
 
@@ -385,6 +387,30 @@ class AggregatedIteration:
             self.step()
         self.store(self.field_dev)
         field_out.copy_(self.field_dev, non_blocking=True)
+
+    def recon_flux_host(self, field_in, amax_out) -> None:
+        """End-to-end aggregated reconstruct+flux from a HOST field: the
+        pinned (grid^3) field goes host->device, is scattered into the
+        current sub-grid pool and ghost-filled (make_state +
+        exchange_ghosts, scenario.py:83-142), the region's captured team
+        plan runs (reconstruct_body + flux_body per slice, um / up / F
+        materialised in HBM), and the per-sub-grid max signal speed — the
+        reduce stage's result (kernels.py:96-97) — comes back to the pinned
+        `amax_out` (S doubles).  Stream-ordered on the current stream."""
+        if not (field_in.is_pinned() and amax_out.is_pinned()):
+            raise ValidationError("recon_flux_host needs pinned host buffers")
+        if amax_out.numel() < self.S:
+            raise ValidationError(f"amax_out must hold {self.S} values")
+        self.field_dev.copy_(field_in, non_blocking=True)
+        self.load(self.field_dev)
+        self.ops.ghost_fill(self.pool, self.n, self.m)
+        self.plans[self.cur].launch()
+        amax_out[:self.S].copy_(self.amax, non_blocking=True)
+
+    @property
+    def recon_flux_launches(self) -> int:
+        """Kernels per recon_flux_host call: scatter, ghost fill, teams."""
+        return 2 + len(self.teams)
 
     @property
     def launches_per_step(self) -> int:

@@ -39,3 +39,29 @@ def test_bench_line_contract(cuda):
         and e["d2h_bytes_per_step"] > 0
     assert d["gpu_launches"] > 0
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(d["clocks"])
+    # the timed outputs were checked against the oracle's digests
+    assert d["self_check"]["bitexact_vs_oracle_digest"] is True
+    assert e["result_check"] is True
+
+
+def test_bench_two_ranks_config5_gloo(cuda):
+    """`--gpus 2` self-launches two ranks (here sharing the one GPU, gloo
+    for the host-side collectives); the N > 1 line is config 5 strong
+    scaling with the ghost exchange inside the step, printed once, with
+    n_gpus = 2 and the three exchange paths cross-checked bit for bit."""
+    import os
+    env = dict(os.environ, TASKFUSE_DIST_BACKEND="gloo")
+    env.pop("WORLD_SIZE", None)
+    out = subprocess.run(
+        [sys.executable, str(ROOT / "bench.py"), "--gpus", "2", "--steps",
+         "3", "--warmup", "3", "--cfg5-grid", "256"],
+        capture_output=True, text=True, timeout=900, cwd=str(ROOT), env=env)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [x for x in out.stdout.splitlines() if x.startswith("{")]
+    assert len(lines) == 1, out.stdout[-2000:]
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["scaling"] == "strong"
+    assert d["config"]["workload"].startswith("config 5")
+    assert d["run"]["halo_bytes_per_rank_per_step"] > 0
+    assert all(d["self_check"].values()) and len(d["self_check"]) == 2
+    assert d["value"] > 0 and d["e2e"]["value"] > 0

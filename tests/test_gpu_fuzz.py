@@ -42,6 +42,17 @@ def _bits(a):
     return np.ascontiguousarray(a).view(np.uint64)
 
 
+def _same(got, want):
+    """Raw 64-bit equality, except that a NaN matches any NaN: its payload
+    is the producing unit's default (x86 SSE: 0xfff8..., the GPU:
+    0x7fff...), not a property of the algorithm.  NaN positions must
+    match exactly."""
+    g, w = np.isnan(got), np.isnan(want)
+    if not np.array_equal(g, w):
+        return False
+    return np.array_equal(_bits(got)[~g], _bits(want)[~w])
+
+
 def _cases():
     rng = np.random.default_rng(20221012)
     kinds = ["uniform", "ties", "signed", "extreme", "constant"]
@@ -106,8 +117,6 @@ def test_random_kt_and_ppm(cuda, case):
     from oracle import ppm_oracle as PO
     from paper_2210_06438_b200 import ops
     k, n, g, kind, vel, _ = case
-    if kind == "extreme":
-        pytest.skip("overflowing fields: the 1e-12 KT check needs finite F")
     rng = np.random.default_rng(2000 + k)
     f = _field(rng, kind, g)
     hp = HO.make_pool(f, n)
@@ -124,23 +133,34 @@ def test_random_kt_and_ppm(cuda, case):
         torch.cuda.synchronize()
         return um.cpu().numpy(), up.cpu().numpy(), F.cpu().numpy()
 
+    # the raw-bit checks against the restatements run on EVERY field kind,
+    # "extreme" (overflowing products, infinities) included; only the 1e-12
+    # relative comparison with the upwind flux is restricted to the faces
+    # where both fluxes are finite
+    with np.errstate(all="ignore"):
+        oum, oup, oF = HO.recon_flux_batch(hp, n, vel)
+        okt = HO.flux_kt_batch(oum, oup, vel)
+        pum, pup = PO.reconstruct_ppm_batch(hp, n)
+        pflux = {0: HO.flux_batch(pum, pup, vel),
+                 1: HO.flux_kt_batch(pum, pup, vel)}
     # minmod + KT
-    oum, oup, oF = HO.recon_flux_batch(hp, n, vel)
     um, up, F = run("minmod", 1)
-    assert np.array_equal(_bits(F), _bits(HO.flux_kt_batch(oum, oup, vel)))
+    assert _same(F, okt), case
     # the wrap layer of F is garbage for a < 0 (flux_body, kernels.py:91)
     inner = (slice(None), slice(None), slice(0, c - 1), slice(0, c - 1),
              slice(0, c - 1))
-    scale = np.maximum(np.abs(oF[inner]), 1e-300)
-    assert (np.abs(F[inner] - oF[inner]) / scale <= 1e-12).all()
+    fin = np.isfinite(F[inner]) & np.isfinite(oF[inner])
+    assert fin.any()
+    scale = np.maximum(np.abs(oF[inner][fin]), 1e-300)
+    with np.errstate(all="ignore"):
+        assert (np.abs(F[inner][fin] - oF[inner][fin]) / scale
+                <= 1e-12).all(), case
     # PPM + upwind / KT
-    pum, pup = PO.reconstruct_ppm_batch(hp, n)
-    for form, flux in ((0, HO.flux_batch), (1, HO.flux_kt_batch)):
+    for form in (0, 1):
         um, up, F = run("ppm", form)
-        assert np.array_equal(_bits(um), _bits(pum)), (case, form)
-        assert np.array_equal(_bits(up), _bits(pup)), (case, form)
-        assert np.array_equal(_bits(F), _bits(flux(pum, pup, vel))), \
-            (case, form)
+        assert _same(um, pum), (case, form)
+        assert _same(up, pup), (case, form)
+        assert _same(F, pflux[form]), (case, form)
 
 
 @pytest.mark.parametrize("n,grid", [(8, 32), (8, 64), (16, 64), (8, 8)])
