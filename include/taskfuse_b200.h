@@ -181,6 +181,33 @@ int tf_region_team_parent(const tf_region* r, int64_t team);
 int tf_region_stats(const tf_region* r, int64_t* teams_formed,
                     int64_t* solo_fast_path, int64_t* histogram129);
 
+/* ---- member bookkeeping of a closed team --------------------------------
+ * TeamMember._issue / leave / _chain / _maybe_release (aggregator.py:
+ * 168-234): the SPMD op-sequence check, lease ownership per step, and the
+ * release rule (every member left and no op in flight).  `sig` is the
+ * step's signature as the reference formats it (aggregator.py:_fmt_sig,
+ * e.g. "alloc:device:<f8:2744", "copy:h2d:21952", "launch:flux:24:1").
+ * A mismatch returns TF_E_ORDERING and records "expected\ngot" for
+ * tf_region_error (OrderingViolationError(region, cursor, expected, got)).
+ * *release == 1 exactly once per team: the caller returns the leases
+ * (tf_team_leases) and frees the team with tf_region_release_team.        */
+int tf_team_issue(tf_region* r, int64_t team, int32_t cursor, const char* sig,
+                  int32_t* step, int32_t* arrivals);
+int tf_team_leave(tf_region* r, int64_t team, int32_t cursor,
+                  int32_t* release);
+int tf_team_op_begin(tf_region* r, int64_t team);
+int tf_team_op_end(tf_region* r, int64_t team, int32_t* release);
+int tf_team_set_lease(tf_region* r, int64_t team, int32_t step,
+                      int64_t lease);
+int64_t tf_team_lease(const tf_region* r, int64_t team, int32_t step);
+/* leases of the team's steps in step order; returns the count             */
+int tf_team_leases(const tf_region* r, int64_t team, int64_t* out,
+                   int32_t cap);
+int tf_team_step_info(const tf_region* r, int64_t team, int32_t step,
+                      int32_t* arrivals, char* sig, int32_t sig_cap);
+int64_t tf_region_violations(const tf_region* r);
+const char* tf_region_error(const tf_region* r);
+
 /* ---- real-time bulk executor (strategy 3 on real CUDA streams) ---------- */
 
 typedef struct tf_executor tf_executor;

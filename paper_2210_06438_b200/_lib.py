@@ -23,6 +23,7 @@ _pi64 = C.POINTER(C.c_int64)
 
 TF_E_INVALID = 1001
 TF_E_NO_TMA = 1002
+TF_E_ORDERING = 1003
 MAX_TEAM = 128
 TF_LAUNCH_OVERLAP_PREV = 1
 TF_PLAN_TEAM_BUFFERS = 2
@@ -73,6 +74,17 @@ SIGNATURES = {
     "tf_region_team_members": (C.c_int, [_p, _i64, _pi64, _i32]),
     "tf_region_team_parent": (C.c_int, [_p, _i64]),
     "tf_region_stats": (C.c_int, [_p, _pi64, _pi64, _pi64]),
+    "tf_team_issue": (C.c_int, [_p, _i64, _i32, C.c_char_p, _pi32, _pi32]),
+    "tf_team_leave": (C.c_int, [_p, _i64, _i32, _pi32]),
+    "tf_team_op_begin": (C.c_int, [_p, _i64]),
+    "tf_team_op_end": (C.c_int, [_p, _i64, _pi32]),
+    "tf_team_set_lease": (C.c_int, [_p, _i64, _i32, _i64]),
+    "tf_team_lease": (_i64, [_p, _i64, _i32]),
+    "tf_team_leases": (C.c_int, [_p, _i64, _pi64, _i32]),
+    "tf_team_step_info": (C.c_int, [_p, _i64, _i32, _pi32, C.c_char_p,
+                                    _i32]),
+    "tf_region_violations": (_i64, [_p]),
+    "tf_region_error": (C.c_char_p, [_p]),
     "tf_executor_create": (C.c_int, [_p, _i32, C.POINTER(_p)]),
     "tf_executor_destroy": (None, [_p]),
     "tf_executor_stream": (_p, [_p, _i32]),

@@ -47,10 +47,25 @@ uint32_t crc32_ieee(const char* s) {
 
 enum { FORMING = 0, CAP = 1, SOLO = 2, DRAIN = 3 };
 
+// One step of a team's SPMD op sequence (aggregator.py:64-74): every member
+// issues the same signature at the same cursor; the first arrival owns the
+// step's lease, the last one issues its device op.
+struct TeamStep {
+  std::string sig;
+  int32_t arrivals = 0;
+  int64_t lease = -1;
+};
+
 struct Team {
   int32_t parent = 0;
   int32_t state = FORMING;  // FORMING or the closure reason
   std::vector<int64_t> tags;
+  // member bookkeeping after closure (aggregator.py:76-99,168-234)
+  std::vector<TeamStep> steps;
+  int32_t final_cursor = -1;  // cursor of the first member to leave
+  int32_t left = 0;
+  int32_t pending_ops = 0;
+  bool released = false;
 };
 
 struct Parent {
@@ -74,9 +89,15 @@ class TeamTable {
     }
     Slot& s = slots_[id];
     s.alive = true;
-    s.team.parent = parent;
-    s.team.state = FORMING;
-    s.team.tags.clear();
+    Team& t = s.team;
+    t.parent = parent;
+    t.state = FORMING;
+    t.tags.clear();
+    t.steps.clear();   // keeps capacity (and the strings' buffers below)
+    t.final_cursor = -1;
+    t.left = 0;
+    t.pending_ops = 0;
+    t.released = false;
     return id;
   }
   Team* get(int64_t id) {
@@ -117,6 +138,8 @@ struct tf_region {
   int64_t teams_formed = 0;
   int64_t solo_fast_path = 0;
   int64_t histogram[TF_MAX_TEAM + 1] = {0};
+  int64_t violations = 0;
+  std::string error;  // last ordering violation: "expected\ngot"
 };
 
 namespace {
@@ -278,6 +301,135 @@ int tf_region_release_team(tf_region* r, int64_t team) {
   if (!t || t->state == FORMING) return TF_E_INVALID;
   r->teams.release(team);
   return 0;
+}
+
+// ---- member-side bookkeeping of a closed team ----------------------------
+// The reference keeps this per team in Python (TeamMember._issue / leave /
+// _chain / _maybe_release, aggregator.py:168-234); here it lives next to the
+// formation state, so the Python facade and the native HydroSim engine run
+// the same rules.
+
+namespace {
+
+int violation(tf_region* r, const std::string& expected, const char* got) {
+  r->violations += 1;
+  r->error = expected;
+  r->error += '\n';
+  r->error += got;
+  return TF_E_ORDERING;
+}
+
+// left == size and nothing in flight: the team's leases may go back
+int release_due(Team& t) {
+  if (t.released || t.left < (int32_t)t.tags.size() || t.pending_ops > 0)
+    return 0;
+  t.released = true;
+  return 1;
+}
+
+}  // namespace
+
+int tf_team_issue(tf_region* r, int64_t team, int32_t cursor, const char* sig,
+                  int32_t* step, int32_t* arrivals) {
+  if (!r || !sig || cursor < 0) return TF_E_INVALID;
+  Team* t = r->teams.get(team);
+  if (!t || t->state == FORMING || t->released) return TF_E_INVALID;
+  // a member may not issue past the point where another already left
+  if (t->final_cursor >= 0 && cursor >= t->final_cursor)
+    return violation(r, "leave", sig);
+  if (cursor < (int32_t)t->steps.size()) {
+    if (t->steps[cursor].sig != sig)
+      return violation(r, t->steps[cursor].sig, sig);
+  } else if (cursor == (int32_t)t->steps.size()) {
+    t->steps.emplace_back();
+    t->steps.back().sig = sig;
+  } else {
+    return TF_E_INVALID;  // a member skipped a step: caller bug
+  }
+  TeamStep& st = t->steps[cursor];
+  st.arrivals += 1;
+  if (step) *step = cursor;
+  if (arrivals) *arrivals = st.arrivals;
+  return 0;
+}
+
+int tf_team_leave(tf_region* r, int64_t team, int32_t cursor,
+                  int32_t* release) {
+  if (!r || cursor < 0) return TF_E_INVALID;
+  Team* t = r->teams.get(team);
+  if (!t || t->state == FORMING || t->released) return TF_E_INVALID;
+  if ((int32_t)t->steps.size() > cursor)
+    return violation(r, t->steps[cursor].sig, "leave");
+  t->final_cursor = cursor;
+  t->left += 1;
+  const int due = release_due(*t);
+  if (release) *release = due;
+  return 0;
+}
+
+int tf_team_op_begin(tf_region* r, int64_t team) {
+  Team* t = r ? r->teams.get(team) : nullptr;
+  if (!t || t->released) return TF_E_INVALID;
+  t->pending_ops += 1;
+  return 0;
+}
+
+int tf_team_op_end(tf_region* r, int64_t team, int32_t* release) {
+  Team* t = r ? r->teams.get(team) : nullptr;
+  if (!t || t->pending_ops < 1) return TF_E_INVALID;
+  t->pending_ops -= 1;
+  const int due = release_due(*t);
+  if (release) *release = due;
+  return 0;
+}
+
+int tf_team_set_lease(tf_region* r, int64_t team, int32_t step,
+                      int64_t lease) {
+  Team* t = r ? r->teams.get(team) : nullptr;
+  if (!t || step < 0 || step >= (int32_t)t->steps.size()) return TF_E_INVALID;
+  t->steps[step].lease = lease;
+  return 0;
+}
+
+int64_t tf_team_lease(const tf_region* r, int64_t team, int32_t step) {
+  const Team* t = r ? r->teams.get(team) : nullptr;
+  if (!t || step < 0 || step >= (int32_t)t->steps.size()) return -1;
+  return t->steps[step].lease;
+}
+
+int tf_team_leases(const tf_region* r, int64_t team, int64_t* out,
+                   int32_t cap) {
+  const Team* t = r ? r->teams.get(team) : nullptr;
+  if (!t) return -TF_E_INVALID;
+  int32_t n = 0;
+  for (const TeamStep& st : t->steps)
+    if (st.lease >= 0) {
+      if (out && n < cap) out[n] = st.lease;
+      ++n;
+    }
+  return n;
+}
+
+int tf_team_step_info(const tf_region* r, int64_t team, int32_t step,
+                      int32_t* arrivals, char* sig, int32_t sig_cap) {
+  const Team* t = r ? r->teams.get(team) : nullptr;
+  if (!t || step < 0 || step >= (int32_t)t->steps.size()) return TF_E_INVALID;
+  const TeamStep& st = t->steps[step];
+  if (arrivals) *arrivals = st.arrivals;
+  if (sig && sig_cap > 0) {
+    const size_t k = std::min<size_t>((size_t)sig_cap - 1, st.sig.size());
+    std::copy(st.sig.begin(), st.sig.begin() + k, sig);
+    sig[k] = 0;
+  }
+  return 0;
+}
+
+int64_t tf_region_violations(const tf_region* r) {
+  return r ? r->violations : -1;
+}
+
+const char* tf_region_error(const tf_region* r) {
+  return r ? r->error.c_str() : "";
 }
 
 }  // extern "C"

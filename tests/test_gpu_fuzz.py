@@ -149,12 +149,18 @@ def test_random_kt_and_ppm(cuda, case):
     # the wrap layer of F is garbage for a < 0 (flux_body, kernels.py:91)
     inner = (slice(None), slice(None), slice(0, c - 1), slice(0, c - 1),
              slice(0, c - 1))
-    fin = np.isfinite(F[inner]) & np.isfinite(oF[inner])
-    assert fin.any()
-    scale = np.maximum(np.abs(oF[inner][fin]), 1e-300)
-    with np.errstate(all="ignore"):
-        assert (np.abs(F[inner][fin] - oF[inner][fin]) / scale
-                <= 1e-12).all(), case
+    # the 1e-12 relative tolerance holds where the KT form's two halves do
+    # not cancel catastrophically: on "extreme" fields a 1e200 face next to
+    # a 1e-200 one makes 1/2(f_L+f_R) - 1/2|a|(u_R-u_L) lose every digit of
+    # the small flux (the forms agree only in exact arithmetic), so there
+    # only the raw-bit restatement check above applies
+    if kind != "extreme":
+        fin = np.isfinite(F[inner]) & np.isfinite(oF[inner])
+        assert fin.any()
+        scale = np.maximum(np.abs(oF[inner][fin]), 1e-300)
+        with np.errstate(all="ignore"):
+            assert (np.abs(F[inner][fin] - oF[inner][fin]) / scale
+                    <= 1e-12).all(), case
     # PPM + upwind / KT
     for form in (0, 1):
         um, up, F = run("ppm", form)
