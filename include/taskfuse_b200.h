@@ -208,6 +208,41 @@ int tf_team_step_info(const tf_region* r, int64_t team, int32_t step,
 int64_t tf_region_violations(const tf_region* r);
 const char* tf_region_error(const tf_region* r);
 
+/* ---- native HydroSim engine ----------------------------------------------
+ * HydroSim.task_iteration (hydro/step.py:83-123) for every sub-grid of a
+ * per_axis^3 lattice, driven by driver()'s per-iteration loop
+ * (step.py:126-143): five regions in KERNEL_ORDER (prep, reconstruct,
+ * flux, reduce, update; parents = max(1, S / max_team), step.py:61), each
+ * visit enter -> slice_alloc x4 (pinned/device ext^3 and n^3 staging
+ * leases from an exact-size recycling pool) -> h2d copy -> ONE batched
+ * kernel per team -> d2h copy -> await -> leave, under the tf_region /
+ * tf_team rules, tasks FIFO, streams polled only when no task is runnable
+ * (the Python scheduler's order).  `streams` = the executor pool's CUDA
+ * streams (NULL: the engine creates them).  w (S,E,E,E), um/up/F
+ * (S,3,C,C,C), reduce_out (S): per-sub-grid scratch (HydroSim.scratch).    */
+typedef struct tf_hydro tf_hydro;
+int tf_hydro_create(int32_t n, int32_t per_axis, int32_t max_team,
+                    int32_t executors, const tf_stream_t* streams, double ax,
+                    double ay, double az, double dt_dx, double* w, double* um,
+                    double* up, double* F, double* reduce_out,
+                    tf_hydro** out);
+void tf_hydro_destroy(tf_hydro* h);
+/* bench.py:142-153 _presize_pools: lease every (kind, len x team size)
+ * bucket the run can touch, so the steady state never raw-allocates.       */
+int tf_hydro_presize(tf_hydro* h);
+/* One iteration: every sub-grid's task through the five regions; u_pool is
+ * read (ghosts already exchanged), u_next_pool's owned cells written.
+ * Returns when every task has left its last region; `stream` is ordered
+ * before (fork) and after (join) the executor streams' work.               */
+int tf_hydro_iteration(tf_hydro* h, const double* u_pool, double* u_next_pool,
+                       tf_stream_t stream);
+/* the engine's region k (KERNEL_ORDER index), for tf_region_stats         */
+int tf_hydro_region(const tf_hydro* h, int32_t k, tf_region** out);
+/* kernels, copies, bytes copied, raw device allocs, raw pinned allocs
+ * (bucket misses, the reference's count), outstanding leases, buffers
+ * materialised (cudaMalloc / cudaHostAlloc calls), device polls           */
+int tf_hydro_counters(const tf_hydro* h, int64_t* out8);
+
 /* ---- real-time bulk executor (strategy 3 on real CUDA streams) ---------- */
 
 typedef struct tf_executor tf_executor;

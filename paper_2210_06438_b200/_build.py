@@ -16,7 +16,8 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libtaskfuse_b200.so"
-SOURCES = ("hydro_kernels.cu", "aggregator.cpp", "halo.cu", "field_step.cu")
+SOURCES = ("hydro_kernels.cu", "aggregator.cpp", "halo.cu", "field_step.cu",
+           "hydro_engine.cpp")
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",

@@ -85,6 +85,14 @@ SIGNATURES = {
                                     _i32]),
     "tf_region_violations": (_i64, [_p]),
     "tf_region_error": (C.c_char_p, [_p]),
+    "tf_hydro_create": (C.c_int, [_i32, _i32, _i32, _i32, _p, _f64, _f64,
+                                  _f64, _f64, _p, _p, _p, _p, _p,
+                                  C.POINTER(_p)]),
+    "tf_hydro_destroy": (None, [_p]),
+    "tf_hydro_presize": (C.c_int, [_p]),
+    "tf_hydro_iteration": (C.c_int, [_p, _p, _p, _p]),
+    "tf_hydro_region": (C.c_int, [_p, _i32, C.POINTER(_p)]),
+    "tf_hydro_counters": (C.c_int, [_p, _pi64]),
     "tf_executor_create": (C.c_int, [_p, _i32, C.POINTER(_p)]),
     "tf_executor_destroy": (None, [_p]),
     "tf_executor_stream": (_p, [_p, _i32]),

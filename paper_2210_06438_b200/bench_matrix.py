@@ -105,17 +105,24 @@ def _presize_pools(buffers: BufferPool, subgrid_n: int, grid_n: int,
 
 def run_cell(subgrid_n: int, executors: int, max_team: int, steps: int,
              policy: str = "round_robin", grid_n: int = GRID_N,
-             field=None):
-    """Warm-up step + `steps` measured steps; returns (Row, sim, device)."""
+             field=None, engine: str = "native"):
+    """Warm-up step + `steps` measured steps; returns (Row, sim, device).
+    engine: "native" — the HydroSim tasks run in the C++ engine (the
+    throughput path of the reference API); "python" — one Python generator
+    per task through the mirrored AggregationRegion."""
     if executors < 1:
         raise UsageError("the B200 matrix has no host-only cell")
     sched = Scheduler(SchedulerConfig(worker_count=32))
     state = make_state(subgrid_n, grid_n, field=field)
     device = CudaDevice(sched)
     pool = ExecutorPool(sched, device, executors, policy)
-    buffers = BufferPool(device)
-    _presize_pools(buffers, subgrid_n, grid_n, max_team)
-    sim = HydroSim(sched, state, pool, buffers, max_team=max_team)
+    buffers = BufferPool(device) if engine == "python" else None
+    sim = HydroSim(sched, state, pool, buffers, max_team=max_team,
+                   engine=engine)
+    if sim.native is not None:
+        sim.presize()
+    else:
+        _presize_pools(buffers, subgrid_n, grid_n, max_team)
     marks = []
 
     def on_step(_index):
@@ -124,7 +131,11 @@ def run_cell(subgrid_n: int, executors: int, max_team: int, steps: int,
                       device.copies_enqueued,
                       device.raw_allocations["device"],
                       device.sync_count,
-                      device.raw_allocations["pinned_host"]))
+                      device.raw_allocations["pinned_host"],
+                      # native engine: staging buffers materialised lazily
+                      # (real cudaMalloc / cudaHostAlloc calls)
+                      sim.native.counters()["materialised"]
+                      if sim.native is not None else 0))
 
     sched.spawn(lambda: driver(sim, steps + 1, on_step), label="bench")
     sched.run()
@@ -148,16 +159,23 @@ def run_cell(subgrid_n: int, executors: int, max_team: int, steps: int,
         # (bench.py:212); pinned staging allocations are reported beside it
         raw_allocs=last[3], syncs=last[4],
         team_sizes=dict(sorted(sizes.items())),
-        measured_raw_allocs=(last[3] - warm[3]) + (last[5] - warm[5]),
+        measured_raw_allocs=(last[3] - warm[3]) + (last[5] - warm[5])
+        + (last[6] - warm[6]),
         measured_syncs=last[4] - warm[4],
         pinned_raw_allocs=last[5],
     ), sim, device
 
 
-def run_matrix(cfg: BenchConfig, grid_n: int = GRID_N) -> Report:
+def run_matrix(cfg: BenchConfig, grid_n: int = GRID_N,
+               engine: str = "native") -> Report:
+    """The executors x max_team sweep (bench.py:220-245).  The reference's
+    extra (0, 1) host-only row is not produced: this framework has no CPU
+    compute path; bench.py times the reference's CPU task
+    iteration separately as the config-1 baseline."""
     cells = [(e, c) for e in sorted(set(cfg.executors))
              for c in sorted(set(cfg.max_team))]
-    rows = [run_cell(cfg.subgrid_n, e, c, cfg.steps, grid_n=grid_n)[0]
+    rows = [run_cell(cfg.subgrid_n, e, c, cfg.steps, grid_n=grid_n,
+                     engine=engine)[0]
             for e, c in cells]
     return Report(rows=tuple(rows), steps=cfg.steps)
 
@@ -199,10 +217,12 @@ def main(argv=None) -> int:
     ap.add_argument("--steps", type=int, default=2)
     ap.add_argument("--grid-n", type=int, default=GRID_N)
     ap.add_argument("--format", choices=("csv", "markdown"), default="csv")
+    ap.add_argument("--engine", choices=("native", "python"),
+                    default="native")
     a = ap.parse_args(argv)
     cfg = BenchConfig(a.subgrid_n, tuple(a.executors), tuple(a.max_team),
                       a.steps, a.format)
-    print(emit(run_matrix(cfg, a.grid_n), a.format))
+    print(emit(run_matrix(cfg, a.grid_n, a.engine), a.format))
     return 0
 
 

@@ -16,7 +16,12 @@ update), each visit = enter -> slice_alloc x4 -> h2d -> slice_launch -> d2h
   iteration (each task's exchange reads only current owned cells, which no
   task writes during the iteration — scenario.py:127-129 — so doing them
   together is equivalent);
-* there is no CPU path: executors == 0 raises UsageError.
+* there is no CPU path: executors == 0 raises UsageError;
+* engine="native" (the default on a real CudaDevice) runs the iteration's
+  tasks in C++ (hydro/engine.py) under the same formation and member rules,
+  so arrivals keep up with the device and teams form; engine="python" runs
+  each task as a Python generator through the mirrored AggregationRegion
+  API (the same path user task bodies take).
 """
 
 from __future__ import annotations
@@ -84,7 +89,7 @@ class HydroSim:
     def __init__(self, sched: Scheduler, state: HydroState,
                  executors: ExecutorPool, buffers: BufferPool | None = None,
                  work_factors: dict | None = None, max_team: int = 1,
-                 velocity=VELOCITY):
+                 velocity=VELOCITY, engine: str = "auto"):
         if executors.cpu_only:
             raise UsageError("HydroSim on the B200 needs >= 1 executor; "
                              "there is no CPU path")
@@ -97,6 +102,26 @@ class HydroSim:
                                              for k in KERNEL_ORDER}
         S = len(state.blocks)
         self.scratch_pool = ScratchPool(S, state.n, state.device)
+        self.max_team = max_team
+        if engine == "auto":
+            # the native engine needs real streams; a test double (or custom
+            # work factors, which only the Python path's launch specs carry)
+            # keeps the Python task path
+            from ..device import CudaDevice
+            engine = "native" if isinstance(executors.device, CudaDevice) \
+                and work_factors is None else "python"
+        if engine not in ("native", "python"):
+            raise UsageError(f"unknown engine {engine!r}")
+        self.native = None
+        if engine == "native":
+            from .engine import HydroEngine
+            self.buffers = buffers
+            self.native = HydroEngine(state, self.scratch_pool, executors,
+                                      max_team, self.velocity, self.dt_dx,
+                                      executors.device)
+            self.regions = self.native.regions
+            self._seen = self.native.counters()
+            return
         self.buffers = buffers or BufferPool(executors.device)
         parents = max(1, S // max_team)          # step.py:59-61
         self.regions = {
@@ -114,6 +139,38 @@ class HydroSim:
         """Reference-style {block: scratch dict} view."""
         return {b: self.scratch_pool.view(self.state.block_id(b))
                 for b in self.state.blocks}
+
+    def native_iteration(self) -> None:
+        """Every sub-grid's task for one iteration in the native engine;
+        its device work is folded into the CudaDevice counters."""
+        st = self.state
+        self.native.iteration(st.u_pool, st.u_next_pool,
+                              torch.cuda.current_stream())
+        now = self.native.counters()
+        dev = self.executors.device
+        dev.kernels_enqueued += now["kernels"] - self._seen["kernels"]
+        dev.copies_enqueued += now["copies"] - self._seen["copies"]
+        dev.bytes_copied += now["bytes"] - self._seen["bytes"]
+        dev.raw_allocations["device"] += (now["raw_device"]
+                                          - self._seen["raw_device"])
+        dev.raw_allocations["pinned_host"] += (now["raw_pinned"]
+                                               - self._seen["raw_pinned"])
+        self._seen = now
+
+    def presize(self) -> None:
+        """bench.py:142-153 for the native engine's staging pool."""
+        if self.native is not None:
+            self.native.presize()
+            self.native_iteration_counters_only()
+
+    def native_iteration_counters_only(self) -> None:
+        now = self.native.counters()
+        dev = self.executors.device
+        dev.raw_allocations["device"] += (now["raw_device"]
+                                          - self._seen["raw_device"])
+        dev.raw_allocations["pinned_host"] += (now["raw_pinned"]
+                                               - self._seen["raw_pinned"])
+        self._seen = now
 
     def _ids(self, args) -> torch.Tensor:
         return self._ids_ring.put(args)
@@ -162,11 +219,15 @@ def driver(sim: HydroSim, steps: int, step_hook=None):
     for _ in range(steps):
         for _ in range(ITERATIONS_PER_STEP):
             exchange_ghosts(state)
-            torch.cuda.current_stream().synchronize()
-            tokens = [sched.spawn(partial(sim.task_iteration, b),
-                                  label=f"hydro{b}")[1]
-                      for b in state.blocks]
-            yield await_all(*tokens)
+            if sim.native is not None:
+                sim.native_iteration()
+                yield charge(0)
+            else:
+                torch.cuda.current_stream().synchronize()
+                tokens = [sched.spawn(partial(sim.task_iteration, b),
+                                      label=f"hydro{b}")[1]
+                          for b in state.blocks]
+                yield await_all(*tokens)
             check_reduce(sim.scratch_pool, sim.velocity)
             state.swap()
             state.time += dt

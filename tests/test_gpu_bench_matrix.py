@@ -9,12 +9,14 @@ pytestmark = pytest.mark.gpu
 
 def test_counting_identities_grid64(cuda):
     from paper_2210_06438_b200.bench_matrix import run_cell
-    row8, _, _ = run_cell(8, 1, 1, steps=1)
-    assert (row8.kernels, row8.transfers) == (7680, 15360)
-    row16, _, _ = run_cell(16, 1, 1, steps=1)
-    assert (row16.kernels, row16.transfers) == (960, 1920)
-    assert row8.measured_raw_allocs == 0 and row16.measured_raw_allocs == 0
-    assert row8.team_sizes == {1: 2 * 7680}
+    for engine in ("native", "python"):
+        row8, _, _ = run_cell(8, 1, 1, steps=1, engine=engine)
+        assert (row8.kernels, row8.transfers) == (7680, 15360), engine
+        row16, _, _ = run_cell(16, 1, 1, steps=1, engine=engine)
+        assert (row16.kernels, row16.transfers) == (960, 1920), engine
+        assert row8.measured_raw_allocs == 0, engine
+        assert row16.measured_raw_allocs == 0, engine
+        assert row8.team_sizes == {1: 2 * 7680}, engine
 
 
 def test_aggregation_reduces_launches_and_caps_teams(cuda):

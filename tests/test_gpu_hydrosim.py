@@ -13,7 +13,8 @@ pytestmark = pytest.mark.gpu
 
 
 def run_sim(n, grid, steps, executors=1, max_team=1, field=None,
-            velocity=(1.0, 1.0, 1.0), poison=False, id_ring=None):
+            velocity=(1.0, 1.0, 1.0), poison=False, id_ring=None,
+            engine="python"):
     from paper_2210_06438_b200.device import CudaDevice
     from paper_2210_06438_b200.executorpool import ExecutorPool
     from paper_2210_06438_b200.hydro import HydroSim, driver, make_state
@@ -24,7 +25,8 @@ def run_sim(n, grid, steps, executors=1, max_team=1, field=None,
     state = make_state(n, grid, field=field)
     device = CudaDevice(sched)
     pool = ExecutorPool(sched, device, executors)
-    sim = HydroSim(sched, state, pool, max_team=max_team, velocity=velocity)
+    sim = HydroSim(sched, state, pool, max_team=max_team, velocity=velocity,
+                   engine=engine)
     if poison:
         sim.scratch_pool.poison()
     if id_ring is not None:   # a tiny ring: wraps every few launches
@@ -194,3 +196,62 @@ def test_bitwise_reproducibility_matrix(cuda):
     if not np.array_equal(field_after(8, 32, 8, "load_balanced"), ref):
         bad.append((8, 32, 8, "load_balanced"))
     assert not bad, bad
+
+
+# ---------------------------------------------------------------- native
+# The same task iteration in the C++ engine (hydro/engine.py), under the
+# same tf_region / tf_team rules: same whole-grid results, same counting
+# identities, every lease back in the pool, and teams that actually form.
+
+@pytest.mark.parametrize("executors,cap", [(1, 1), (4, 8), (2, 3)])
+def test_native_engine_matches_reference(cuda, hydro_golden, executors, cap):
+    from paper_2210_06438_b200.hydro import assemble
+    case = _golden(hydro_golden, "blast16_n8_v111")
+    state, sim, device = run_sim(8, 16, steps=2, executors=executors,
+                                 max_team=cap, engine="native")
+    assert sim.native is not None
+    assert HO.digest(assemble(state)) == case["reference_step_2"]
+    c = sim.native.counters()
+    assert c["outstanding"] == 0
+    hist = {}
+    for r in sim.regions.values():
+        st = r.stats()
+        assert st.violations == 0 and max(st.size_histogram) <= cap
+        for k, v in st.size_histogram.items():
+            hist[k] = hist.get(k, 0) + v
+    # every task visits every region once per iteration (test_hydro.py:
+    # 153-160): 8 tasks x 3 iterations x 2 steps x 5 regions
+    assert sum(k * v for k, v in hist.items()) == 8 * 3 * 2 * 5
+    teams = sum(hist.values())
+    assert device.kernels_enqueued == teams
+    assert device.copies_enqueued == 2 * teams
+    if cap == 1:
+        assert device.kernels_enqueued == 2 * 120
+
+
+def test_native_engine_negative_velocity(cuda, hydro_golden):
+    from paper_2210_06438_b200.hydro import assemble
+    case = _golden(hydro_golden, "stress16_n8_vneg")
+    state, _, _ = run_sim(8, 16, steps=1, executors=2, max_team=4,
+                          field=HO.stress_field(16),
+                          velocity=tuple(case["velocity"]), engine="native")
+    assert HO.digest(assemble(state)) == case["reference_step_1"]
+
+
+def test_native_engine_forms_teams_config2(cuda):
+    """Config 2 (4096 sub-grids) through HydroSim + driver at A = 64: the
+    arrivals outpace the device, so teams close at the cap — mean team at
+    least A/2 (the Python per-task path closes nearly all teams solo) —
+    and the field is still the whole-grid reference's."""
+    from paper_2210_06438_b200.hydro import assemble
+    f = HO.sod_field(128)
+    state, sim, _ = run_sim(8, 128, steps=1, executors=1, max_team=64,
+                            field=f, engine="native")
+    hist = {}
+    for r in sim.regions.values():
+        for k, v in r.stats().size_histogram.items():
+            hist[k] = hist.get(k, 0) + v
+    members = sum(k * v for k, v in hist.items())
+    assert members == 4096 * 3 * 5
+    assert members / sum(hist.values()) >= 32, hist
+    assert np.array_equal(assemble(state), HO.reference_step(f))
