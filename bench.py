@@ -671,21 +671,131 @@ def e2e_faces_leg(wl, step_fn, steps, warmup, world, stream):
     return ms, host_in.numel() * 8, sum(o.numel() * 8 for o in outs)
 
 
+# ------------------------------------------------- real-time aggregation
+def realtime_leg(wl, args, world, stream, peak):
+    """Strategy 3 formed ON THE FLY inside the timed region: every step
+    submits the 4096 arrivals to the formation core (real-time starvation
+    signal: published slices not yet completed), each closed team is
+    published to the resident consumer grid (strategy3.QueueExecutor)
+    instead of launched.  Same outputs as `value` (checked against the
+    oracle digests), per-sub-grid slots."""
+    from paper_2210_06438_b200.strategy3 import (QueueExecutor,
+                                                 default_parents)
+    arrivals = np.arange(wl.S, dtype=np.int32)
+    A = args.max_team
+    q = QueueExecutor("reconstruct", A, default_parents(wl.S, A), wl.n)
+
+    def step(k):
+        q.run(wl.pools[k % len(wl.pools)], VELOCITY, arrivals, wl.um, wl.up,
+              wl.F, amax=wl.amax)
+    with ClockSampler(0) as clk:
+        ms = timed(step, args.steps, args.warmup, world, stream)
+    q.wait()
+    st = q.stats()
+    check = cfg2_output_check(wl, rerun=lambda: (step(0), q.wait()))
+    if not check["bitexact_vs_oracle_digest"]:
+        raise SystemExit(f"bench.py: real-time queue outputs differ {check}")
+    achieved = wl.S * b_alg(wl.n) / (ms * 1e-3) / 1e9
+    return {"value": rate(wl.S * world, wl.n, ms), "unit": UNIT,
+            "ms_per_step": ms, "max_team": A,
+            "mean_team": sum(k * v for k, v in st["size_histogram"].items())
+            / max(1, st["teams_formed"]),
+            "teams_per_step": st["teams_formed"] / max(1, q.runs),
+            "solo_fast_path": st["solo_fast_path"],
+            "roofline": {"achieved": achieved, "peak": peak,
+                         "frac": achieved / peak, "unit": "GB/s"},
+            "gpu_launches_per_step": 1, "self_check": check,
+            "clocks": clk.summary(),
+            "step": "4096 task arrivals -> C++ formation core (cap / solo "
+                    "fast path / drain on 'all published slices "
+                    "completed') -> closed teams published to a ring -> "
+                    "resident consumer grid (one launch per step)"}
+
+
+# ------------------------------------------------ the reference API path
+def reference_api_legs(args):
+    """The reference's own entry points — HydroSim + driver (step.py:
+    38-143) through the mirrored API, the native engine running the
+    per-sub-grid tasks: five region visits each (alloc x4, h2d, one
+    batched kernel per team, d2h, await, leave), real staging copies, teams
+    formed in real time.  ms per reference step (3 iterations).
+
+    config 1: 64 Sod sub-grids, executors 1, max_team 1 (the BASELINE
+    config, "runs on the CPU reference as-is"), beside the reference's CPU
+    task iteration (exchange_ghosts + the five bodies, step.py:93-97) for
+    the same 64 sub-grids on ONE host core (the reference is a single
+    Python process).  config 2: 4096 Sod sub-grids, aggregation sweep."""
+    from paper_2210_06438_b200.bench_matrix import run_cell
+    from paper_2210_06438_b200.hydro import sod_field
+    out = {}
+    row, sim, _ = run_cell(8, 1, 1, steps=3, grid_n=32,
+                           field=sod_field(32, "cuda"))
+    out["config1"] = {"ms_per_step": row.ms_per_step,
+                      "cell_updates_per_s": 64 * 512 * 3
+                      / (row.ms_per_step * 1e-3),
+                      "kernels_per_step": row.kernels,
+                      "transfers_per_step": row.transfers,
+                      "measured_raw_allocs": row.measured_raw_allocs}
+    del sim
+    if not args.no_cpu_baseline:
+        from oracle.cpu_baseline import CpuBaseline, cpu_model
+        cb = CpuBaseline("sod", 32, N_SUB, VELOCITY, range(64), workers=1,
+                         bodies="iteration")
+        try:
+            best = min(cb.step() for _ in range(5))
+        finally:
+            cb.close()
+        ms_cpu = 3 * best * 1e3
+        out["config1"]["cpu_reference"] = {
+            "ms_per_step": ms_cpu, "cores": 1, "kind": "port",
+            "sample": "all 64 sub-grids x 3 iterations: exchange_ghosts + "
+                      "prep/reconstruct/flux/reduce/update bodies (oracle "
+                      f"port), best of 5; CPU {cpu_model()}"}
+        out["config1"]["speedup_vs_cpu"] = ms_cpu / row.ms_per_step
+    sweep = {}
+    for A in (1, 4, 16, 64, 128):
+        row, sim, _ = run_cell(8, 1, A, steps=1, grid_n=GRID,
+                               field=sod_field(GRID, "cuda"))
+        members = sum(k * v for k, v in row.team_sizes.items())
+        teams = sum(row.team_sizes.values())
+        sweep[A] = {"ms_per_step": row.ms_per_step,
+                    "cell_updates_per_s": 4096 * 512 * 3
+                    / (row.ms_per_step * 1e-3),
+                    "kernels_per_step": row.kernels,
+                    "mean_team": members / teams,
+                    "measured_raw_allocs": row.measured_raw_allocs}
+        del sim
+    out["config2_sweep"] = sweep
+    out["config2_A64_vs_A1"] = sweep[1]["ms_per_step"] / \
+        sweep[64]["ms_per_step"]
+    out["note"] = ("HydroSim + driver through the mirrored reference API "
+                   "(bench_matrix.run_cell, engine native); each step = 3 "
+                   "iterations x S tasks x 5 region visits with real "
+                   "staging copies (ext^3 up, n^3 down per slice)")
+    return out
+
+
 # -------------------------------------------------------------- self-checks
-def cfg2_output_check(wl, plans, team_buffers=True):
-    """The timed team plan's outputs against the oracle's digests for this
-    exact workload (tests/golden/bench_cfg2.json; the Sod data are exactly
+def cfg2_output_check(wl, plans=None, team_buffers=True, rerun=None):
+    """The timed path's outputs against the oracle's digests for this exact
+    workload (tests/golden/bench_cfg2.json; the Sod data are exactly
     representable, so the digests are machine-independent).  Packed team
-    leases are put back in sub-grid order first."""
+    leases are put back in sub-grid order first.  `rerun()` (or the first
+    plan) recomputes pool 0's outputs after a NaN fill."""
     import hashlib
     import torch
     path = os.path.join(ROOT, "tests", "golden", "bench_cfg2.json")
     with open(path) as fh:
         want = json.load(fh)
     torch.cuda.synchronize()
-    plans[0].launch()
+    for t in (wl.um, wl.up, wl.F, wl.amax):
+        t.fill_(float("nan"))
+    if rerun is not None:
+        rerun()
+    else:
+        plans[0].launch()
     torch.cuda.synchronize()
-    if team_buffers:
+    if plans is not None and team_buffers:
         inv = torch.empty(wl.S, dtype=torch.int64, device="cuda")
         order = torch.from_numpy(plans[0].order.astype(np.int64)).cuda()
         inv[order] = torch.arange(wl.S, device="cuda")
@@ -1011,6 +1121,7 @@ def main():
                 "frac": bytes_step / (ms_single * 1e-3) / 1e9 / peak}},
         "clocks": clk.summary(),
     }
+    line["realtime"] = realtime_leg(wl, args, world, stream, peak)
     line["e2e"] = e2e_leg(args, max(10, args.steps // 2), 3, world, stream)
     # the host link bounds e2e: bytes both ways per step against the
     # measured concurrent copy-engine rate (48.9 GB/s per direction on this
@@ -1033,6 +1144,7 @@ def main():
                                              world, stream, peak)
     if not args.no_sweep:
         line["sweep"] = run_sweep(wl, args, world, stream, peak)
+        line["reference_api"] = reference_api_legs(args)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline_leg(wl.S, wl.n, GRID)
     if rank == 0:

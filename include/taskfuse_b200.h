@@ -38,7 +38,8 @@ enum {
   TF_E_INVALID = 1001,     /* bad argument (n, T, pointer, id range) */
   TF_E_NO_TMA = 1002,      /* cuTensorMapEncodeTiled unavailable */
   TF_E_ORDERING = 1003,    /* aggregation: replay diverged / misuse */
-  TF_E_CAPACITY = 1004     /* aggregation: out of slots */
+  TF_E_CAPACITY = 1004,    /* aggregation: out of slots */
+  TF_E_TIMEOUT = 1005      /* a device queue / barrier gave up waiting */
 };
 
 #define TF_MAX_TEAM 128 /* aggregator.py:42 MAX_TEAM */
@@ -125,6 +126,11 @@ int tf_field_to_pool_f64(const double* field, int32_t grid_n, int32_t n,
                          double* pool_ext, tf_stream_t stream);
 int tf_pool_to_field_f64(const double* pool_ext, int32_t grid_n, int32_t n,
                          double* field, tf_stream_t stream);
+/* make_state for the sub-grid layers [layer0, layer0+layers) along x only
+ * (one chunk of a pipelined host upload).                                  */
+int tf_field_to_pool_layers_f64(const double* field, int32_t grid_n,
+                                int32_t n, int32_t layer0, int32_t layers,
+                                double* pool_ext, tf_stream_t stream);
 
 /* prep_body (kernels.py:69-70): w[slot] = pool_ext[ids[s]].                */
 int tf_prep_f64(const double* pool_ext, const int32_t* ids, int32_t T,
@@ -293,9 +299,13 @@ int tf_qexec_run_recon_flux(tf_qexec* q, const double* pool_ext,
                             int64_t* teams_published);
 /* slices the consumer has completed so far (host view)                     */
 int64_t tf_qexec_completed(const tf_qexec* q);
+/* Wait for every run in flight; TF_E_TIMEOUT if a consumer grid gave up
+ * (its timeout expired with slices unprocessed).  A run reusing a queue
+ * slot reports a timeout of that slot's previous run the same way.        */
+int tf_qexec_wait(tf_qexec* q);
 int tf_queue_consumer_ctas(int32_t n);
 /* ring_h/ctl_h: mapped pinned host ring + control block {published,
- * final_count, completed}; ring_d: device mirror of tagged entries
+ * final_count, completed, status}; ring_d: device mirror of tagged entries
  * (epoch << 32 | id), ring_cap of them (the most this launch may publish),
  * zeroed once at allocation; epoch >= 1, new for every launch on that ring;
  * qdev: {published, final_count, claim, done}, one 128-B line each (zeroed,

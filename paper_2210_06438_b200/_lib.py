@@ -24,6 +24,7 @@ _pi64 = C.POINTER(C.c_int64)
 TF_E_INVALID = 1001
 TF_E_NO_TMA = 1002
 TF_E_ORDERING = 1003
+TF_E_TIMEOUT = 1005
 MAX_TEAM = 128
 TF_LAUNCH_OVERLAP_PREV = 1
 TF_PLAN_TEAM_BUFFERS = 2
@@ -60,6 +61,8 @@ SIGNATURES = {
     "tf_prep_f64": (C.c_int, [_p, _p, _i32, _i32, _p, _i32, _p]),
     "tf_field_to_pool_f64": (C.c_int, [_p, _i32, _i32, _p, _p]),
     "tf_pool_to_field_f64": (C.c_int, [_p, _i32, _i32, _p, _p]),
+    "tf_field_to_pool_layers_f64": (C.c_int, [_p, _i32, _i32, _i32, _i32, _p,
+                                              _p]),
     "tf_reduce_f64": (C.c_int, [_p, _i32, _f64, _f64, _f64, _p, _i32, _p]),
     "tf_region_create": (C.c_int, [C.c_char_p, _i32, _i32, _i32,
                                    C.POINTER(_p)]),
@@ -141,6 +144,7 @@ SIGNATURES = {
                                           _f64, _f64, _p, _p, _p, _p, _i32,
                                           _p, _pi64]),
     "tf_qexec_completed": (_i64, [_p]),
+    "tf_qexec_wait": (C.c_int, [_p]),
     "tf_queue_consumer_ctas": (C.c_int, [_i32]),
     "tf_queue_consumer_launch": (C.c_int, [_p, _i64, _i32, _p, _p, _p, _i64,
                                            _p, _p, _i32, _i32, _f64, _f64,
@@ -183,6 +187,8 @@ def check(rc: int, what: str) -> None:
             msg = "invalid argument"
         elif rc == TF_E_NO_TMA:
             msg = "cuTensorMapEncodeTiled unavailable"
+        elif rc == TF_E_TIMEOUT:
+            msg = "device queue timed out with work unprocessed"
         else:
             msg = f"CUDA error {rc}"
         raise TaskfuseCudaError(f"{what} failed: {msg} (rc={rc})")

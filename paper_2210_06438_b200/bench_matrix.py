@@ -97,10 +97,7 @@ def _presize_pools(buffers: BufferPool, subgrid_n: int, grid_n: int,
         for kind in ("device", "pinned_host"):
             for length in (ext3, n3):
                 buffers.ensure(kind, "f8", length * size, count)
-    for bucket in buffers._buckets.values():       # materialise storage
-        for b in bucket:
-            if b.storage is None:
-                b.storage = buffers._materialise(b)
+    buffers.materialise_all()
 
 
 def run_cell(subgrid_n: int, executors: int, max_team: int, steps: int,

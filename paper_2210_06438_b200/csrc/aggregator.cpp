@@ -660,6 +660,7 @@ struct QueueCtlHost {   // mirrors QueueCtl (hydro_kernels.cu)
   long long published;
   long long final_count;
   long long completed;
+  long long status;       // 1: the consumer grid timed out
 };
 struct QueueDevInit {   // mirrors QueueDev (one 128-B line per word)
   alignas(128) long long published;
@@ -680,6 +681,7 @@ struct QueueSlot {
   int64_t ring_cap = 0;
   void* qdev = nullptr;            // QueueDevInit on the device
   cudaEvent_t done_ev = nullptr;
+  cudaStream_t stream = nullptr;   // where this slot's last run went
   bool in_flight = false;
 };
 
@@ -793,6 +795,11 @@ int tf_qexec_run_recon_flux(tf_qexec* q, const double* pool_ext,
     cudaError_t e = cudaEventSynchronize(S.done_ev);
     if (e != cudaSuccess) return e;
     S.in_flight = false;
+    // a consumer grid that gave up left slices unprocessed: report it
+    if (__atomic_load_n(&S.ctl_h->status, __ATOMIC_ACQUIRE)) {
+      S.ctl_h->status = 0;
+      return TF_E_TIMEOUT;
+    }
   }
   if (count > S.ring_cap || !S.ring_h) {
     if (S.ring_h) cudaFreeHost(S.ring_h);
@@ -818,8 +825,18 @@ int tf_qexec_run_recon_flux(tf_qexec* q, const double* pool_ext,
   S.ctl_h->published = 0;
   S.ctl_h->final_count = -1;
   S.ctl_h->completed = 0;
+  S.ctl_h->status = 0;
   __atomic_thread_fence(__ATOMIC_SEQ_CST);
   cudaStream_t st = (cudaStream_t)stream;
+  // this slot's device counters are reset by the OTHER slot's previous run
+  // on its way out: when that run went to a different stream, order this
+  // launch after it
+  QueueSlot& other = q->slots[q->cur ^ 1];
+  if (other.in_flight && other.stream != st) {
+    cudaError_t e = cudaStreamWaitEvent(st, other.done_ev, 0);
+    if (e != cudaSuccess) return e;
+  }
+  S.stream = st;
   // the slot's device counters were reset by the previous run's kernel on
   // its way out (qdev_next), or at creation
   int rc = tf_queue_consumer_launch(
@@ -859,6 +876,22 @@ int tf_qexec_run_recon_flux(tf_qexec* q, const double* pool_ext,
 }
 
 int64_t tf_qexec_completed(const tf_qexec* q) { return q ? q_done(q) : -1; }
+
+int tf_qexec_wait(tf_qexec* q) {
+  if (!q) return TF_E_INVALID;
+  int rc = 0;
+  for (QueueSlot& S : q->slots) {
+    if (!S.in_flight) continue;
+    cudaError_t e = cudaEventSynchronize(S.done_ev);
+    if (e != cudaSuccess) return e;
+    S.in_flight = false;
+    if (__atomic_load_n(&S.ctl_h->status, __ATOMIC_ACQUIRE)) {
+      S.ctl_h->status = 0;
+      rc = TF_E_TIMEOUT;
+    }
+  }
+  return rc;
+}
 
 }  // extern "C"
 

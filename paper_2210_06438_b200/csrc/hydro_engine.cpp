@@ -62,27 +62,52 @@ int blocks_for(int k, int n) {
 // counted) whose storage is materialised lazily — here on first lease
 // (cudaMalloc / cudaHostAlloc, counted separately) — so presizing every
 // team-size bucket (bench.py:142-153) costs no memory until a size occurs.
+//
+// Storage comes from one pre-allocated arena per kind (pinned host, device),
+// carved by a bump pointer: materialising a buffer in the middle of a run
+// costs no allocator call (a cudaHostAlloc per new team size took up to a
+// millisecond — long enough to drain every stream and turn the real-time
+// formation into solo launches).  Only an exhausted arena falls back to a
+// real allocation per buffer.
 class StagingPool {
  public:
   ~StagingPool() {
     for (Buf* b : all_) {
-      if (b->ptr) {
+      if (b->ptr && b->own) {
         if (b->kind == KIND_DEVICE) cudaFree(b->ptr);
         else cudaFreeHost(b->ptr);
       }
       delete b;
     }
+    if (arena_[KIND_DEVICE]) cudaFree(arena_[KIND_DEVICE]);
+    if (arena_[KIND_PINNED]) cudaFreeHost(arena_[KIND_PINNED]);
+  }
+  int reserve(int64_t bytes_per_kind) {
+    cudaError_t e = cudaMalloc(&arena_[KIND_DEVICE], (size_t)bytes_per_kind);
+    if (e == cudaSuccess)
+      e = cudaHostAlloc(&arena_[KIND_PINNED], (size_t)bytes_per_kind, 0);
+    if (e != cudaSuccess) return e;
+    cap_ = bytes_per_kind;
+    return 0;
   }
   int acquire(int kind, int64_t bytes, void** out) {
     Buf* b = take(kind, bytes);
     if (!b->ptr) {
-      cudaError_t e = kind == KIND_DEVICE
-                          ? cudaMalloc(&b->ptr, (size_t)bytes)
-                          : cudaHostAlloc(&b->ptr, (size_t)bytes, 0);
-      if (e != cudaSuccess) {
-        b->ptr = nullptr;
-        give(b);
-        return e;
+      const int64_t need = (bytes + 255) & ~int64_t(255);
+      if (arena_[kind] && used_[kind] + need <= cap_) {
+        b->ptr = static_cast<char*>(arena_[kind]) + used_[kind];
+        used_[kind] += need;
+      } else {
+        cudaError_t e = kind == KIND_DEVICE
+                            ? cudaMalloc(&b->ptr, (size_t)bytes)
+                            : cudaHostAlloc(&b->ptr, (size_t)bytes, 0);
+        if (e != cudaSuccess) {
+          b->ptr = nullptr;
+          give(b);
+          return e;
+        }
+        b->own = true;
+        spilled_[kind] += 1;
       }
       materialised_[kind] += 1;
     }
@@ -90,6 +115,7 @@ class StagingPool {
     *out = b->ptr;
     return 0;
   }
+  int64_t spilled() const { return spilled_[0] + spilled_[1]; }
   int release(void* p) {
     auto it = leased_.find(p);
     if (it == leased_.end()) return TF_E_INVALID;
@@ -113,6 +139,7 @@ class StagingPool {
     int kind;
     int64_t bytes;
     void* ptr = nullptr;
+    bool own = false;  // a real allocation (arena exhausted)
   };
   Buf* take(int kind, int64_t bytes) {
     acquisitions_ += 1;
@@ -131,8 +158,11 @@ class StagingPool {
   std::map<std::pair<int, int64_t>, std::vector<Buf*>> buckets_;
   std::map<void*, Buf*> leased_;
   std::vector<Buf*> all_;
-  int64_t raw_[2] = {0, 0}, materialised_[2] = {0, 0};
+  int64_t raw_[2] = {0, 0}, materialised_[2] = {0, 0}, spilled_[2] = {0, 0};
   int64_t acquisitions_ = 0;
+  void* arena_[2] = {nullptr, nullptr};
+  int64_t used_[2] = {0, 0};
+  int64_t cap_ = 0;
 };
 
 // Engine-side objects of one live core team (the rules are in tf_team_*).
@@ -473,6 +503,14 @@ int tf_hydro_create(int32_t n, int32_t per_axis, int32_t max_team,
     h->sig[k][6] = "copy:d2h:" + std::to_string(n3 * 8);
   }
   h->tasks.resize(h->S);
+  // staging arenas: every task of an iteration holding its region's ext^3
+  // and n^3 leases at once, twice over (buckets are exact sizes, so several
+  // team sizes coexist), capped at 1 GiB per kind
+  if (!rc) {
+    int64_t arena = 2LL * h->S * (ext3 + n3) * 8;
+    if (arena > (1LL << 30)) arena = 1LL << 30;
+    rc = h->pool.reserve(arena);
+  }
   if (rc) {
     tf_hydro_destroy(h);
     return rc;

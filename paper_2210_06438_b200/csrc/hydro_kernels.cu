@@ -487,6 +487,84 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// The ghost shell of one sub-grid as a table built at compile time: for
+// every ghost cell, in increasing extended-offset order, its offset (low 16
+// bits) and its direction code t = 9 (di+1) + 3 (dj+1) + (dk+1) (high bits).
+// A CTA then walks only the shell (2232 of the 2744 cells at n = 8) with one
+// coalesced 4-byte table load per cell instead of the div/mod index math.
+template <int N>
+struct GhostShell {
+  static constexpr int E = N + 6;
+  static constexpr int COUNT = E * E * E - N * N * N;
+  uint32_t v[COUNT];
+  constexpr GhostShell() : v() {
+    int q = 0;
+    for (int i = 0; i < E; ++i)
+      for (int j = 0; j < E; ++j)
+        for (int k = 0; k < E; ++k) {
+          const int ti = (i >= 3) + (i >= N + 3), tj = (j >= 3) + (j >= N + 3),
+                    tk = (k >= 3) + (k >= N + 3);
+          const int t = (ti * 3 + tj) * 3 + tk;
+          if (t == 13) continue;  // owned
+          v[q++] = (uint32_t)((i * E + j) * E + k) | ((uint32_t)t << 16);
+        }
+  }
+};
+__device__ const GhostShell<8> g_shell8{};
+__device__ const GhostShell<16> g_shell16{};
+
+template <int N>
+__device__ __forceinline__ const uint32_t* ghost_shell() {
+  if constexpr (N == 8) return g_shell8.v;
+  else return g_shell16.v;
+}
+
+template <int N>
+__global__ void __launch_bounds__(256)
+    k_ghost_fill_shell(double* __restrict__ pool,
+                       const int32_t* __restrict__ ids, int per_axis) {
+  using G = Geo<N>;
+  constexpr int E = G::E;
+  constexpr int COUNT = GhostShell<N>::COUNT;
+  const int s = blockIdx.x;
+  const int g = ids ? ids[s] : s;
+  // the 27 periodic neighbours' base offsets minus the direction shift:
+  // ghost cell c of direction d is the neighbour's ext cell c - d*N
+  __shared__ int64_t nbase[27];
+  if (threadIdx.x < 27) {
+    const int m = per_axis;
+    const int bx = g / (m * m), by = (g / m) % m, bz = g % m;
+    const int t = threadIdx.x;
+    const int di = t / 9 - 1, dj = (t / 3) % 3 - 1, dk = t % 3 - 1;
+    const int nx = (bx + di + m) % m, ny = (by + dj + m) % m,
+              nz = (bz + dk + m) % m;
+    nbase[t] = ((int64_t)(nx * m + ny) * m + nz) * G::EXT3 -
+               (int64_t)((di * E + dj) * E + dk) * N;
+  }
+  __syncthreads();
+  const uint32_t* __restrict__ shell = ghost_shell<N>();
+  double* __restrict__ dst = pool + (int64_t)g * G::EXT3;
+  constexpr int TH = 256, PER = (COUNT + TH - 1) / TH;
+  constexpr int GRP = PER < 12 ? PER : 12;  // loads in flight per thread
+#pragma unroll 1
+  for (int q0 = 0; q0 < PER; q0 += GRP) {
+    double v[GRP];
+    uint32_t e[GRP];
+#pragma unroll
+    for (int q = 0; q < GRP; ++q) {
+      const int c = threadIdx.x + (q0 + q) * TH;
+      e[q] = c < COUNT ? __ldg(shell + c) : 0xFFFFFFFFu;
+    }
+#pragma unroll
+    for (int q = 0; q < GRP; ++q)
+      if (e[q] != 0xFFFFFFFFu)
+        v[q] = pool[nbase[e[q] >> 16] + (e[q] & 0xFFFFu)];
+#pragma unroll
+    for (int q = 0; q < GRP; ++q)
+      if (e[q] != 0xFFFFFFFFu) dst[e[q] & 0xFFFFu] = v[q];
+  }
+}
+
 // prep_body (kernels.py:69-70): whole-extended-array copy, 16 B vectors.
 template <int N>
 __global__ void __launch_bounds__(256)
@@ -506,16 +584,20 @@ __global__ void __launch_bounds__(256)
 // (G,G,G) field <-> the owned cells of the (S,E,E,E) pool.  DIR 0: field ->
 // pool (ghosts untouched), DIR 1: pool -> field.  One thread per owned cell,
 // consecutive threads along z in both layouts.
+// Sub-grid layers [layer0, layer0 + layers) along x only (the chunks of a
+// pipelined upload); the whole field is layer0 = 0, layers = per_axis.
 template <int N, int DIR>
 __global__ void __launch_bounds__(256)
     k_field_pool(double* __restrict__ field, double* __restrict__ pool,
-                 int per_axis) {
+                 int per_axis, int layer0, int layers) {
   using G = Geo<N>;
   constexpr int E = G::E;
   const int m = per_axis, Gn = per_axis * N;
-  const int64_t total = (int64_t)Gn * Gn * Gn;
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
-       t += (int64_t)gridDim.x * blockDim.x) {
+  const int64_t plane = (int64_t)Gn * Gn;
+  const int64_t first = (int64_t)layer0 * N * plane;
+  const int64_t total = first + (int64_t)layers * N * plane;
+  for (int64_t t = first + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+       t < total; t += (int64_t)gridDim.x * blockDim.x) {
     const int x = (int)(t / ((int64_t)Gn * Gn));
     const int y = (int)((t / Gn) % Gn), z = (int)(t % Gn);
     const int64_t id = ((int64_t)(x / N) * m + y / N) * m + z / N;
@@ -655,6 +737,7 @@ struct QueueCtl {
   long long published;    // slices published so far (monotonic)
   long long final_count;  // -1 while more may come
   long long completed;    // slices finished (written by the fetcher only)
+  long long status;       // 0 ok; 1 a fetcher / consumer timed out
 };
 // device-side mirror, polled by the consumers through L2 (only the fetcher
 // CTA ever touches host memory, so the pollers do not flood PCIe)
@@ -772,6 +855,7 @@ __device__ void queue_fetcher(const int* __restrict__ ring_h, QueueCtl* ctl,
       int stop = fin >= 0 && fetched >= fin ? 1 : 0;
       if (!stop && (long long)(globaltimer() - last_change) > timeout_ns) {
         st_release_gpu(&qd->final_count, fetched);
+        st_release_sys(&ctl->status, 1);
         stop = 2;
       }
       s_stop = stop;
@@ -796,7 +880,10 @@ __device__ void queue_fetcher(const int* __restrict__ ring_h, QueueCtl* ctl,
         last_change = globaltimer();
       }
       if (done >= fin) break;
-      if ((long long)(globaltimer() - last_change) > timeout_ns) break;
+      if ((long long)(globaltimer() - last_change) > timeout_ns) {
+        st_release_sys(&ctl->status, 1);
+        break;
+      }
       __nanosleep(32);
     }
   }
@@ -811,7 +898,34 @@ __device__ void queue_fetcher(const int* __restrict__ ring_h, QueueCtl* ctl,
   }
 }
 
-template <int N, int THREADS>
+// Claim the next published slice for this CTA (thread 0 only): one atomic
+// on the claim counter, then poll the tagged ring slot until it carries this
+// run's epoch.  Returns the sub-grid id, -1 once the queue is closed and
+// drained, -2 on timeout.
+__device__ __forceinline__ int queue_claim(QueueDev* qd,
+                                           const unsigned long long* ring_d,
+                                           long long ring_cap, unsigned epoch,
+                                           long long timeout_ns) {
+  const long long k = (long long)atomicAdd(&qd->claim, 1ULL);
+  const unsigned long long t0 = globaltimer();
+  for (;;) {
+    // this run publishes at most ring_cap ids: a slot beyond them is never
+    // filled (and lies outside the ring)
+    if (k >= ring_cap) return -1;
+    // relaxed polls only: an acquire would invalidate the SM's L1
+    // (CCTL.IVALL) once per slice, under every CTA's spilled registers
+    const unsigned long long v = ld_relaxed_gpu_u64(ring_d + k);
+    if ((unsigned)(v >> 32) == epoch) return (int)(unsigned)v;
+    const long long fin = ld_relaxed_gpu(&qd->final_count);
+    if (fin >= 0 && k >= fin) return -1;  // queue closed and drained
+    if ((long long)(globaltimer() - t0) > timeout_ns) return -2;
+    __nanosleep(100);
+  }
+}
+
+// DEPTH boxes per CTA: with DEPTH = 2 the next slice is claimed and its
+// stencil box is in flight (TMA) while the current one is computed.
+template <int N, int THREADS, int DEPTH>
 __global__ void __launch_bounds__(THREADS, recon_min_blocks<THREADS>())
     k_queue_consumer(const __grid_constant__ CUtensorMap tmap,
                      const int* __restrict__ ring_h, QueueCtl* ctl,
@@ -830,62 +944,47 @@ __global__ void __launch_bounds__(THREADS, recon_min_blocks<THREADS>())
     return;
   }
   extern __shared__ __align__(128) double sbox[];
-  __shared__ __align__(8) uint64_t bar;
+  __shared__ __align__(8) uint64_t bar[DEPTH];
   __shared__ double red[THREADS / 32];
-  __shared__ int s_g;
-  if (threadIdx.x == 0) mbar_init(&bar, 1);
-  __syncthreads();
-  uint32_t phase = 0;
-  for (;;) {
-    if (threadIdx.x == 0) {
-      const long long k = (long long)atomicAdd(&qd->claim, 1ULL);
-      const unsigned long long t0 = globaltimer();
-      int g;
-      for (;;) {
-        // this run publishes at most ring_cap ids: a slot beyond them is
-        // never filled (and lies outside the ring)
-        if (k >= ring_cap) {
-          g = -1;
-          break;
-        }
-        // relaxed polls only: an acquire would invalidate the SM's L1
-        // (CCTL.IVALL) once per slice, under every CTA's spilled registers
-        const unsigned long long v = ld_relaxed_gpu_u64(ring_d + k);
-        if ((unsigned)(v >> 32) == epoch) {
-          g = (int)(unsigned)v;
-          break;
-        }
-        const long long fin = ld_relaxed_gpu(&qd->final_count);
-        if (fin >= 0 && k >= fin) {
-          g = -1;  // queue closed and drained
-          break;
-        }
-        if ((long long)(globaltimer() - t0) > timeout_ns) {
-          g = -2;  // nothing arrives: give the GPU back
-          break;
-        }
-        __nanosleep(100);
-      }
-      s_g = g;
-      if (g >= 0) {
-        mbar_expect_tx(&bar, G::BOX * (uint32_t)sizeof(double));
-        tma_load_box(sbox, &tmap, 0, 1, 1, g, &bar);
-      }
+  __shared__ int s_g[DEPTH];
+  auto claim_into = [&](int d) {
+    const int g = queue_claim(qd, ring_d, ring_cap, epoch, timeout_ns);
+    s_g[d] = g;
+    if (g >= 0) {
+      mbar_expect_tx(&bar[d], G::BOX * (uint32_t)sizeof(double));
+      tma_load_box(sbox + d * G::BOX, &tmap, 0, 1, 1, g, &bar[d]);
+    } else if (g == -2) {
+      // nothing arrived in time: give the GPU back and tell the host
+      st_release_sys(&ctl->status, 1);
     }
-    __syncthreads();
-    const int g = s_g;
+  };
+  if (threadIdx.x == 0) {
+    for (int d = 0; d < DEPTH; ++d) mbar_init(&bar[d], 1);
+    claim_into(0);
+  }
+  __syncthreads();
+  uint32_t phases = 0;
+  for (int i = 0;; ++i) {
+    const int d = DEPTH == 1 ? 0 : i % DEPTH;
+    const int g = s_g[d];
     if (g < 0) break;
-    mbar_wait(&bar, phase);
-    phase ^= 1;
+    if (DEPTH > 1 && threadIdx.x == 0) claim_into((i + 1) % DEPTH);
+    mbar_wait(&bar[d], (phases >> d) & 1u);
+    phases ^= 1u << d;
     const double speed = slice_compute<N, THREADS, 0, true>(
-        sbox, um + (int64_t)g * 3 * CELLS, up + (int64_t)g * 3 * CELLS,
-        F + (int64_t)g * 3 * CELLS, ax, ay, az, flux_form);
+        sbox + d * G::BOX, um + (int64_t)g * 3 * CELLS,
+        up + (int64_t)g * 3 * CELLS, F + (int64_t)g * 3 * CELLS, ax, ay, az,
+        flux_form);
     if (amax != nullptr) block_max_store<THREADS>(speed, red, amax + g);
-    __syncthreads();  // box consumed, this slice's stores issued
+    __syncthreads();  // box d consumed, this slice's stores issued
     // the completion count is the host's busy signal only (the kernel's
     // exit orders the outputs for the stream), so no fence before it: a
     // fence here held the CTA until its stores drained (-5 us per run)
-    if (threadIdx.x == 0) atomicAdd(&qd->done, 1ULL);
+    if (threadIdx.x == 0) {
+      atomicAdd(&qd->done, 1ULL);
+      if (DEPTH == 1) claim_into(0);
+    }
+    if (DEPTH == 1) __syncthreads();
   }
 }
 
@@ -989,10 +1088,18 @@ int tf_ghost_fill_f64(double* pool_ext, const int32_t* ids, int32_t T,
   if (T < 0 || (ids == nullptr && T != S)) return TF_E_INVALID;
   if (T == 0) return 0;
   cudaStream_t st = (cudaStream_t)stream;
-  if (n == 8)
-    k_ghost_fill<8><<<T, 256, 0, st>>>(pool_ext, ids, per_axis);
-  else
-    k_ghost_fill<16><<<T, 256, 0, st>>>(pool_ext, ids, per_axis);
+  // TASKFUSE_GHOST_V=1: the index-math gather (A/B runs)
+  static const bool v1 = [] {
+    const char* e = std::getenv("TASKFUSE_GHOST_V");
+    return e && e[0] == '1';
+  }();
+  if (n == 8) {
+    if (v1) k_ghost_fill<8><<<T, 256, 0, st>>>(pool_ext, ids, per_axis);
+    else k_ghost_fill_shell<8><<<T, 256, 0, st>>>(pool_ext, ids, per_axis);
+  } else {
+    if (v1) k_ghost_fill<16><<<T, 256, 0, st>>>(pool_ext, ids, per_axis);
+    else k_ghost_fill_shell<16><<<T, 256, 0, st>>>(pool_ext, ids, per_axis);
+  }
   return cudaGetLastError();
 }
 
@@ -1023,26 +1130,39 @@ int tf_reduce_f64(const int32_t* ids, int32_t T, double ax, double ay,
 }
 
 static int field_pool(double* field, double* pool, int32_t grid_n, int32_t n,
-                      int dir, tf_stream_t stream) {
+                      int dir, tf_stream_t stream, int layer0 = 0,
+                      int layers = -1) {
   if (!valid_n(n) || grid_n < n || grid_n % n || !field || !pool)
     return TF_E_INVALID;
   const int m = grid_n / n;
-  const int64_t total = (int64_t)grid_n * grid_n * grid_n;
+  if (layers < 0) layers = m;
+  if (layer0 < 0 || layer0 + layers > m) return TF_E_INVALID;
+  if (layers == 0) return 0;
+  const int64_t total = (int64_t)layers * n * grid_n * grid_n;
   const int blocks =
       (int)((total + 255) / 256 < 148 * 32 ? (total + 255) / 256 : 148 * 32);
   cudaStream_t st = (cudaStream_t)stream;
   if (n == 8) {
     if (dir == 0)
-      k_field_pool<8, 0><<<blocks, 256, 0, st>>>(field, pool, m);
+      k_field_pool<8, 0><<<blocks, 256, 0, st>>>(field, pool, m, layer0, layers);
     else
-      k_field_pool<8, 1><<<blocks, 256, 0, st>>>(field, pool, m);
+      k_field_pool<8, 1><<<blocks, 256, 0, st>>>(field, pool, m, layer0, layers);
   } else {
     if (dir == 0)
-      k_field_pool<16, 0><<<blocks, 256, 0, st>>>(field, pool, m);
+      k_field_pool<16, 0><<<blocks, 256, 0, st>>>(field, pool, m, layer0,
+                                                  layers);
     else
-      k_field_pool<16, 1><<<blocks, 256, 0, st>>>(field, pool, m);
+      k_field_pool<16, 1><<<blocks, 256, 0, st>>>(field, pool, m, layer0,
+                                                  layers);
   }
   return cudaGetLastError();
+}
+
+int tf_field_to_pool_layers_f64(const double* field, int32_t grid_n,
+                                int32_t n, int32_t layer0, int32_t layers,
+                                double* pool_ext, tf_stream_t stream) {
+  return field_pool(const_cast<double*>(field), pool_ext, grid_n, n, 0,
+                    stream, layer0, layers);
 }
 
 int tf_field_to_pool_f64(const double* field, int32_t grid_n, int32_t n,
@@ -1091,29 +1211,63 @@ int tf_recon_flux_ppm_f64(const double* pool_ext, int64_t pool_slices,
   return cudaGetLastError();
 }
 
+}  // extern "C"
+
+namespace {
+
+// Box ring depth of the consumer: 2 (the next slice's box in flight while
+// the current one is computed) unless TASKFUSE_QUEUE_DEPTH=1 (A/B runs).
+int queue_depth() {
+  static const int d = [] {
+    const char* e = std::getenv("TASKFUSE_QUEUE_DEPTH");
+    return (e && e[0] == '1') ? 1 : 2;
+  }();
+  return d;
+}
+
+template <int N, int DEPTH>
+int consumer_occupancy(int* res) {
+  constexpr int TH = 512;
+  const int smem = DEPTH * Geo<N>::BOX * (int)sizeof(double);
+  cudaError_t e = cudaFuncSetAttribute(
+      k_queue_consumer<N, TH, DEPTH>,
+      cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e == cudaSuccess)
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+        res, k_queue_consumer<N, TH, DEPTH>, TH, smem);
+  return e;
+}
+
+template <int N, int DEPTH>
+void consumer_launch(const CUtensorMap& map, int ctas, cudaStream_t st,
+                     const int32_t* ring_h, QueueCtl* c, int64_t* ring_d,
+                     int64_t ring_cap, QueueDev* q, QueueDev* qn,
+                     int32_t epoch, double ax, double ay, double az,
+                     double* um, double* up, double* F, double* amax,
+                     int32_t flux_form, int64_t timeout_ns) {
+  constexpr int TH = 512;
+  k_queue_consumer<N, TH, DEPTH>
+      <<<ctas + 1, TH, DEPTH * Geo<N>::BOX * sizeof(double), st>>>(
+          map, ring_h, c, reinterpret_cast<unsigned long long*>(ring_d),
+          (long long)ring_cap, q, qn, (unsigned)epoch, ax, ay, az, um, up, F,
+          amax, flux_form, timeout_ns);
+}
+
+}  // namespace
+
+extern "C" {
+
 int tf_queue_consumer_ctas(int32_t n) {
   if (!valid_n(n)) return -TF_E_INVALID;
   int dev = 0, sms = 0, res = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  constexpr int TH = 512;
-  cudaError_t e;
-  if (n == 8) {
-    e = cudaFuncSetAttribute(k_queue_consumer<8, TH>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)(Geo<8>::BOX * sizeof(double)));
-    if (e == cudaSuccess)
-      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-          &res, k_queue_consumer<8, TH>, TH, Geo<8>::BOX * sizeof(double));
-  } else {
-    e = cudaFuncSetAttribute(k_queue_consumer<16, TH>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)(Geo<16>::BOX * sizeof(double)));
-    if (e == cudaSuccess)
-      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-          &res, k_queue_consumer<16, TH>, TH, Geo<16>::BOX * sizeof(double));
-  }
-  if (e != cudaSuccess) return -(int)e;
+  const bool two = queue_depth() == 2;
+  int e = n == 8 ? (two ? consumer_occupancy<8, 2>(&res)
+                        : consumer_occupancy<8, 1>(&res))
+                 : (two ? consumer_occupancy<16, 2>(&res)
+                        : consumer_occupancy<16, 1>(&res));
+  if (e != cudaSuccess) return -e;
   return sms * (res > 0 ? res : 1);
 }
 
@@ -1131,23 +1285,31 @@ int tf_queue_consumer_launch(const double* pool_ext, int64_t pool_slices,
   CUtensorMap map;
   int rc = pool_map(pool_ext, pool_slices, n, &map);
   if (rc) return rc;
-  constexpr int TH = 512;
   cudaStream_t st = (cudaStream_t)stream;
   QueueCtl* c = static_cast<QueueCtl*>(ctl_h);
   QueueDev* q = static_cast<QueueDev*>(qdev);
+  QueueDev* qn = static_cast<QueueDev*>(qdev_next);
   // grid: the fetcher block + `ctas` consumers
-  if (n == 8)
-    k_queue_consumer<8, TH><<<ctas + 1, TH, Geo<8>::BOX * sizeof(double), st>>>(
-        map, ring_h, c, reinterpret_cast<unsigned long long*>(ring_d),
-        (long long)ring_cap, q, static_cast<QueueDev*>(qdev_next),
-        (unsigned)epoch, ax, ay, az, um, up, F, amax, flux_form, timeout_ns);
-  else
-    k_queue_consumer<16, TH>
-        <<<ctas + 1, TH, Geo<16>::BOX * sizeof(double), st>>>(
-            map, ring_h, c, reinterpret_cast<unsigned long long*>(ring_d),
-            (long long)ring_cap, q, static_cast<QueueDev*>(qdev_next),
-            (unsigned)epoch, ax, ay, az, um, up, F, amax, flux_form,
-            timeout_ns);
+  const bool two = queue_depth() == 2;
+  if (n == 8) {
+    if (two)
+      consumer_launch<8, 2>(map, ctas, st, ring_h, c, ring_d, ring_cap, q, qn,
+                            epoch, ax, ay, az, um, up, F, amax, flux_form,
+                            timeout_ns);
+    else
+      consumer_launch<8, 1>(map, ctas, st, ring_h, c, ring_d, ring_cap, q, qn,
+                            epoch, ax, ay, az, um, up, F, amax, flux_form,
+                            timeout_ns);
+  } else {
+    if (two)
+      consumer_launch<16, 2>(map, ctas, st, ring_h, c, ring_d, ring_cap, q,
+                             qn, epoch, ax, ay, az, um, up, F, amax,
+                             flux_form, timeout_ns);
+    else
+      consumer_launch<16, 1>(map, ctas, st, ring_h, c, ring_d, ring_cap, q,
+                             qn, epoch, ax, ay, az, um, up, F, amax,
+                             flux_form, timeout_ns);
+  }
   return cudaGetLastError();
 }
 

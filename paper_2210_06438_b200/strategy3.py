@@ -284,6 +284,7 @@ class QueueExecutor:
                    "tf_qexec_create")
         self.handle = h
         self.n = n
+        self.runs = 0
 
     def run(self, pool, velocity, ids, um, up, F, amax=None, flux_form=0,
             stream=None) -> int:
@@ -303,10 +304,16 @@ class QueueExecutor:
             um.data_ptr(), up.data_ptr(), F.data_ptr(),
             None if amax is None else amax.data_ptr(), int(flux_form),
             s.cuda_stream, C.byref(teams)), "tf_qexec_run_recon_flux")
+        self.runs += 1
         return teams.value
 
     def completed(self) -> int:
         return self.lib.tf_qexec_completed(self.handle)
+
+    def wait(self) -> None:
+        """Block until every run has drained; raises TaskfuseCudaError if a
+        consumer grid timed out with slices unprocessed."""
+        _lib.check(self.lib.tf_qexec_wait(self.handle), "tf_qexec_wait")
 
     def stats(self) -> dict:
         return self.core.stats()
