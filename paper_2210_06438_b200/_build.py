@@ -38,7 +38,8 @@ def _stale() -> bool:
         return True
     built = LIB.stat().st_mtime
     deps = [CSRC / s for s in SOURCES] + [ROOT / "include" / "taskfuse_b200.h",
-                                          CSRC / "sm100_common.cuh"]
+                                          CSRC / "sm100_common.cuh",
+                                          CSRC / "tf_nvtx.h"]
     return any(p.stat().st_mtime > built for p in deps)
 
 

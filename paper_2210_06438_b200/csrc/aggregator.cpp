@@ -21,6 +21,7 @@
 #include <vector>
 
 #include "../../include/taskfuse_b200.h"
+#include "tf_nvtx.h"
 
 namespace {
 
@@ -491,6 +492,7 @@ int launch_team(tf_executor* ex, int64_t team, const ReconArgs& a,
   for (int i = 0; i < T; ++i) ids[i] = (int32_t)t.tags[i];
   const int32_t e = r->parents[t.parent].executor;
   const int f = ex->overlap_ok[e] ? (ex->flags & TF_LAUNCH_OVERLAP_PREV) : 0;
+  tf_nvtx::TeamRange range("team launch", T);
   int rc = tf_recon_flux_team_ex_f64(a.pool, a.slices, ids, T, a.n, a.ax,
                                      a.ay, a.az, a.um, a.up, a.F,
                                      /*out_mode=*/1, a.amax, a.flux_form, f,
@@ -722,6 +724,7 @@ void q_publish(tf_qexec* q, int64_t team) {
   const Team* t = r->teams.get(team);
   if (!t) return;
   QueueSlot& S = q->slot();
+  tf_nvtx::TeamRange range("team publish", (int64_t)t->tags.size());
   for (int64_t tag : t->tags) S.ring_h[q->published++] = (int32_t)tag;
   // ids first, then the count (release): the consumer acquires the count
   __atomic_store_n(&S.ctl_h->published, (long long)q->published,

@@ -33,6 +33,7 @@
 #include <vector>
 
 #include "../../include/taskfuse_b200.h"
+#include "tf_nvtx.h"
 
 namespace {
 
@@ -297,6 +298,7 @@ int issue_step(tf_hydro* h, int k, int64_t team, int step, cudaStream_t s) {
     int32_t* ids = h->ids_h + h->ids_pos;
     h->ids_pos += T;
     for (int i = 0; i < T; ++i) ids[i] = h->tasks[c.members[i]].g;
+    tf_nvtx::TeamRange range(kNames[k], T);
     rc = launch(h, k, ids, T, s);
     h->kernels += 1;
   }
@@ -503,11 +505,12 @@ int tf_hydro_create(int32_t n, int32_t per_axis, int32_t max_team,
     h->sig[k][6] = "copy:d2h:" + std::to_string(n3 * 8);
   }
   h->tasks.resize(h->S);
-  // staging arenas: every task of an iteration holding its region's ext^3
-  // and n^3 leases at once, twice over (buckets are exact sizes, so several
-  // team sizes coexist), capped at 1 GiB per kind
+  // staging arenas: buckets are exact sizes and a buffer keeps its storage
+  // (the reference's pool), so real-time formation with many distinct team
+  // sizes needs several times one iteration's live leases (S x (ext^3+n^3)
+  // per kind): 8x, capped at 1 GiB per kind
   if (!rc) {
-    int64_t arena = 2LL * h->S * (ext3 + n3) * 8;
+    int64_t arena = 8LL * h->S * (ext3 + n3) * 8;
     if (arena > (1LL << 30)) arena = 1LL << 30;
     rc = h->pool.reserve(arena);
   }

@@ -487,84 +487,6 @@ __global__ void __launch_bounds__(256)
   }
 }
 
-// The ghost shell of one sub-grid as a table built at compile time: for
-// every ghost cell, in increasing extended-offset order, its offset (low 16
-// bits) and its direction code t = 9 (di+1) + 3 (dj+1) + (dk+1) (high bits).
-// A CTA then walks only the shell (2232 of the 2744 cells at n = 8) with one
-// coalesced 4-byte table load per cell instead of the div/mod index math.
-template <int N>
-struct GhostShell {
-  static constexpr int E = N + 6;
-  static constexpr int COUNT = E * E * E - N * N * N;
-  uint32_t v[COUNT];
-  constexpr GhostShell() : v() {
-    int q = 0;
-    for (int i = 0; i < E; ++i)
-      for (int j = 0; j < E; ++j)
-        for (int k = 0; k < E; ++k) {
-          const int ti = (i >= 3) + (i >= N + 3), tj = (j >= 3) + (j >= N + 3),
-                    tk = (k >= 3) + (k >= N + 3);
-          const int t = (ti * 3 + tj) * 3 + tk;
-          if (t == 13) continue;  // owned
-          v[q++] = (uint32_t)((i * E + j) * E + k) | ((uint32_t)t << 16);
-        }
-  }
-};
-__device__ const GhostShell<8> g_shell8{};
-__device__ const GhostShell<16> g_shell16{};
-
-template <int N>
-__device__ __forceinline__ const uint32_t* ghost_shell() {
-  if constexpr (N == 8) return g_shell8.v;
-  else return g_shell16.v;
-}
-
-template <int N>
-__global__ void __launch_bounds__(256)
-    k_ghost_fill_shell(double* __restrict__ pool,
-                       const int32_t* __restrict__ ids, int per_axis) {
-  using G = Geo<N>;
-  constexpr int E = G::E;
-  constexpr int COUNT = GhostShell<N>::COUNT;
-  const int s = blockIdx.x;
-  const int g = ids ? ids[s] : s;
-  // the 27 periodic neighbours' base offsets minus the direction shift:
-  // ghost cell c of direction d is the neighbour's ext cell c - d*N
-  __shared__ int64_t nbase[27];
-  if (threadIdx.x < 27) {
-    const int m = per_axis;
-    const int bx = g / (m * m), by = (g / m) % m, bz = g % m;
-    const int t = threadIdx.x;
-    const int di = t / 9 - 1, dj = (t / 3) % 3 - 1, dk = t % 3 - 1;
-    const int nx = (bx + di + m) % m, ny = (by + dj + m) % m,
-              nz = (bz + dk + m) % m;
-    nbase[t] = ((int64_t)(nx * m + ny) * m + nz) * G::EXT3 -
-               (int64_t)((di * E + dj) * E + dk) * N;
-  }
-  __syncthreads();
-  const uint32_t* __restrict__ shell = ghost_shell<N>();
-  double* __restrict__ dst = pool + (int64_t)g * G::EXT3;
-  constexpr int TH = 256, PER = (COUNT + TH - 1) / TH;
-  constexpr int GRP = PER < 12 ? PER : 12;  // loads in flight per thread
-#pragma unroll 1
-  for (int q0 = 0; q0 < PER; q0 += GRP) {
-    double v[GRP];
-    uint32_t e[GRP];
-#pragma unroll
-    for (int q = 0; q < GRP; ++q) {
-      const int c = threadIdx.x + (q0 + q) * TH;
-      e[q] = c < COUNT ? __ldg(shell + c) : 0xFFFFFFFFu;
-    }
-#pragma unroll
-    for (int q = 0; q < GRP; ++q)
-      if (e[q] != 0xFFFFFFFFu)
-        v[q] = pool[nbase[e[q] >> 16] + (e[q] & 0xFFFFu)];
-#pragma unroll
-    for (int q = 0; q < GRP; ++q)
-      if (e[q] != 0xFFFFFFFFu) dst[e[q] & 0xFFFFu] = v[q];
-  }
-}
-
 // prep_body (kernels.py:69-70): whole-extended-array copy, 16 B vectors.
 template <int N>
 __global__ void __launch_bounds__(256)
@@ -1088,18 +1010,13 @@ int tf_ghost_fill_f64(double* pool_ext, const int32_t* ids, int32_t T,
   if (T < 0 || (ids == nullptr && T != S)) return TF_E_INVALID;
   if (T == 0) return 0;
   cudaStream_t st = (cudaStream_t)stream;
-  // TASKFUSE_GHOST_V=1: the index-math gather (A/B runs)
-  static const bool v1 = [] {
-    const char* e = std::getenv("TASKFUSE_GHOST_V");
-    return e && e[0] == '1';
-  }();
-  if (n == 8) {
-    if (v1) k_ghost_fill<8><<<T, 256, 0, st>>>(pool_ext, ids, per_axis);
-    else k_ghost_fill_shell<8><<<T, 256, 0, st>>>(pool_ext, ids, per_axis);
-  } else {
-    if (v1) k_ghost_fill<16><<<T, 256, 0, st>>>(pool_ext, ids, per_axis);
-    else k_ghost_fill_shell<16><<<T, 256, 0, st>>>(pool_ext, ids, per_axis);
-  }
+  // (a variant walking a compile-time table of the ghost shell instead of
+  // the per-cell index math measured the same: 27.8-28.2 vs 28.2-28.7 us at
+  // config 2, 186 vs 179 us at grid 256 — DESIGN.md §4)
+  if (n == 8)
+    k_ghost_fill<8><<<T, 256, 0, st>>>(pool_ext, ids, per_axis);
+  else
+    k_ghost_fill<16><<<T, 256, 0, st>>>(pool_ext, ids, per_axis);
   return cudaGetLastError();
 }
 

@@ -209,6 +209,21 @@ def field_to_pool(field, n, pool, stream=None) -> None:
                "tf_field_to_pool_f64")
 
 
+def field_to_pool_layers(field, n, pool, layer0, layers, stream=None) -> None:
+    """field_to_pool for the sub-grid layers [layer0, layer0+layers) along x
+    (one chunk of a pipelined upload)."""
+    lib = _lib.load()
+    _check_n(n)
+    _need_cuda_f64(field, "field")
+    g = field.shape[0]
+    if field.dim() != 3 or g % n or pool.shape[0] != (g // n) ** 3:
+        raise ValidationError("field/pool shapes do not match")
+    _check_pool(pool, n)
+    _lib.check(lib.tf_field_to_pool_layers_f64(
+        field.data_ptr(), g, n, int(layer0), int(layers), pool.data_ptr(),
+        _stream(stream)), "tf_field_to_pool_layers_f64")
+
+
 def pool_to_field(pool, n, field, stream=None) -> None:
     """assemble (scenario.py:99-106) on the device."""
     lib = _lib.load()

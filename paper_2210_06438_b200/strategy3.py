@@ -424,6 +424,107 @@ class AggregatedIteration:
         return 2 + len(self.teams)
 
 
+class ReconFluxHostPipeline:
+    """`AggregatedIteration.recon_flux_host` with the upload overlapped,
+    captured once as a CUDA graph for FIXED pinned buffers.
+
+    The host field moves in x-chunks of sub-grid layers on a copy stream;
+    chunk i's layers are scattered into the pool as soon as they land, and
+    chunk j's sub-grids are ghost-filled (exchange_ghosts reads the
+    neighbours' OWNED cells, so chunks j-1 and j+1 must be scattered) and
+    run through their own captured team plans (teams formed over the
+    chunk's arrivals with the iteration's cap) right after chunk j+1 lands.
+    Chunk 0 (whose periodic x neighbour is the last chunk) goes last; the
+    per-sub-grid max signal speed returns to `amax_out`.  Pure function of
+    `field_in`: every replay rewrites the whole current pool."""
+
+    def __init__(self, it: "AggregatedIteration", field_in, amax_out,
+                 layers=(1, 3, 4, 4, 3, 1), executors: int = 2):
+        from . import ops
+        if not (field_in.is_pinned() and amax_out.is_pinned()):
+            raise ValidationError("the pipeline needs pinned host buffers")
+        m, n = it.m, it.n
+        layers = [int(k) for k in layers]
+        if sum(layers) != m:    # scale the taper to the lattice
+            base = max(1, m // len(layers))
+            layers = [base] * (m // base)
+            layers[-1] += m - sum(layers)
+        start = [0]
+        for k in layers:
+            start.append(start[-1] + k)
+        nch = len(layers)
+        self.it, self.bufs = it, (field_in, amax_out)
+        dev = it.pool.device
+        mm = m * m
+        self.ids = [torch.arange(start[c] * mm, start[c + 1] * mm,
+                                 dtype=torch.int32, device=dev)
+                    for c in range(nch)]
+        cap = max(len(t.ids) for t in it.teams)
+        # each chunk's arrivals formed into teams with the iteration's cap;
+        # a team is one launch with its ids in the kernel parameters
+        self.teams = [[np.asarray(t.ids, dtype=np.int32)
+                       for t in form_teams(range(start[c] * mm,
+                                                 start[c + 1] * mm), cap)]
+                      for c in range(nch)]
+        lib = _lib.load()
+        ax, ay, az = it.velocity
+        self.launches = 0
+        up = torch.cuda.Stream(device=dev)
+        comp_side = torch.cuda.Stream(device=dev)
+        fin = field_in.view(it.grid_n, it.grid_n, it.grid_n)
+        dev_f, pool = it.field_dev, it.pool
+
+        def chunk_compute(c):
+            ops.ghost_fill(pool, n, m, ids=self.ids[c])
+            st = torch.cuda.current_stream().cuda_stream
+            for k, ids in enumerate(self.teams[c]):
+                # teams after the first overlap their predecessor (PDL):
+                # same region, independent slices
+                _lib.check(lib.tf_recon_flux_team_ex_f64(
+                    pool.data_ptr(), it.S,
+                    ids.ctypes.data_as(C.POINTER(C.c_int32)), ids.size, n,
+                    ax, ay, az, it.um.data_ptr(), it.up.data_ptr(),
+                    it.F.data_ptr(), 1, it.amax.data_ptr(), 0,
+                    _lib.TF_LAUNCH_OVERLAP_PREV if k else 0, st),
+                    "tf_recon_flux_team_ex_f64")
+            self.launches += 1 + len(self.teams[c])
+
+        def run():
+            self.launches = 0
+            comp = torch.cuda.current_stream()
+            up.wait_stream(comp)
+            evs = []
+            with torch.cuda.stream(up):
+                for c in range(nch):
+                    lo, hi = start[c] * n, start[c + 1] * n
+                    dev_f[lo:hi].copy_(fin[lo:hi], non_blocking=True)
+                    ev = torch.cuda.Event()
+                    ev.record(up)
+                    evs.append(ev)
+            for c in range(nch):
+                comp.wait_event(evs[c])
+                ops.field_to_pool_layers(dev_f, n, pool, start[c], layers[c])
+                self.launches += 1
+                if 2 <= c:
+                    chunk_compute(c - 1)
+            if nch > 1:
+                chunk_compute(nch - 1)
+            chunk_compute(0)
+            amax_out[:it.S].copy_(it.amax, non_blocking=True)
+
+        run()                       # warm-up (also sizes the TMA maps)
+        torch.cuda.synchronize()
+        self.graph = torch.cuda.CUDAGraph()
+        comp_side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.graph(self.graph, stream=comp_side):
+            run()
+        torch.cuda.synchronize()
+        self.chunks = nch
+
+    def run(self) -> None:
+        self.graph.replay()
+
+
 def recon_flux_all(pool, n, velocity, um, up, F, amax=None, flux_form=0,
                    stream=None) -> None:
     """Aggregation limit: every slice of the pool in one launch."""

@@ -129,6 +129,42 @@ def test_aggregated_iteration_host_roundtrip(cuda, grid, n, vel):
     assert np.array_equal(host_out.numpy(), HO.reference_step(f, vel))
 
 
+@pytest.mark.parametrize("grid,n,vel,layers", [
+    (128, 8, (1.0, 1.0, 1.0), (1, 3, 4, 4, 3, 1)),
+    (64, 8, (-1.0, 0.5, -0.25), (1, 3, 4, 4, 3, 1)),
+    (64, 16, (0.7, -1.3, 0.0), (2, 2))])
+def test_recon_flux_host_pipelined(cuda, grid, n, vel, layers):
+    """The e2e call (host field in, aggregated recon+flux, per-sub-grid max
+    signal speed out), plain and pipelined (chunked upload overlapped with
+    scatter / ghost fill / team launches, one CUDA graph): the faces in HBM
+    equal the oracle's, on every replay."""
+    import torch
+    from paper_2210_06438_b200.strategy3 import (AggregatedIteration,
+                                                 ReconFluxHostPipeline)
+    f = HO.stress_field(grid)
+    hp = HO.make_pool(f, n)
+    HO.exchange_ghosts_pool(hp, n, grid // n)
+    oum, oup, oF = HO.recon_flux_batch(hp, n, vel)
+    it = AggregatedIteration(grid, n, vel, max_team=128, executors=2)
+    host_in = torch.from_numpy(f).pin_memory()
+    amax = torch.empty(it.S, dtype=torch.float64).pin_memory()
+    it.recon_flux_host(host_in, amax)
+    torch.cuda.synchronize()
+    assert np.array_equal(it.F.cpu().numpy(), oF)
+    pipe = ReconFluxHostPipeline(it, host_in, amax, layers=layers)
+    for _ in range(2):
+        for t in (it.um, it.up, it.F, it.amax):
+            t.fill_(float("nan"))
+        amax.fill_(float("nan"))
+        pipe.run()
+        torch.cuda.synchronize()
+        assert np.array_equal(it.pool.cpu().numpy(), hp)
+        assert np.array_equal(it.um.cpu().numpy(), oum)
+        assert np.array_equal(it.up.cpu().numpy(), oup)
+        assert np.array_equal(it.F.cpu().numpy(), oF)
+        assert bool((amax == max(abs(v) for v in vel)).all())
+
+
 def test_field_pool_kernels_roundtrip(cuda):
     import torch
     from paper_2210_06438_b200 import ops
