@@ -288,12 +288,12 @@ class Workload:
 
 
 def plan_runner(wl, max_team, executors, parents=None, overlap=True,
-                team_buffers=False):
+                team_buffers=False, geometry="tma"):
     from paper_2210_06438_b200.strategy3 import TeamPlan, form_teams
     teams = form_teams(range(wl.S), max_team, executors, parents)
     plans = [TeamPlan(teams, p, wl.n, VELOCITY, wl.um, wl.up, wl.F,
                       executors, amax=wl.amax, overlap=overlap,
-                      team_buffers=team_buffers)
+                      team_buffers=team_buffers, geometry=geometry)
              for p in wl.pools]
     hist = {}
     for t in teams:
@@ -408,15 +408,38 @@ def run_sweep(wl, args, world, stream, peak):
         ms = timed(step, ks, kw, world, stream)
         out["strategy2"][E] = {"cell_updates_per_s": rate(wl.S, wl.n, ms),
                                "ms_per_iter": ms, "launches": nk}
+    # strategy 1: 512 sub-grids of 16^3 (same cells), one launch per
+    # sub-grid.  "refgeo": the reference's launch geometry, 46 CTAs x 128
+    # threads per 16^3 sub-grid (blocks_for, kernels.py:51-55) — the fair
+    # baseline; "tma1": our one-CTA-per-slice TMA kernel at 16^3
     wl16 = Workload(n=16, grid=wl.grid, field=FIELD)
-    for E in sorted({args.executors, 4}):
-        step, nk, _, _ = plan_runner(wl16, 1, E)
+    for geo, tag in (("reference", "refgeo"), ("tma", "tma1")):
+        for E in sorted({args.executors, 4}):
+            step, nk, _, _ = plan_runner(wl16, 1, E, geometry=geo)
+            ms = timed(step, ks, kw, world, stream)
+            out["strategy1"][f"16^3_A1_E{E}_{tag}"] = {
+                "cell_updates_per_s": rate(wl16.S, 16, ms),
+                "ms_per_iter": ms, "launches": nk,
+                "ctas_per_launch": 46 if geo == "reference" else 1,
+                "hbm_frac": wl16.S * b_alg(16) / (ms * 1e-3)
+                / (peak * 1e9)}
+    # the same kernels with all 512 sub-grids in one launch (the limit)
+    for geo, tag in (("reference", "refgeo"), ("tma", "tma1")):
+        step, nk, _, _ = plan_runner(wl16, 128, 1, parents=1, geometry=geo)
         ms = timed(step, ks, kw, world, stream)
-        out["strategy1"][f"16^3_A1_E{E}"] = {
+        out["strategy1"][f"16^3_A128_{tag}"] = {
             "cell_updates_per_s": rate(wl16.S, 16, ms), "ms_per_iter": ms,
             "launches": nk, "hbm_frac": wl16.S * b_alg(16) / (ms * 1e-3)
             / (peak * 1e9)}
     del wl16
+    # the 8^3 aggregated path with the reference geometry (A = 128)
+    step, nk, _, _ = plan_runner(wl, 128, args.executors,
+                                 geometry="reference")
+    ms = timed(step, ks, kw, world, stream)
+    out["refgeo_8^3_A128"] = {
+        "cell_updates_per_s": rate(wl.S, wl.n, ms), "ms_per_iter": ms,
+        "launches": nk, "hbm_frac": wl.S * b_alg(wl.n) / (ms * 1e-3)
+        / (peak * 1e9)}
     out["config3"] = config3_sweep(args, world, stream, peak, ks, kw)
     return out
 

@@ -85,6 +85,18 @@ int tf_recon_flux_team_ex_f64(const double* pool_ext, int64_t pool_slices,
                               int32_t flux_form, int32_t flags,
                               tf_stream_t stream);
 
+/* The same team launch with the REFERENCE's launch geometry (blocks_for,
+ * kernels.py:39-55): ceil((n+2)^3/128) blocks of 128 threads per slice
+ * (46 at n = 16), one cell per thread, stencil read from global memory.
+ * The strategy-1 baseline kernel (a 16^3 sub-grid spread over 46 CTAs).   */
+int tf_recon_flux_refgeo_f64(const double* pool_ext, int64_t pool_slices,
+                             const int32_t* host_ids, int32_t T, int32_t n,
+                             double ax, double ay, double az,
+                             double* um, double* up, double* F,
+                             int32_t out_mode, double* amax,
+                             int32_t flux_form, int32_t flags,
+                             tf_stream_t stream);
+
 /* PPM variant (north_star's "batched PPM reconstruction"; Colella-Woodward
  * 1984 with CW84 limiting) of tf_recon_flux_f64, same arguments and layout.
  * The reference has no PPM (its scheme is minmod): parity is
@@ -331,6 +343,9 @@ typedef struct tf_plan tf_plan;
  * buffers: team t's slice s at flat index team_offsets[t] + s — the
  * reference's slice_alloc lease layout (aggregator.py:121-128).            */
 #define TF_PLAN_TEAM_BUFFERS 2
+/* TF_PLAN_REFGEO: capture tf_recon_flux_refgeo_f64 team launches (the
+ * reference's launch geometry) instead of the TMA kernel.                  */
+#define TF_PLAN_REFGEO 16
 int tf_plan_capture_recon_flux(const int32_t* ids, const int64_t* team_offsets,
                                const int32_t* team_executor, int64_t nteams,
                                int32_t executors, const double* pool_ext,

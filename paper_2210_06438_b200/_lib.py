@@ -28,6 +28,7 @@ TF_E_TIMEOUT = 1005
 MAX_TEAM = 128
 TF_LAUNCH_OVERLAP_PREV = 1
 TF_PLAN_TEAM_BUFFERS = 2
+TF_PLAN_REFGEO = 16
 TF_STEP_HALO_YZ = 4
 TF_STEP_HALO_X = 8
 
@@ -49,6 +50,9 @@ SIGNATURES = {
     "tf_recon_flux_team_ex_f64": (C.c_int, [_p, _i64, _pi32, _i32, _i32, _f64,
                                             _f64, _f64, _p, _p, _p, _i32, _p,
                                             _i32, _i32, _p]),
+    "tf_recon_flux_refgeo_f64": (C.c_int, [_p, _i64, _pi32, _i32, _i32, _f64,
+                                           _f64, _f64, _p, _p, _p, _i32, _p,
+                                           _i32, _i32, _p]),
     "tf_recon_flux_ppm_f64": (C.c_int, [_p, _i64, _p, _i32, _i32, _f64, _f64,
                                         _f64, _p, _p, _p, _i32, _p, _i32,
                                         _p]),

@@ -1005,20 +1005,22 @@ int tf_plan_capture_recon_flux(const int32_t* ids, const int64_t* team_offsets,
                                int32_t flags, tf_plan** out) {
   const int64_t per = 3LL * (n + 2) * (n + 2) * (n + 2);
   const bool team_buffers = (flags & TF_PLAN_TEAM_BUFFERS) != 0;
+  // TF_PLAN_REFGEO: the reference's launch geometry instead of one TMA CTA
+  // per slice (the strategy-1 baseline)
+  auto team_launch = (flags & TF_PLAN_REFGEO) ? tf_recon_flux_refgeo_f64
+                                              : tf_recon_flux_team_ex_f64;
   return capture_teams(
       ids, team_offsets, team_executor, nteams, executors, flags,
       [&](const int32_t* tid, int T, int f, tf_stream_t s) {
         if (!team_buffers)
-          return tf_recon_flux_team_ex_f64(pool_ext, pool_slices, tid, T, n,
-                                           ax, ay, az, um, up, F, 1, amax,
-                                           flux_form, f, s);
+          return team_launch(pool_ext, pool_slices, tid, T, n, ax, ay, az, um,
+                             up, F, 1, amax, flux_form, f, s);
         // the team's lease: slices [lo, lo+T) of the iteration's packed
         // team buffers (aggregator.py:121-128), slice s at lo + s
         const int64_t lo = tid - ids;
-        return tf_recon_flux_team_ex_f64(
-            pool_ext, pool_slices, tid, T, n, ax, ay, az, um + lo * per,
-            up + lo * per, F + lo * per, 0, amax ? amax + lo : nullptr,
-            flux_form, f, s);
+        return team_launch(pool_ext, pool_slices, tid, T, n, ax, ay, az,
+                           um + lo * per, up + lo * per, F + lo * per, 0,
+                           amax ? amax + lo : nullptr, flux_form, f, s);
       },
       out);
 }

@@ -58,28 +58,25 @@ int blocks_for(int k, int n) {
 }
 
 // Exact-size recycling pool over real memory (bufferpool.py:112-159):
-// buckets keyed by (kind, bytes), most recently returned first.  As in the
-// reference, a bucket miss creates a buffer record (a "raw allocation",
-// counted) whose storage is materialised lazily — here on first lease
-// (cudaMalloc / cudaHostAlloc, counted separately) — so presizing every
-// team-size bucket (bench.py:142-153) costs no memory until a size occurs.
-//
-// Storage comes from one pre-allocated arena per kind (pinned host, device),
-// carved by a bump pointer: materialising a buffer in the middle of a run
-// costs no allocator call (a cudaHostAlloc per new team size took up to a
-// millisecond — long enough to drain every stream and turn the real-time
-// formation into solo launches).  Only an exhausted arena falls back to a
-// real allocation per buffer.
+// buckets keyed by (kind, bytes), most recently returned record first; a
+// bucket miss creates a buffer record (a "raw allocation", the reference's
+// count).  Storage is managed apart from the records: a lease takes a chunk
+// of the next power-of-two size class from a per-kind free list, or carves
+// a new one from the kind's pre-allocated arena (bump pointer), and gives
+// it back on release.  Real-time formation produces many distinct team
+// sizes; with storage bound to exact-size records every new size held its
+// own memory for good, the arena ran dry and each further size cost a
+// cudaHostAlloc of up to a millisecond — enough to drain the streams and
+// turn formation into solo launches.  Only an exhausted arena falls back to
+// a real allocation per chunk.
 class StagingPool {
  public:
   ~StagingPool() {
-    for (Buf* b : all_) {
-      if (b->ptr && b->own) {
-        if (b->kind == KIND_DEVICE) cudaFree(b->ptr);
-        else cudaFreeHost(b->ptr);
+    for (auto& kv : owned_)
+      for (void* p : kv.second) {
+        if (kv.first == KIND_DEVICE) cudaFree(p);
+        else cudaFreeHost(p);
       }
-      delete b;
-    }
     if (arena_[KIND_DEVICE]) cudaFree(arena_[KIND_DEVICE]);
     if (arena_[KIND_PINNED]) cudaFreeHost(arena_[KIND_PINNED]);
   }
@@ -92,73 +89,81 @@ class StagingPool {
     return 0;
   }
   int acquire(int kind, int64_t bytes, void** out) {
-    Buf* b = take(kind, bytes);
-    if (!b->ptr) {
-      const int64_t need = (bytes + 255) & ~int64_t(255);
-      if (arena_[kind] && used_[kind] + need <= cap_) {
-        b->ptr = static_cast<char*>(arena_[kind]) + used_[kind];
-        used_[kind] += need;
+    take(kind, bytes);  // the record (bucket accounting)
+    const int cls = size_class(bytes);
+    auto& fl = free_[kind][cls];
+    void* p;
+    if (!fl.empty()) {
+      p = fl.back();
+      fl.pop_back();
+    } else {
+      const int64_t chunk = int64_t(1) << cls;
+      if (arena_[kind] && used_[kind] + chunk <= cap_) {
+        p = static_cast<char*>(arena_[kind]) + used_[kind];
+        used_[kind] += chunk;
       } else {
-        cudaError_t e = kind == KIND_DEVICE
-                            ? cudaMalloc(&b->ptr, (size_t)bytes)
-                            : cudaHostAlloc(&b->ptr, (size_t)bytes, 0);
+        cudaError_t e = kind == KIND_DEVICE ? cudaMalloc(&p, (size_t)chunk)
+                                            : cudaHostAlloc(&p, (size_t)chunk, 0);
         if (e != cudaSuccess) {
-          b->ptr = nullptr;
-          give(b);
+          give(kind, bytes);
           return e;
         }
-        b->own = true;
+        owned_[kind].push_back(p);
         spilled_[kind] += 1;
       }
       materialised_[kind] += 1;
     }
-    leased_[b->ptr] = b;
-    *out = b->ptr;
+    leased_[p] = Lease{kind, bytes, cls};
+    *out = p;
     return 0;
   }
-  int64_t spilled() const { return spilled_[0] + spilled_[1]; }
   int release(void* p) {
     auto it = leased_.find(p);
     if (it == leased_.end()) return TF_E_INVALID;
-    give(it->second);
+    const Lease l = it->second;
     leased_.erase(it);
+    free_[l.kind][l.cls].push_back(p);
+    give(l.kind, l.bytes);
     return 0;
   }
-  // bufferpool.py:154-159: `count` buffers of this bucket exist afterwards
+  // bufferpool.py:154-159: `count` records of this bucket exist afterwards
   void ensure(int kind, int64_t bytes, int count) {
-    std::vector<Buf*> held;
-    for (int i = 0; i < count; ++i) held.push_back(take(kind, bytes));
-    for (auto it = held.rbegin(); it != held.rend(); ++it) give(*it);
+    for (int i = 0; i < count; ++i) take(kind, bytes);
+    for (int i = 0; i < count; ++i) give(kind, bytes);
   }
   int64_t raw(int kind) const { return raw_[kind]; }
   int64_t materialised(int kind) const { return materialised_[kind]; }
+  int64_t spilled() const { return spilled_[0] + spilled_[1]; }
   int64_t outstanding() const { return (int64_t)leased_.size(); }
   int64_t acquisitions() const { return acquisitions_; }
 
  private:
-  struct Buf {
+  struct Lease {
     int kind;
     int64_t bytes;
-    void* ptr = nullptr;
-    bool own = false;  // a real allocation (arena exhausted)
+    int cls;
   };
-  Buf* take(int kind, int64_t bytes) {
-    acquisitions_ += 1;
-    auto& b = buckets_[{kind, bytes}];
-    if (!b.empty()) {
-      Buf* x = b.back();
-      b.pop_back();
-      return x;
-    }
-    raw_[kind] += 1;
-    Buf* x = new Buf{kind, bytes};
-    all_.push_back(x);
-    return x;
+  static int size_class(int64_t bytes) {
+    int c = 8;  // 256 B minimum chunk
+    while ((int64_t(1) << c) < bytes) ++c;
+    return c;
   }
-  void give(Buf* b) { buckets_[{b->kind, b->bytes}].push_back(b); }
-  std::map<std::pair<int, int64_t>, std::vector<Buf*>> buckets_;
-  std::map<void*, Buf*> leased_;
-  std::vector<Buf*> all_;
+  // records: per bucket, the number of idle records (LIFO order is moot
+  // once storage is decoupled; the counts are the reference's accounting)
+  void take(int kind, int64_t bytes) {
+    acquisitions_ += 1;
+    int64_t& idle = idle_[{kind, bytes}];
+    if (idle > 0) {
+      idle -= 1;
+    } else {
+      raw_[kind] += 1;
+    }
+  }
+  void give(int kind, int64_t bytes) { idle_[{kind, bytes}] += 1; }
+  std::map<std::pair<int, int64_t>, int64_t> idle_;
+  std::map<int, std::vector<void*>> free_[2];
+  std::map<void*, Lease> leased_;
+  std::map<int, std::vector<void*>> owned_;
   int64_t raw_[2] = {0, 0}, materialised_[2] = {0, 0}, spilled_[2] = {0, 0};
   int64_t acquisitions_ = 0;
   void* arena_[2] = {nullptr, nullptr};

@@ -226,6 +226,50 @@ __global__ void __launch_bounds__(THREADS, recon_min_blocks<THREADS>())
   if (MODE == 0 && amax != nullptr) block_max_store<THREADS>(speed, red, amax + slot);
 }
 
+// ------------------------------------------ reference launch geometry
+// reconstruct_body + flux_body with the REFERENCE's launch geometry
+// (blocks_for, kernels.py:39-55): ceil((n+2)^3 / 128) blocks of 128
+// threads per slice, one face-cube cell per thread, every stencil value
+// read straight from the slice's ghosted sub-grid in global memory (L1 /
+// L2), no staging.  Used for the strategy-1 baseline (n = 16: 46 blocks per
+// sub-grid) so that a larger sub-grid's launch is spread over as many CTAs
+// as the reference assumes.  Same arithmetic as cell_axis (bit-identical).
+template <int N>
+__global__ void __launch_bounds__(128)
+    k_recon_flux_refgeo(const double* __restrict__ pool,
+                        const __grid_constant__ TeamIds team, int out_mode,
+                        double ax, double ay, double az,
+                        double* __restrict__ um, double* __restrict__ up,
+                        double* __restrict__ F, double* __restrict__ amax,
+                        int flux_form) {
+  using G = Geo<N>;
+  constexpr int C = G::C, E = G::E, CELLS = G::CELLS;
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  const int s = blockIdx.y;
+  const int g = team.id[s];
+  const int c = blockIdx.x * 128 + threadIdx.x;
+  const int64_t slot = out_mode ? (int64_t)g : (int64_t)s;
+  if (c < CELLS) {
+    const double* __restrict__ w = pool + (int64_t)g * G::EXT3;
+    const int ci = c / (C * C), cj = (c / C) % C, ck = c % C;
+    // cube (ci,cj,ck) = ext (ci+2, cj+2, ck+2)
+    const int b = ((ci + 2) * E + (cj + 2)) * E + (ck + 2);
+    const int stv[3] = {E * E, E, 1};
+    const int pos[3] = {ci, cj, ck};
+    const double av[3] = {ax, ay, az};
+#pragma unroll
+    for (int axis = 0; axis < 3; ++axis) {
+      const Faces r = cell_axis(w, b, stv[axis], pos[axis], C, av[axis], 0,
+                                flux_form);
+      um[(slot * 3 + axis) * CELLS + c] = r.vm;
+      up[(slot * 3 + axis) * CELLS + c] = r.vp;
+      F[(slot * 3 + axis) * CELLS + c] = r.f;
+    }
+  }
+  if (amax != nullptr && blockIdx.x == 0 && threadIdx.x == 0)
+    amax[slot] = fmax(fmax(fabs(ax), fabs(ay)), fabs(az));
+}
+
 // ------------------------------------------------ PPM reconstruction
 // Piecewise-parabolic reconstruction (Colella & Woodward 1984), the scheme
 // north_star names for Octo-Tiger; the reference artifact has no PPM
@@ -957,6 +1001,38 @@ int tf_recon_flux_team_ex_f64(const double* pool_ext, int64_t pool_slices,
   return dispatch_recon<0, false>(pool_ext, pool_slices, nullptr, team, T, n,
                                   out_mode, ax, ay, az, um, up, F, amax,
                                   flux_form, (cudaStream_t)stream, flags);
+}
+
+int tf_recon_flux_refgeo_f64(const double* pool_ext, int64_t pool_slices,
+                             const int32_t* host_ids, int32_t T, int32_t n,
+                             double ax, double ay, double az, double* um,
+                             double* up, double* F, int32_t out_mode,
+                             double* amax, int32_t flux_form, int32_t flags,
+                             tf_stream_t stream) {
+  if (!valid_n(n) || T < 1 || T > TF_MAX_TEAM || !host_ids || !pool_ext ||
+      !um || !up || !F || (flux_form != 0 && flux_form != 1))
+    return TF_E_INVALID;
+  TeamIds team;
+  for (int i = 0; i < T; ++i) {
+    if (host_ids[i] < 0 || host_ids[i] >= pool_slices) return TF_E_INVALID;
+    team.id[i] = host_ids[i];
+  }
+  const int C = n + 2;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)((C * C * C + 127) / 128), (unsigned)T);
+  cfg.blockDim = dim3(128);
+  cfg.stream = (cudaStream_t)stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = (flags & TF_LAUNCH_OVERLAP_PREV) ? 1 : 0;
+  if (n == 8)
+    return cudaLaunchKernelEx(&cfg, k_recon_flux_refgeo<8>, pool_ext, team,
+                              out_mode, ax, ay, az, um, up, F, amax,
+                              flux_form);
+  return cudaLaunchKernelEx(&cfg, k_recon_flux_refgeo<16>, pool_ext, team,
+                            out_mode, ax, ay, az, um, up, F, amax, flux_form);
 }
 
 int tf_reconstruct_f64(const double* pool_ext, int64_t pool_slices,

@@ -171,10 +171,17 @@ class TeamPlan:
     """One iteration's teams captured as a CUDA graph (tf_plan)."""
 
     def __init__(self, teams, pool, n, velocity, um, up, F, executors,
-                 amax=None, flux_form=0, overlap=True, team_buffers=False):
+                 amax=None, flux_form=0, overlap=True, team_buffers=False,
+                 geometry="tma"):
         """team_buffers: write each team's outputs into its lease of the
         iteration's packed team buffers (slot = flat slice index in closure
-        order, `self.order`) instead of per-sub-grid slots."""
+        order, `self.order`) instead of per-sub-grid slots.
+        geometry: "tma" — one CTA per slice, the stencil box staged by TMA
+        (the product kernel); "reference" — the reference's blocks_for
+        launch geometry, ceil((n+2)^3/128) CTAs of 128 threads per slice
+        (the strategy-1 baseline)."""
+        if geometry not in ("tma", "reference"):
+            raise ValidationError(f"unknown geometry {geometry!r}")
         self.lib = _lib.load()
         ids = np.concatenate([np.asarray(t.ids, dtype=np.int32)
                               for t in teams]) if teams else \
@@ -198,7 +205,8 @@ class TeamPlan:
             F.data_ptr(), None if amax is None else amax.data_ptr(),
             int(flux_form),
             (_lib.TF_LAUNCH_OVERLAP_PREV if overlap else 0)
-            | (_lib.TF_PLAN_TEAM_BUFFERS if team_buffers else 0),
+            | (_lib.TF_PLAN_TEAM_BUFFERS if team_buffers else 0)
+            | (_lib.TF_PLAN_REFGEO if geometry == "reference" else 0),
             C.byref(h))
         self.order = ids      # flat slice index -> sub-grid id
         _lib.check(rc, "tf_plan_capture_recon_flux")

@@ -64,6 +64,36 @@ def test_team_plan_bit_exact(cuda, cfg2, A, E):
     assert bool((amax == 1.0).all())
 
 
+@pytest.mark.parametrize("n,grid,vel", [(8, 32, (-1.0, 0.5, -0.25)),
+                                        (16, 64, (0.7, -1.3, 0.0)),
+                                        (16, 32, (1.0, 1.0, 1.0))])
+@pytest.mark.parametrize("form", [0, 1])
+def test_reference_geometry_plan_bit_exact(cuda, n, grid, vel, form):
+    """The strategy-1 baseline kernel (the reference's launch geometry:
+    ceil((n+2)^3/128) CTAs of 128 threads per slice, stencil from global
+    memory) is as exact as the TMA kernel, upwind and KT forms."""
+    import torch
+    from paper_2210_06438_b200.strategy3 import TeamPlan, form_teams
+    f = HO.stress_field(grid)
+    hp = HO.make_pool(f, n)
+    HO.exchange_ghosts_pool(hp, n, grid // n)
+    oum, oup, oF = HO.recon_flux_batch(hp, n, vel)
+    if form:
+        oF = HO.flux_kt_batch(oum, oup, vel)
+    pool = torch.from_numpy(hp).to(cuda)
+    S = pool.shape[0]
+    um, up, F = _outs(S, n, cuda)
+    amax = torch.full((S,), float("nan"), dtype=torch.float64, device=cuda)
+    plan = TeamPlan(form_teams(range(S), 1, 2), pool, n, vel, um, up, F, 2,
+                    amax=amax, flux_form=form, geometry="reference")
+    plan.launch()
+    torch.cuda.synchronize()
+    assert np.array_equal(um.cpu().numpy(), oum)
+    assert np.array_equal(up.cpu().numpy(), oup)
+    assert np.array_equal(F.cpu().numpy(), oF)
+    assert bool((amax == max(abs(v) for v in vel)).all())
+
+
 @pytest.mark.parametrize("A,E", [(16, 4), (128, 4)])
 def test_team_plan_team_buffers(cuda, cfg2, A, E):
     """Outputs into the packed team leases: flat slot k holds sub-grid
