@@ -90,6 +90,30 @@ def ncu_traffic_per_launch(team: int,
         return None
 
 
+def ncu_graph_traffic(capture: str = "r02_ncu_plan_graph_A128.csv"):
+    """DRAM bytes (read + write) of ONE timed step: the committed ncu
+    capture of the bench's own A = 128 plan graph replays
+    (--graph-profiling graph --cache-control none: the whole step as one
+    workload, L2 state as the timed loop leaves it), mean over the captured
+    replays.  None if the capture is missing."""
+    import csv
+    path = os.path.join(ROOT, "profiles", capture)
+    try:
+        with open(path) as fh:
+            txt = fh.read()
+        rows = list(csv.reader(txt[txt.index('"ID"'):].splitlines()))
+        hdr = rows[0]
+        idi, mi, vi = (hdr.index("ID"), hdr.index("Metric Name"),
+                       hdr.index("Metric Value"))
+        per = {}
+        for r in rows[1:]:
+            if r[mi] in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+                per[r[idi]] = per.get(r[idi], 0.0) + float(r[vi])
+        return sum(per.values()) / len(per) if per else None
+    except (OSError, ValueError, IndexError):
+        return None
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -765,8 +789,18 @@ def reference_api_legs(args):
                       / (row.ms_per_step * 1e-3),
                       "kernels_per_step": row.kernels,
                       "transfers_per_step": row.transfers,
-                      "measured_raw_allocs": row.measured_raw_allocs}
+                      "measured_raw_allocs": row.measured_raw_allocs,
+                      "host_us_per_iteration": {
+                          k: v / 12 / 1e3 for k, v in
+                          sim.native.host_times().items()}}
     del sim
+    # the same per-task path with two executor streams (strategy 2), and
+    # with aggregation (A = 64: one team per region per iteration)
+    for E, A in ((2, 1), (1, 64)):
+        row, sim, _ = run_cell(8, E, A, steps=3, grid_n=32,
+                               field=sod_field(32, "cuda"))
+        out["config1"][f"E{E}_A{A}_ms_per_step"] = row.ms_per_step
+        del sim
     if not args.no_cpu_baseline:
         from oracle.cpu_baseline import CpuBaseline, cpu_model
         cb = CpuBaseline("sod", 32, N_SUB, VELOCITY, range(64), workers=1,
@@ -1110,6 +1144,8 @@ def main():
     value = rate(total_S, wl.n, ms)
     bytes_step = wl.S * b_alg(wl.n)
     achieved = bytes_step / (ms * 1e-3) / 1e9
+    traffic = ncu_graph_traffic() if (args.mode == "plan"
+                                      and args.max_team == 128) else None
     check = cfg2_output_check(wl, plans, args.outputs == "team") \
         if plans else None
     if check is not None and not check["bitexact_vs_oracle_digest"]:
@@ -1134,15 +1170,19 @@ def main():
         "roofline": {
             "bound": "hbm", "achieved": achieved, "peak": peak,
             "unit": "GB/s", "frac": achieved / peak, "peak_source": peak_src,
-            "traffic": ncu_traffic_per_launch(args.max_team),
-            "alg_bytes_per_launch": b_alg(wl.n) * args.max_team,
+            "traffic": traffic,
+            "traffic_frac": (traffic / (ms * 1e-3) / 1e9 / peak
+                             if traffic else None),
+            "alg_bytes_per_step": bytes_step,
             "per_subgrid_alg_bytes": b_alg(wl.n),
             "note": "achieved = algorithmic bytes of the whole step / step "
                     "time (every launch in the step is the recon+flux team "
-                    "kernel); traffic = dram read+write per team launch from "
-                    "the committed ncu --set full capture of the same kernel "
-                    "(profiles/r01_ncu_recon_flux_single.txt), per slice x "
-                    "team size",
+                    "kernel: 32 launches of 128 slices); traffic = DRAM "
+                    "read+write bytes of one step from the ncu capture of "
+                    "this bench's own plan-graph replays "
+                    "(profiles/r02_ncu_plan_graph_A128.csv, --graph-"
+                    "profiling graph --cache-control none); traffic_frac = "
+                    "traffic / step time / peak",
             # also against the 8 TB/s HBM3e spec figure
             "spec_frac_8tbs": achieved / 8000.0,
             "kernel_alone": {

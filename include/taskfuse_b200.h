@@ -260,6 +260,9 @@ int tf_hydro_region(const tf_hydro* h, int32_t k, tf_region** out);
  * (bucket misses, the reference's count), outstanding leases, buffers
  * materialised (cudaMalloc / cudaHostAlloc calls), device polls           */
 int tf_hydro_counters(const tf_hydro* h, int64_t* out8);
+/* host nanoseconds spent issuing device ops, polling without progress, and
+ * in tf_hydro_iteration altogether (cumulative)                           */
+int tf_hydro_host_times(const tf_hydro* h, int64_t* out3);
 
 /* ---- real-time bulk executor (strategy 3 on real CUDA streams) ---------- */
 

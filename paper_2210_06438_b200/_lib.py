@@ -100,6 +100,7 @@ SIGNATURES = {
     "tf_hydro_iteration": (C.c_int, [_p, _p, _p, _p]),
     "tf_hydro_region": (C.c_int, [_p, _i32, C.POINTER(_p)]),
     "tf_hydro_counters": (C.c_int, [_p, _pi64]),
+    "tf_hydro_host_times": (C.c_int, [_p, _pi64]),
     "tf_executor_create": (C.c_int, [_p, _i32, C.POINTER(_p)]),
     "tf_executor_destroy": (None, [_p]),
     "tf_executor_stream": (_p, [_p, _i32]),

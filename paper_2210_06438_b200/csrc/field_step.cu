@@ -89,13 +89,15 @@ __global__ void __launch_bounds__(THREADS)
   const int s = blockIdx.x;
   const int g = DEV_IDS ? (dev_ids ? dev_ids[s] : s) : team.id[s];
   const int bx = g / (m * m), by = (g / m) % m, bz = g % m;
+  if (threadIdx.x == 0) mbar_init(&bar, 1);
+  // initialised before the arrive: the order compute-sanitizer's racecheck
+  // models (an arrive before the block barrier reads as a RAW hazard)
+  __syncthreads();
   if (threadIdx.x == 0) {
-    mbar_init(&bar, 1);
     mbar_expect_tx(&bar, G::BOX * (uint32_t)sizeof(double));
     // padded coords of the box origin: global (b*n-2, b*n-2, b*n-4)
     tma_load_3d(sbox, &tmap, bz * N, by * N, bx * N, &bar);
   }
-  __syncthreads();
   mbar_wait(&bar, 0);
 
   // Each thread: its owned cells' 6 face fluxes straight from the box, then
@@ -402,12 +404,12 @@ __global__ void __launch_bounds__(cols8_threads<CPT>(), cols8s_min_blocks<CPT>()
   const int g = DEV_IDS ? (dev_ids ? dev_ids[s] : s) : team.id[s];
   const int bx = g / (m * m), by = (g / m) % m, bz = g % m;
   const int sx = ax >= 0.0 ? 0 : 1, sy = ay >= 0.0 ? 0 : 1;
+  if (threadIdx.x == 0) mbar_init(bar, 1);
+  __syncthreads();  // initialised before the arrive (racecheck-clean order)
   if (threadIdx.x == 0) {
-    mbar_init(bar, 1);
     mbar_expect_tx(bar, COLS8_BOX_BYTES);
     tma_load_3d(box, &tmap, bz * N, by * N + sy, bx * N + sx, bar);
   }
-  __syncthreads();
   mbar_wait(bar, 0);
   double* halo = reinterpret_cast<double*>(box + COLS8S_HALO_OFF) +
                  (threadIdx.x >> 5) * 12 * CPT;

@@ -25,6 +25,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <chrono>
 #include <cstring>
 #include <deque>
 #include <map>
@@ -219,6 +220,9 @@ struct tf_hydro {
   std::deque<int32_t> runnable;
   // counters (device.py:168-173 + the bench columns)
   int64_t kernels = 0, copies = 0, bytes = 0, polls = 0;
+  // host nanoseconds in device-op issue (copies, launches, events), in
+  // device polls that found no progress, and whole iterations
+  int64_t ns_issue = 0, ns_idle_poll = 0, ns_iter = 0;
   // per-iteration state
   const double* u = nullptr;
   double* u_next = nullptr;
@@ -226,6 +230,12 @@ struct tf_hydro {
 };
 
 namespace {
+
+int64_t host_ns() {
+  return std::chrono::duration_cast<std::chrono::nanoseconds>(
+             std::chrono::steady_clock::now().time_since_epoch())
+      .count();
+}
 
 int busy_cb(void* ctx, int32_t e) {
   tf_hydro* h = static_cast<tf_hydro*>(ctx);
@@ -371,7 +381,9 @@ int run_task(tf_hydro* h, int32_t ti) {
             if (rc) return rc;
           }
         } else if (arrivals == T) {
+          const int64_t t0 = host_ns();
           rc = issue_step(h, k, t.team, step, s);
+          h->ns_issue += host_ns() - t0;
           if (rc) return rc;
         }
       }
@@ -565,6 +577,7 @@ int tf_hydro_presize(tf_hydro* h) {
 int tf_hydro_iteration(tf_hydro* h, const double* u_pool, double* u_next_pool,
                        tf_stream_t stream) {
   if (!h || !u_pool || !u_next_pool) return TF_E_INVALID;
+  const int64_t t_begin = host_ns();
   h->u = u_pool;
   h->u_next = u_next_pool;
   h->ids_pos = 0;
@@ -592,7 +605,9 @@ int tf_hydro_iteration(tf_hydro* h, const double* u_pool, double* u_next_pool,
       continue;
     }
     int err = 0;
+    const int64_t t0 = host_ns();
     const int progress = poll(h, &err);
+    if (!progress) h->ns_idle_poll += host_ns() - t0;
     if (err) return err;
     if (!progress) {
       bool any = false;
@@ -608,12 +623,21 @@ int tf_hydro_iteration(tf_hydro* h, const double* u_pool, double* u_next_pool,
     rc = cudaEventRecord(h->fork, h->streams[e]);
     if (!rc) rc = cudaStreamWaitEvent((cudaStream_t)stream, h->fork, 0);
   }
+  h->ns_iter += host_ns() - t_begin;
   return rc;
 }
 
 int tf_hydro_region(const tf_hydro* h, int32_t k, tf_region** out) {
   if (!h || k < 0 || k >= kRegions || !out) return TF_E_INVALID;
   *out = h->regions[k];
+  return 0;
+}
+
+int tf_hydro_host_times(const tf_hydro* h, int64_t* out3) {
+  if (!h || !out3) return TF_E_INVALID;
+  out3[0] = h->ns_issue;
+  out3[1] = h->ns_idle_poll;
+  out3[2] = h->ns_iter;
   return 0;
 }
 

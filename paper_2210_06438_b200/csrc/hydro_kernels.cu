@@ -209,14 +209,18 @@ __global__ void __launch_bounds__(THREADS, recon_min_blocks<THREADS>())
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int s = blockIdx.x;
   const int g = DEV_IDS ? (dev_ids ? dev_ids[s] : s) : team.id[s];
+  if (threadIdx.x == 0) mbar_init(&bar, 1);
+  // the barrier is initialised (and the init fenced) before anyone arrives
+  // on it or polls it — also the order compute-sanitizer's racecheck
+  // models: an arrive by the initialising thread before a block barrier is
+  // reported as a warp-level RAW hazard on the mbarrier word
+  __syncthreads();
   if (threadIdx.x == 0) {
-    mbar_init(&bar, 1);
     mbar_expect_tx(&bar, G::BOX * (uint32_t)sizeof(double));
     // box origin = extended index (x,y,z) = (1,1,0) of sub-grid g;
     // coordinates innermost first
     tma_load_box(sbox, &tmap, 0, 1, 1, g, &bar);
   }
-  __syncthreads();  // barrier initialised before anyone polls it
   mbar_wait(&bar, 0);
 
   const int64_t slot = out_mode ? (int64_t)g : (int64_t)s;
@@ -331,12 +335,12 @@ __global__ void __launch_bounds__(THREADS, MINB)
   __shared__ double s_ul[CELLS];  // one axis' left states (KT / a < 0)
   const int s = blockIdx.x;
   const int g = dev_ids ? dev_ids[s] : s;
+  if (threadIdx.x == 0) mbar_init(&bar, 1);
+  __syncthreads();  // initialised before the arrive (see k_recon_flux)
   if (threadIdx.x == 0) {
-    mbar_init(&bar, 1);
     mbar_expect_tx(&bar, G::EXT3 * (uint32_t)sizeof(double));
     tma_load_box(sbox, &tmap, 0, 0, 0, g, &bar);
   }
-  __syncthreads();
   mbar_wait(&bar, 0);
   const int64_t slot = out_mode ? (int64_t)g : (int64_t)s;
   double* um_s = um + slot * 3 * CELLS;
@@ -924,10 +928,10 @@ __global__ void __launch_bounds__(THREADS, recon_min_blocks<THREADS>())
       st_release_sys(&ctl->status, 1);
     }
   };
-  if (threadIdx.x == 0) {
+  if (threadIdx.x == 0)
     for (int d = 0; d < DEPTH; ++d) mbar_init(&bar[d], 1);
-    claim_into(0);
-  }
+  __syncthreads();  // initialised before the first arrive (k_recon_flux)
+  if (threadIdx.x == 0) claim_into(0);
   __syncthreads();
   uint32_t phases = 0;
   for (int i = 0;; ++i) {

@@ -87,6 +87,13 @@ class HydroEngine:
                    "tf_hydro_counters")
         return dict(zip(self.COUNTERS, buf))
 
+    def host_times(self) -> dict:
+        """Cumulative host ns: issuing device ops, idle polling, iterations."""
+        buf = (C.c_int64 * 3)()
+        _lib.check(self.lib.tf_hydro_host_times(self.handle, buf),
+                   "tf_hydro_host_times")
+        return dict(zip(("issue_ns", "idle_poll_ns", "iteration_ns"), buf))
+
     def __del__(self):
         h = getattr(self, "handle", None)
         if h:
