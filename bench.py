@@ -266,7 +266,10 @@ def timed(fn, steps, warmup, world, stream, settle_s: float = 0.02):
     clocks), then EXACTLY `steps` steps between barrier+sync on both sides,
     CUDA events on the launching stream; ms/step (max over ranks)."""
     import torch
-    t_end = time.time() + settle_s
+    # ranks must run the same number of steps (every step may hold a
+    # collective or a peer barrier), so the wall-clock settle applies to
+    # one rank only
+    t_end = time.time() + (settle_s if world == 1 else 0.0)
     k = 0
     while k < warmup or time.time() < t_end:
         fn(k)
@@ -782,8 +785,9 @@ def reference_api_legs(args):
     from paper_2210_06438_b200.bench_matrix import run_cell
     from paper_2210_06438_b200.hydro import sod_field
     out = {}
-    row, sim, _ = run_cell(8, 1, 1, steps=3, grid_n=32,
-                           field=sod_field(32, "cuda"))
+    row1, sim, _ = run_cell(8, 1, 1, steps=3, grid_n=32,
+                            field=sod_field(32, "cuda"))
+    row = row1
     out["config1"] = {"ms_per_step": row.ms_per_step,
                       "cell_updates_per_s": 64 * 512 * 3
                       / (row.ms_per_step * 1e-3),
@@ -815,7 +819,9 @@ def reference_api_legs(args):
             "sample": "all 64 sub-grids x 3 iterations: exchange_ghosts + "
                       "prep/reconstruct/flux/reduce/update bodies (oracle "
                       f"port), best of 5; CPU {cpu_model()}"}
-        out["config1"]["speedup_vs_cpu"] = ms_cpu / row.ms_per_step
+        out["config1"]["speedup_vs_cpu"] = ms_cpu / row1.ms_per_step
+        out["config1"]["speedup_vs_cpu_E2"] = \
+            ms_cpu / out["config1"]["E2_A1_ms_per_step"]
     sweep = {}
     for A in (1, 4, 16, 64, 128):
         row, sim, _ = run_cell(8, 1, A, steps=1, grid_n=GRID,
