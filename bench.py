@@ -753,7 +753,38 @@ def realtime_leg(wl, args, world, stream, peak):
     if not check["bitexact_vs_oracle_digest"]:
         raise SystemExit(f"bench.py: real-time queue outputs differ {check}")
     achieved = wl.S * b_alg(wl.n) / (ms * 1e-3) / 1e9
+    # the same real-time formation with each closed team launched as its
+    # own grid from the device (strategy3.DeviceLaunchExecutor): A sweep
+    from paper_2210_06438_b200.strategy3 import DeviceLaunchExecutor
+    dl = {}
+    for a in (1, 4, 16, 64, 128):
+        ex = DeviceLaunchExecutor("reconstruct", a,
+                                  default_parents(wl.S, a), wl.n)
+
+        def dstep(k, ex=ex):
+            ex.run(wl.pools[k % len(wl.pools)], VELOCITY, arrivals, wl.um,
+                   wl.up, wl.F, amax=wl.amax)
+        dms = timed(dstep, max(5, args.steps // 2), 3, world, stream)
+        ex.wait()
+        dst = ex.stats()
+        dl[a] = {"value": rate(wl.S * world, wl.n, dms), "ms_per_step": dms,
+                 "mean_team": sum(k * v for k, v in
+                                  dst["size_histogram"].items())
+                 / max(1, dst["teams_formed"]),
+                 "hbm_frac": wl.S * b_alg(wl.n) / (dms * 1e-3) / 1e9 / peak}
+        del ex
+    dcheck = None
+    ex = DeviceLaunchExecutor("reconstruct", A, default_parents(wl.S, A),
+                              wl.n)
+    dcheck = cfg2_output_check(
+        wl, rerun=lambda: (ex.run(wl.pools[0], VELOCITY, arrivals, wl.um,
+                                  wl.up, wl.F, amax=wl.amax), ex.wait()))
+    del ex
+    if not dcheck["bitexact_vs_oracle_digest"]:
+        raise SystemExit(f"bench.py: device-launch outputs differ {dcheck}")
     return {"value": rate(wl.S * world, wl.n, ms), "unit": UNIT,
+            "device_launch_sweep": dl,
+            "device_launch_self_check": dcheck["bitexact_vs_oracle_digest"],
             "ms_per_step": ms, "max_team": A,
             "mean_team": sum(k * v for k, v in st["size_histogram"].items())
             / max(1, st["teams_formed"]),

@@ -335,6 +335,27 @@ int tf_queue_consumer_launch(const double* pool_ext, int64_t pool_slices,
                              int32_t flux_form, int64_t timeout_ns,
                              tf_stream_t stream);
 
+/* ---- device-launch executor (strategy 3, teams launched by the GPU) ----- */
+/* The formation core's closed teams are published (ids + end offset) into
+ * mapped pinned memory; a one-CTA launcher kernel, resident for the run,
+ * mirrors them to device memory and launches EACH TEAM as its own grid of
+ * T CTAs from the device (dynamic parallelism, fire-and-forget) — the
+ * reference's one aggregated kernel per team (aggregator.py:157-165)
+ * without a host launch.  busy = published slices not all completed.
+ * The region must have one executor; n = 8.  run() returns once every
+ * arrival is published; the work completes on `stream`.                   */
+typedef struct tf_dlexec tf_dlexec;
+int tf_dlexec_create(tf_region* region, int32_t n, tf_dlexec** out);
+void tf_dlexec_destroy(tf_dlexec* q);
+int tf_dlexec_run_recon_flux(tf_dlexec* q, const double* pool_ext,
+                             int64_t pool_slices, const int32_t* ids,
+                             int64_t count, double ax, double ay, double az,
+                             double* um, double* up, double* F, double* amax,
+                             int32_t flux_form, tf_stream_t stream,
+                             int64_t* teams_published);
+/* Wait for every run in flight; TF_E_TIMEOUT if a launcher gave up.       */
+int tf_dlexec_wait(tf_dlexec* q);
+
 /* ---- captured team plans (CUDA graphs) ----------------------------------- */
 
 typedef struct tf_plan tf_plan;

@@ -18,6 +18,8 @@ CSRC = PKG / "csrc"
 LIB = PKG / "libtaskfuse_b200.so"
 SOURCES = ("hydro_kernels.cu", "aggregator.cpp", "halo.cu", "field_step.cu",
            "hydro_engine.cpp")
+# relocatable device code (device-side kernel launches), device-linked
+RDC_SOURCES = ("device_launch.cu",)
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",
@@ -37,9 +39,9 @@ def _stale() -> bool:
     if not LIB.exists():
         return True
     built = LIB.stat().st_mtime
-    deps = [CSRC / s for s in SOURCES] + [ROOT / "include" / "taskfuse_b200.h",
-                                          CSRC / "sm100_common.cuh",
-                                          CSRC / "tf_nvtx.h"]
+    deps = [CSRC / s for s in SOURCES + RDC_SOURCES] + [
+        ROOT / "include" / "taskfuse_b200.h", CSRC / "sm100_common.cuh",
+        CSRC / "tf_nvtx.h", CSRC / "recon_flux.cuh", CSRC / "internal.h"]
     return any(p.stat().st_mtime > built for p in deps)
 
 
@@ -51,20 +53,33 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     tmp.mkdir(exist_ok=True)
     objs = []
     log = []
-    for src in SOURCES:
+    rdc_objs = []
+    for src in SOURCES + RDC_SOURCES:
         obj = tmp / (src + ".o")
         # TASKFUSE_NVCC_EXTRA: extra -D tuning flags for experiment builds
         extra = os.environ.get("TASKFUSE_NVCC_EXTRA", "").split()
-        cmd = [nvcc(), *NVCC_FLAGS, *extra, "-x", "cu", "-c", str(CSRC / src),
-               "-o", str(obj)]
+        rdc = ["-rdc=true"] if src in RDC_SOURCES else []
+        cmd = [nvcc(), *NVCC_FLAGS, *rdc, *extra, "-x", "cu", "-c",
+               str(CSRC / src), "-o", str(obj)]
         res = subprocess.run(cmd, capture_output=True, text=True)
         log.append(res.stdout + res.stderr)
         if res.returncode != 0:
             raise RuntimeError(f"nvcc failed on {src}:\n{res.stderr}")
         objs.append(str(obj))
+        if rdc:
+            rdc_objs.append(str(obj))
+    gen = ["-gencode", "arch=compute_100a,code=sm_100a"]
+    if rdc_objs:
+        dlink = tmp / "device_link.o"
+        cmd = [nvcc(), *gen, "-dlink", "-Xcompiler", "-fPIC", *rdc_objs,
+               "-o", str(dlink), "-lcudadevrt"]
+        res = subprocess.run(cmd, capture_output=True, text=True)
+        if res.returncode != 0:
+            raise RuntimeError(f"nvcc device link failed:\n{res.stderr}")
+        objs.append(str(dlink))
     out = tmp / LIB.name
-    cmd = [nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared",
-           "-Xcompiler", "-fPIC", *objs, "-o", str(out)]
+    cmd = [nvcc(), *gen, "-shared", "-Xcompiler", "-fPIC", *objs, "-o",
+           str(out), "-lcudadevrt"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError(f"nvcc link failed:\n{res.stderr}")

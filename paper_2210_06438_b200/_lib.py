@@ -143,6 +143,12 @@ SIGNATURES = {
     "tf_field_unpad_host_f64": (C.c_int, [_p, _i32, _i32, _i32, _p, _i32,
                                           _p]),
     "tf_memcpy_async": (C.c_int, [_p, _p, _i64, _p]),
+    "tf_dlexec_create": (C.c_int, [_p, _i32, C.POINTER(_p)]),
+    "tf_dlexec_destroy": (None, [_p]),
+    "tf_dlexec_run_recon_flux": (C.c_int, [_p, _p, _i64, _pi32, _i64, _f64,
+                                           _f64, _f64, _p, _p, _p, _p, _i32,
+                                           _p, _pi64]),
+    "tf_dlexec_wait": (C.c_int, [_p]),
     "tf_qexec_create": (C.c_int, [_p, _i32, C.POINTER(_p)]),
     "tf_qexec_destroy": (None, [_p]),
     "tf_qexec_run_recon_flux": (C.c_int, [_p, _p, _i64, _pi32, _i64, _f64,

@@ -333,6 +333,59 @@ class QueueExecutor:
             self.handle = None
 
 
+class DeviceLaunchExecutor:
+    """Strategy 3 with DEVICE-side team launches (tf_dlexec): the formation
+    core's closed teams are published to a one-CTA launcher kernel that
+    launches each team as its own T-CTA grid of the fused kernel from the
+    GPU (dynamic parallelism) — one aggregated kernel per team as in the
+    reference (aggregator.py:157-165), with no host launch per team."""
+
+    def __init__(self, name: str, max_team: int, parents: int, n: int = 8):
+        if n != 8:
+            raise ValidationError("the device-launch executor supports n = 8")
+        self.core = FormationCore(name, max_team, parents, 1)
+        self.lib = self.core.lib
+        h = C.c_void_p()
+        _lib.check(self.lib.tf_dlexec_create(self.core.handle, n, C.byref(h)),
+                   "tf_dlexec_create")
+        self.handle = h
+        self.n = n
+        self.runs = 0
+
+    def run(self, pool, velocity, ids, um, up, F, amax=None, flux_form=0,
+            stream=None) -> int:
+        """Publish the arrivals; returns teams published.  The launcher and
+        its team grids complete on `stream` (default: the current one)."""
+        arr = np.ascontiguousarray(np.asarray(ids, dtype=np.int32))
+        S = _check_recon_args(pool, self.n, um, up, F, amax)
+        if arr.size and (arr.min() < 0 or arr.max() >= S):
+            raise ValidationError("arrival id outside the pool")
+        s = stream if stream is not None else torch.cuda.current_stream()
+        teams = C.c_int64()
+        ax, ay, az = (float(v) for v in velocity)
+        self._keep = arr
+        _lib.check(self.lib.tf_dlexec_run_recon_flux(
+            self.handle, pool.data_ptr(), S,
+            arr.ctypes.data_as(C.POINTER(C.c_int32)), arr.size, ax, ay, az,
+            um.data_ptr(), up.data_ptr(), F.data_ptr(),
+            None if amax is None else amax.data_ptr(), int(flux_form),
+            s.cuda_stream, C.byref(teams)), "tf_dlexec_run_recon_flux")
+        self.runs += 1
+        return teams.value
+
+    def wait(self) -> None:
+        _lib.check(self.lib.tf_dlexec_wait(self.handle), "tf_dlexec_wait")
+
+    def stats(self) -> dict:
+        return self.core.stats()
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h:
+            self.lib.tf_dlexec_destroy(h)
+            self.handle = None
+
+
 class AggregatedIteration:
     """One device-resident hydro iteration with strategy-3 team launches:
     ghost fill -> reconstruct+flux (captured team plan) -> update -> swap.

@@ -310,3 +310,28 @@ def test_queue_consumer_gives_the_gpu_back_when_nothing_arrives(cuda):
     torch.cuda.synchronize()
     assert time.time() - t0 < 5.0
     assert int(ctl_h[2]) == 0           # nothing completed
+
+
+@pytest.mark.parametrize("A", [1, 16, 128])
+def test_device_launch_executor_bit_exact(cuda, cfg2, A):
+    """Teams formed in real time, each launched as its own grid FROM THE
+    DEVICE (tf_dlexec): every slice of config 2 equals the oracle, on
+    back-to-back runs, and every arrival lands in exactly one team."""
+    import torch
+    from paper_2210_06438_b200.strategy3 import (DeviceLaunchExecutor,
+                                                 default_parents)
+    pool, n, vel, oum, oup, oF = cfg2
+    S = pool.shape[0]
+    ex = DeviceLaunchExecutor("reconstruct", A, default_parents(S, A), n)
+    amax = torch.full((S,), float("nan"), dtype=torch.float64, device=cuda)
+    for _ in range(2):
+        um, up, F = _outs(S, n, cuda)
+        ex.run(pool, vel, np.arange(S, dtype=np.int32), um, up, F, amax=amax)
+        ex.wait()
+        assert np.array_equal(F.cpu().numpy(), oF)
+        assert np.array_equal(um.cpu().numpy(), oum)
+        assert np.array_equal(up.cpu().numpy(), oup)
+    assert bool((amax == 1.0).all())
+    st = ex.stats()
+    assert sum(k * v for k, v in st["size_histogram"].items()) == 2 * S
+    assert max(st["size_histogram"]) <= A
