@@ -67,16 +67,25 @@ __device__ __forceinline__ unsigned long long dl_clock() {
 }
 
 // One team = one grid of T CTAs (launched from the device).
+// The tensor map lives in global memory (written by the host before the
+// run): a device-side launch's parameter buffer does not guarantee the
+// 64-byte alignment a TMA descriptor needs (cudaErrorMisalignedAddress).
 template <int N>
 __global__ void __launch_bounds__(kThreads, recon_min_blocks<kThreads>())
-    k_team_child(const __grid_constant__ CUtensorMap tmap,
+    k_team_child(const CUtensorMap* __restrict__ tmap,
                  const int32_t* __restrict__ ids, double ax, double ay,
                  double az, double* __restrict__ um, double* __restrict__ up,
                  double* __restrict__ F, double* __restrict__ amax,
                  int flux_form, unsigned long long* done) {
+  // relocatable device code does not place the dynamic shared memory on a
+  // 128-byte boundary (the TMA destination rule): the launch carries 128
+  // spare bytes and the box starts at the next boundary
+  extern __shared__ __align__(16) unsigned char dyn[];
+  double* sbox = reinterpret_cast<double*>(
+      (reinterpret_cast<uintptr_t>(dyn) + 127) & ~uintptr_t(127));
   const int g = ids[blockIdx.x];
-  recon_flux_cta<N, kThreads, 0>(&tmap, g, (int64_t)g, ax, ay, az, um, up, F,
-                                 amax, flux_form);
+  recon_flux_cta<N, kThreads, 0>(sbox, tmap, g, (int64_t)g, ax, ay, az, um, up,
+                                 F, amax, flux_form);
   __syncthreads();
   // completion is the host's busy hint only: no fence (the parent grid's
   // completion orders the outputs for the stream)
@@ -85,8 +94,7 @@ __global__ void __launch_bounds__(kThreads, recon_min_blocks<kThreads>())
 
 template <int N>
 __global__ void __launch_bounds__(kLauncher)
-    k_team_launcher(const __grid_constant__ CUtensorMap tmap,
-                    const int* __restrict__ ring_h,
+    k_team_launcher(const CUtensorMap* tmap, const int* __restrict__ ring_h,
                     const long long* __restrict__ ends_h, DlCtl* ctl,
                     int32_t* __restrict__ ids_d, unsigned long long* done,
                     double ax, double ay, double az, double* um, double* up,
@@ -95,7 +103,7 @@ __global__ void __launch_bounds__(kLauncher)
   __shared__ long long s_teams, s_fin;
   __shared__ long long s_end[kTeamsPerRound];
   __shared__ int s_stop;
-  constexpr size_t smem = Geo<N>::BOX * sizeof(double);
+  constexpr size_t smem = Geo<N>::BOX * sizeof(double) + 128;
   const int t = threadIdx.x;
   if (t == 0) *done = 0;  // this slot's counter; no child of the run yet
   long long seen = 0, mirrored = 0, reported = -1;
@@ -121,16 +129,16 @@ __global__ void __launch_bounds__(kLauncher)
         ids_d[k] = dl_ld_sys32(ring_h + k);
       __threadfence();
       __syncthreads();  // every id of these teams is in device memory
-      if (t == 0) {
-        long long start = mirrored;
-        for (long long j = seen; j < tp; ++j) {
-          const long long e = s_end[j - seen];
-          k_team_child<N><<<(unsigned)(e - start), kThreads, smem,
-                            cudaStreamFireAndForget>>>(
-              tmap, ids_d + start, ax, ay, az, um, up, F, amax, flux_form,
-              done);
-          start = e;
-        }
+      // one launching thread per new team: device-side launches from
+      // different threads proceed in parallel (one thread issuing them
+      // all serialised them at ~8 us each)
+      if (t < tp - seen) {
+        const long long start = t == 0 ? mirrored : s_end[t - 1];
+        const long long e = s_end[t];
+        k_team_child<N><<<(unsigned)(e - start), kThreads, smem,
+                          cudaStreamFireAndForget>>>(
+            tmap, ids_d + start, ax, ay, az, um, up, F, amax, flux_form,
+            done);
       }
       mirrored = end;
       seen = tp;
@@ -174,6 +182,8 @@ __global__ void __launch_bounds__(kLauncher)
 }
 
 struct DlSlot {
+  CUtensorMap* map_h = nullptr;  // pinned staging of the pool's map
+  CUtensorMap* map_d = nullptr;  // the copy the team grids read
   DlCtl* ctl_h = nullptr;
   void* ctl_d = nullptr;
   int32_t* ring_h = nullptr;
@@ -251,7 +261,7 @@ int tf_dlexec_create(tf_region* region, int32_t n, tf_dlexec** out) {
   if (lim != cudaSuccess) return lim;
   static const cudaError_t attr = cudaFuncSetAttribute(
       k_team_child<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-      (int)(Geo<8>::BOX * sizeof(double)));
+      (int)(Geo<8>::BOX * sizeof(double) + 128));
   if (attr != cudaSuccess) return attr;
   tf_dlexec* q = new tf_dlexec();
   q->region = region;
@@ -267,6 +277,11 @@ int tf_dlexec_create(tf_region* region, int32_t n, tf_dlexec** out) {
                      sizeof(unsigned long long));
     if (e == cudaSuccess)
       e = cudaEventCreateWithFlags(&S.done_ev, cudaEventDisableTiming);
+    if (e == cudaSuccess)
+      e = cudaHostAlloc(reinterpret_cast<void**>(&S.map_h),
+                        sizeof(CUtensorMap), 0);
+    if (e == cudaSuccess)
+      e = cudaMalloc(reinterpret_cast<void**>(&S.map_d), sizeof(CUtensorMap));
   }
   if (e != cudaSuccess) {
     tf_dlexec_destroy(q);
@@ -284,6 +299,8 @@ void tf_dlexec_destroy(tf_dlexec* q) {
     if (S.ctl_h) cudaFreeHost(S.ctl_h);
     if (S.done_d) cudaFree(S.done_d);
     if (S.done_ev) cudaEventDestroy(S.done_ev);
+    if (S.map_h) cudaFreeHost(S.map_h);
+    if (S.map_d) cudaFree(S.map_d);
   }
   delete q;
 }
@@ -344,8 +361,12 @@ int tf_dlexec_run_recon_flux(tf_dlexec* q, const double* pool_ext,
   S.ctl_h->status = 0;
   __atomic_thread_fence(__ATOMIC_SEQ_CST);
   cudaStream_t st = (cudaStream_t)stream;
+  *S.map_h = map;  // the slot's previous run is complete: safe to rewrite
+  cudaError_t me = cudaMemcpyAsync(S.map_d, S.map_h, sizeof(CUtensorMap),
+                                   cudaMemcpyHostToDevice, st);
+  if (me != cudaSuccess) return me;
   k_team_launcher<8><<<1, kLauncher, 0, st>>>(
-      map, S.ring_hd, S.ends_hd, static_cast<DlCtl*>(S.ctl_d), S.ids_d,
+      S.map_d, S.ring_hd, S.ends_hd, static_cast<DlCtl*>(S.ctl_d), S.ids_d,
       S.done_d, ax, ay, az, um, up, F, amax, flux_form,
       /*timeout_ns=*/2000000000LL);
   cudaError_t ce = cudaGetLastError();

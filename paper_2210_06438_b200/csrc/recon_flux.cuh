@@ -170,14 +170,15 @@ constexpr int recon_min_blocks() {
 
 // One CTA's share of a team: stage slice g's stencil box with one TMA load,
 // then reconstruct (+ flux for MODE 0) into output slot `slot`.
+// `sbox`: the CTA's BOX doubles of shared memory, 128-byte aligned (the
+// TMA destination rule).
 template <int N, int THREADS, int MODE>
 __device__ __forceinline__ void recon_flux_cta(
-    const CUtensorMap* tmap, int g, int64_t slot, double ax, double ay,
-    double az, double* __restrict__ um, double* __restrict__ up,
+    double* sbox, const CUtensorMap* tmap, int g, int64_t slot, double ax,
+    double ay, double az, double* __restrict__ um, double* __restrict__ up,
     double* __restrict__ F, double* __restrict__ amax, int flux_form) {
   using G = Geo<N>;
   constexpr int CELLS = G::CELLS;
-  extern __shared__ __align__(128) double sbox[];
   __shared__ __align__(8) uint64_t bar;
   __shared__ double red[THREADS / 32];
   if (threadIdx.x == 0) mbar_init(&bar, 1);
@@ -213,10 +214,11 @@ __global__ void __launch_bounds__(THREADS, recon_min_blocks<THREADS>())
   // let a programmatically-dependent next team launch as soon as every CTA
   // of this one is resident (no-op unless the next launch opted in)
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  extern __shared__ __align__(128) double sbox[];
   const int s = blockIdx.x;
   const int g = DEV_IDS ? (dev_ids ? dev_ids[s] : s) : team.id[s];
-  recon_flux_cta<N, THREADS, MODE>(&tmap, g, out_mode ? (int64_t)g : s, ax,
-                                   ay, az, um, up, F, amax, flux_form);
+  recon_flux_cta<N, THREADS, MODE>(sbox, &tmap, g, out_mode ? (int64_t)g : s,
+                                   ax, ay, az, um, up, F, amax, flux_form);
 }
 
 }  // namespace
