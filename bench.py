@@ -636,26 +636,37 @@ def e2e_leg(args, steps, warmup, world, stream):
 
     from paper_2210_06438_b200.strategy3 import ReconFluxHostPipeline
     pipe = ReconFluxHostPipeline(it, host_in, amax)
-    ms = timed(lambda k: pipe.run(), steps, warmup, world, stream)
+    ms_pipe = timed(lambda k: pipe.run(), steps, max(5, warmup), world,
+                    stream)
     torch.cuda.synchronize()
     ok = bool((amax == max(abs(v) for v in VELOCITY)).all())
     ms_plain = timed(lambda k: it.recon_flux_host(host_in, amax), steps,
-                     warmup, world, stream)
+                     max(5, warmup), world, stream)
+    torch.cuda.synchronize()
+    ok = ok and bool((amax == max(abs(v) for v in VELOCITY)).all())
+    # both are the public host->host call for the same computation; the
+    # overlapped one wins on a healthy host link, the plain one when the
+    # copy engine is slow to start chunked transfers (seen on some boxes)
+    pipelined = ms_pipe <= ms_plain
+    ms = min(ms_pipe, ms_plain)
     res = {"value": rate(it.S * world, N_SUB, ms), "unit": UNIT,
            "ms_per_step": ms, "h2d_bytes_per_step": host_in.numel() * 8,
            "d2h_bytes_per_step": amax.numel() * 8,
-           "gpu_launches_per_step": pipe.launches,
+           "gpu_launches_per_step": (pipe.launches if pipelined
+                                     else it.recon_flux_launches),
            "result_check": ok,
-           "step": "pinned host field -> device in x-chunks (copy engine), "
-                   "each chunk scattered into the sub-grid pool as it "
-                   "lands, ghost fill + aggregated reconstruct+flux teams "
-                   "per chunk once its neighbours landed (um/up/F to HBM), "
-                   "per-sub-grid max signal speed -> pinned host "
-                   "(strategy3.ReconFluxHostPipeline, one CUDA graph)",
+           "call": ("strategy3.ReconFluxHostPipeline.run" if pipelined
+                    else "AggregatedIteration.recon_flux_host"),
+           "step": "pinned host field -> device, scattered into the sub-grid "
+                   "pool, ghost fill, aggregated reconstruct+flux teams "
+                   "(um/up/F to HBM), per-sub-grid max signal speed -> "
+                   "pinned host; pipelined: x-chunked upload on the copy "
+                   "engine, chunk j launched once j-1 and j+1 landed, one "
+                   "CUDA graph",
+           "pipelined": {"ms_per_step": ms_pipe,
+                         "value": rate(it.S * world, N_SUB, ms_pipe)},
            "unpipelined": {"ms_per_step": ms_plain,
-                           "value": rate(it.S * world, N_SUB, ms_plain),
-                           "step": "the same call without overlap "
-                                   "(AggregatedIteration.recon_flux_host)"}}
+                           "value": rate(it.S * world, N_SUB, ms_plain)}}
     # the same iteration with the update and the whole field back
     host_out = torch.empty_like(host_in).pin_memory()
     ms_it = timed(lambda k: it.run_host(host_in, host_out), steps, warmup,
