@@ -734,17 +734,23 @@ __global__ void __launch_bounds__(THREADS, recon_min_blocks<THREADS>())
       st_release_sys(&ctl->status, 1);
     }
   };
-  if (threadIdx.x == 0)
+  // the service thread claims slices, issues the box loads and counts
+  // completions: the LAST thread, which the z-pair split leaves idle at
+  // n = 8 (500 pairs over 512 threads), so the next slice's claim and box
+  // load overlap the compute instead of delaying warp 0's share of it
+  constexpr int kSvc = THREADS - 1;
+  const bool svc = threadIdx.x == kSvc;
+  if (svc)
     for (int d = 0; d < DEPTH; ++d) mbar_init(&bar[d], 1);
   __syncthreads();  // initialised before the first arrive (k_recon_flux)
-  if (threadIdx.x == 0) claim_into(0);
+  if (svc) claim_into(0);
   __syncthreads();
   uint32_t phases = 0;
   for (int i = 0;; ++i) {
     const int d = DEPTH == 1 ? 0 : i % DEPTH;
     const int g = s_g[d];
     if (g < 0) break;
-    if (DEPTH > 1 && threadIdx.x == 0) claim_into((i + 1) % DEPTH);
+    if (DEPTH > 1 && svc) claim_into((i + 1) % DEPTH);
     mbar_wait(&bar[d], (phases >> d) & 1u);
     phases ^= 1u << d;
     const double speed = slice_compute<N, THREADS, 0, true>(
@@ -756,7 +762,7 @@ __global__ void __launch_bounds__(THREADS, recon_min_blocks<THREADS>())
     // the completion count is the host's busy signal only (the kernel's
     // exit orders the outputs for the stream), so no fence before it: a
     // fence here held the CTA until its stores drained (-5 us per run)
-    if (threadIdx.x == 0) {
+    if (svc) {
       atomicAdd(&qd->done, 1ULL);
       if (DEPTH == 1) claim_into(0);
     }
