@@ -90,6 +90,23 @@ def ncu_traffic_per_launch(team: int,
         return None
 
 
+def ncu_kernel_traffic(capture: str):
+    """DRAM bytes (read + write) of one whole launch from a committed
+    scripts/ncu_stalls.py text capture (None if missing)."""
+    path = os.path.join(ROOT, "profiles", capture)
+    try:
+        vals = {}
+        with open(path) as fh:
+            for line in fh:
+                parts = line.split()
+                if len(parts) >= 2 and parts[0] in ("dram__bytes_read.sum",
+                                                    "dram__bytes_write.sum"):
+                    vals[parts[0]] = float(parts[1])
+        return vals["dram__bytes_read.sum"] + vals["dram__bytes_write.sum"]
+    except (OSError, KeyError, ValueError):
+        return None
+
+
 def ncu_graph_traffic(capture: str = "r02_ncu_plan_graph_A128.csv"):
     """DRAM bytes (read + write) of ONE timed step: the committed ncu
     capture of the bench's own A = 128 plan graph replays
@@ -989,7 +1006,23 @@ def cfg5_leg(args, world, rank, local, peak):
     torch.cuda.empty_cache()
     ms_peer = None
     clk = None
+    ms_cols = None
     if use_peer:
+        # the per-sub-grid kernel (one CTA per 8^3 sub-grid + halo kernels)
+        # on the same peer path, for the record
+        cols = PeerSlabFieldIteration(part, slab, VELOCITY, device=dev,
+                                      kernel="cols")
+        got = first_iteration(cols, cols.iteration)
+        cols.check()
+        checks["peer_per_subgrid_vs_nccl_ring"] = all_true(
+            world, torch.equal(got, ref))
+        del got
+        ms_cols = timed(lambda k: cols.iteration(), args.steps, args.warmup,
+                        world, stream)
+        cols.check()
+        del cols
+        torch.cuda.empty_cache()
+        # headline: the whole-slab march kernel (csrc/field_march.cu)
         peer = PeerSlabFieldIteration(part, slab, VELOCITY, device=dev)
         got = first_iteration(peer, peer.iteration)
         peer.check()
@@ -1042,20 +1075,23 @@ def cfg5_leg(args, world, rank, local, peak):
     value = rate(S_total, n, ms)
     bytes_alg = part.subgrids * b_alg(n)
     unique = part.subgrids * 16 * n ** 3    # field in + out, 16 B per cell
-    # per iteration: 2 halo kernels + the step (+ the peer barrier, or a
-    # second step launch for the boundary layers on the NCCL path; NCCL's
-    # own kernels are not counted)
-    launches = 4
+    # per iteration, peer path: the march kernel + the peer barrier; NCCL
+    # path: 2 halo kernels + 2 step launches (interior, boundary layers;
+    # NCCL's own kernels not counted)
+    launches = 2 if use_peer else 4
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic",
         "config": cfg5_config(world, grid),
-        "run": {"path": ("peer-fused: the step kernel stores the slab's "
-                         "boundary layers into the ring neighbours' next "
-                         "fields over CUDA-IPC peer memory, then a device "
-                         "peer barrier" if use_peer else
+        "run": {"path": ("peer-fused: ONE march kernel per iteration "
+                         "(warp columns marching x through TMA plane boxes, "
+                         "csrc/field_march.cu) stores the slab's boundary "
+                         "layers into the ring neighbours' next fields over "
+                         "CUDA-IPC peer memory and the next field's y/z "
+                         "halos, then a device peer barrier"
+                         if use_peer else
                          "NCCL ring exchange of the halo planes, interior "
                          "layers stepped while they are in flight "
                          "(no peer access between the GPUs)"),
@@ -1066,6 +1102,10 @@ def cfg5_leg(args, world, rank, local, peak):
                                  else None)},
         "self_check": checks,
         "gpu_launches": launches * args.steps,
+        "per_subgrid_kernel_path": None if ms_cols is None else {
+            "ms_per_step": ms_cols, "value": rate(S_total, n, ms_cols),
+            "step": "the same peer path with one CTA per 8^3 sub-grid "
+                    "(k_step_cols8s) + the y/z halo kernels"},
         "nccl_exchange_path": {
             "ms_per_step": ms_nccl, "value": rate(S_total, n, ms_nccl),
             "step": "fused step + separate NCCL ring exchange of the halo "
@@ -1074,10 +1114,10 @@ def cfg5_leg(args, world, rank, local, peak):
             "bound": "hbm", "unit": "GB/s", "peak": peak,
             "achieved": unique / (ms * 1e-3) / 1e9,
             "frac": unique / (ms * 1e-3) / 1e9 / peak,
-            "traffic": ncu_traffic_per_launch(
-                part.subgrids, "r01_ncu_step_fused_cfg5g256.txt"),
+            "traffic": (ncu_kernel_traffic("r02_ncu_march_cfg5.txt")
+                        if use_peer and world == 1 and grid == 512 else None),
             "per_subgrid_alg_bytes": 16 * n ** 3,
-            "note": "fused step; algorithmic bytes = the field read once "
+            "note": "march kernel; algorithmic bytes = the field read once "
                     "and written once, 16 B per cell (8 KB per 8^3 "
                     "sub-grid): every halo re-read is served by L2 in the "
                     "padded-field layout (DESIGN.md §4), so this is the "

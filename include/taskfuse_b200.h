@@ -443,6 +443,28 @@ int tf_field_step_peer_f64(const double* padded_in, int32_t X, int32_t Gy,
                            int32_t T, double ax, double ay, double az,
                            double dt_dx, double* padded_out, double* peer_lo,
                            double* peer_hi, tf_stream_t stream);
+/* The fused iteration over the WHOLE slab in one launch (every sub-grid of
+ * the (X/n, Gy/n, Gz/n) lattice; what tf_field_step_f64 / _peer_f64 do with
+ * ids == NULL and T = S), tiled by warp columns instead of sub-grids: a
+ * warp marches R (8, or 4 with TF_MARCH_ROWS4) y rows x 32 z cells through
+ * xc x planes (0 = 16) of the field, one TMA plane box at a time
+ * (csrc/field_march.cu).  Same arithmetic, bit-identical.  Needs
+ * Gy % R == 0 and Gz % 32 == 0.  flags: TF_STEP_HALO_YZ (also write the
+ * next field's periodic y/z halos), TF_STEP_HALO_X (also its periodic x
+ * halo: one GPU; peer_lo/peer_hi must then be NULL), TF_MARCH_ROWS4.
+ * peer_lo / peer_hi: as tf_field_step_peer_f64 (the ring neighbours' next
+ * fields, or NULL).  work: two zeroed uint32 counters private to this
+ * launch's stream order (the kernel claims work items from them and leaves
+ * them zeroed), or NULL for a static round-robin split.  Replaces the
+ * per-sub-grid loop of advect_once / HydroSim's iteration over a whole
+ * rank (reference.py:28-52, step.py:125-143) plus exchange_ghosts
+ * (scenario.py:124-142) for the x halos.                                   */
+#define TF_MARCH_ROWS4 16
+int tf_field_march_f64(const double* padded_in, int32_t X, int32_t Gy,
+                       int32_t Gz, double ax, double ay, double az,
+                       double dt_dx, double* padded_out, double* peer_lo,
+                       double* peer_hi, int32_t flags, int32_t xc,
+                       uint32_t* work, tf_stream_t stream);
 int tf_peer_barrier(long long* my_flags, long long* left_flags,
                     long long* right_flags, long long epoch,
                     long long timeout_ns, int* err, tf_stream_t stream);

@@ -17,7 +17,7 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libtaskfuse_b200.so"
 SOURCES = ("hydro_kernels.cu", "aggregator.cpp", "halo.cu", "field_step.cu",
-           "hydro_engine.cpp")
+           "field_march.cu", "hydro_engine.cpp")
 # relocatable device code (device-side kernel launches), device-linked
 RDC_SOURCES = ("device_launch.cu",)
 NVCC_FLAGS = [

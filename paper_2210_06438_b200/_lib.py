@@ -31,6 +31,7 @@ TF_PLAN_TEAM_BUFFERS = 2
 TF_PLAN_REFGEO = 16
 TF_STEP_HALO_YZ = 4
 TF_STEP_HALO_X = 8
+TF_MARCH_ROWS4 = 16
 
 
 class EnterResult(C.Structure):
@@ -132,6 +133,8 @@ SIGNATURES = {
     "tf_field_step_peer_f64": (C.c_int, [_p, _i32, _i32, _i32, _i32, _p, _i32,
                                          _f64, _f64, _f64, _f64, _p, _p, _p,
                                          _p]),
+    "tf_field_march_f64": (C.c_int, [_p, _i32, _i32, _i32, _f64, _f64, _f64,
+                                     _f64, _p, _p, _p, _i32, _i32, _p, _p]),
     "tf_peer_barrier": (C.c_int, [_p, _p, _p, _i64, _i64, _p, _p]),
     "tf_field_halo_layers_f64": (C.c_int, [_p, _i32, _i32, _i32, _i32, _i32,
                                            _p]),

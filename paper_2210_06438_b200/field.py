@@ -109,6 +109,32 @@ class _FieldBase:
             self.dt_dx, nxt.data_ptr(), 0, self._s(stream)),
             "tf_field_step_f64")
 
+    def march_ok(self) -> bool:
+        """The whole-slab march kernel tiles the field by 8-row x 32-cell
+        warp columns (csrc/field_march.cu)."""
+        return self.G % 32 == 0
+
+    def march(self, flags: int = 0, peer_lo: int | None = None,
+              peer_hi: int | None = None, xc: int = 0, stream=None) -> None:
+        """One fused iteration over EVERY sub-grid of the field in one launch
+        (tf_field_march_f64): current -> next padded field.  flags:
+        TF_STEP_HALO_YZ / TF_STEP_HALO_X (also write the next field's
+        periodic halos), TF_MARCH_ROWS4; peer_lo / peer_hi: device pointers
+        of the ring neighbours' next fields (their x halos)."""
+        cur, nxt = self.P[self.cur], self.P[1 - self.cur]
+        ax, ay, az = self.velocity
+        work = getattr(self, "_march_work", None)
+        if work is None:
+            # the launch's item counters (the kernel leaves them zeroed);
+            # one pair per object: concurrent iterations must not share
+            work = self._march_work = torch.zeros(
+                2, dtype=torch.int32, device=self.device)
+        _lib.check(self.lib.tf_field_march_f64(
+            cur.data_ptr(), self.X, self.G, self.G, ax, ay, az, self.dt_dx,
+            nxt.data_ptr(), peer_lo, peer_hi, flags, xc,
+            work.data_ptr() if getattr(self, "march_dynamic", True) else None,
+            self._s(stream)), "tf_field_march_f64")
+
     def swap(self) -> None:
         self.cur = 1 - self.cur
 
@@ -318,6 +344,36 @@ class FieldIteration(_FieldBase):
         return launches
 
 
+class MarchFieldIteration(_FieldBase):
+    """One-GPU fused iteration of the whole field in ONE launch per step:
+    the march kernel (csrc/field_march.cu) also writes the next field's
+    periodic y/z and x halos, so after the first step no halo kernel runs.
+    The config-5 iteration at N = 1 (one team = every sub-grid)."""
+
+    def __init__(self, grid_n: int, n: int = 8, velocity=(1.0, 1.0, 1.0),
+                 dt_dx=None, device=None, xc: int = 0, rows4: bool = False):
+        super().__init__(grid_n, grid_n, n, velocity, dt_dx, device)
+        if not self.march_ok():
+            raise ValidationError("the march kernel needs grid_n % 32 == 0")
+        self.xc = xc
+        self.flags = _lib.TF_STEP_HALO_YZ | _lib.TF_STEP_HALO_X | \
+            (_lib.TF_MARCH_ROWS4 if rows4 else 0)
+        self.halo_fresh = False
+
+    def load(self, field_dev: torch.Tensor, stream=None) -> None:
+        super().load(field_dev, stream)
+        self.halo_fresh = False
+
+    def step(self, stream=None) -> None:
+        if not self.halo_fresh:
+            self.halo(True, stream)
+        self.march(self.flags, xc=self.xc, stream=stream)
+        self.swap()
+        self.halo_fresh = True
+
+    launches_per_step = 1
+
+
 class HostPipeline:
     """`FieldIteration.run_host_pipelined` for FIXED pinned host buffers,
     captured once as a CUDA graph (copies, per-chunk kernels and the
@@ -361,10 +417,20 @@ class PeerSlabFieldIteration(_FieldBase):
 
     def __init__(self, part: SlabPartition, slab_field=None,
                  velocity=(1.0, 1.0, 1.0), dt_dx=None, device=None,
-                 group=None, timeout_s: float = 10.0):
+                 group=None, timeout_s: float = 10.0, kernel: str = "auto",
+                 xc: int = 0):
         super().__init__(part.mx * part.n, part.grid_n, part.n, velocity,
                          dt_dx, device)
         self.part = part
+        # "march": the whole-slab march kernel (also writes the next
+        # field's y/z halos: no halo kernel per iteration); "cols": one CTA
+        # per sub-grid (k_step_cols8s) + the halo kernels
+        if kernel == "auto":
+            kernel = "march" if self.march_ok() else "cols"
+        if kernel not in ("march", "cols") or \
+                (kernel == "march" and not self.march_ok()):
+            raise ValidationError(f"kernel {kernel!r} not usable here")
+        self.kernel, self.xc = kernel, xc
         self.timeout_ns = int(timeout_s * 1e9)
         dev = self.device
         self.flags = torch.zeros(2, dtype=torch.int64, device=dev)
@@ -415,6 +481,15 @@ class PeerSlabFieldIteration(_FieldBase):
 
     def iteration(self) -> None:
         cur, nxt = self.cur, 1 - self.cur
+        if self.kernel == "march":
+            # y/z halos of the current field: written by the previous
+            # iteration's kernel (or _prime); the x halo by the neighbours
+            self.march(_lib.TF_STEP_HALO_YZ,
+                       self.left["P"][nxt].data_ptr(),
+                       self.right["P"][nxt].data_ptr(), self.xc)
+            self._barrier()
+            self.swap()
+            return
         self.halo(False)          # y/z halos incl. the received x layers
         ax, ay, az = self.velocity
         _lib.check(self.lib.tf_field_step_peer_f64(

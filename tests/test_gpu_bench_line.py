@@ -63,5 +63,5 @@ def test_bench_two_ranks_config5_gloo(cuda):
     assert d["n_gpus"] == 2 and d["scaling"] == "strong"
     assert d["config"]["workload"].startswith("config 5")
     assert d["run"]["halo_bytes_per_rank_per_step"] > 0
-    assert all(d["self_check"].values()) and len(d["self_check"]) == 2
+    assert all(d["self_check"].values()) and len(d["self_check"]) == 3
     assert d["value"] > 0 and d["e2e"]["value"] > 0

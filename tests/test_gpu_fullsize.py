@@ -42,13 +42,16 @@ def cfg5():
     return f, HO.advect_once(f, VEL)
 
 
-def test_cfg5_peer_fused_step_whole_grid(cuda, cfg5):
+@pytest.mark.parametrize("kernel", ["march", "cols"])
+def test_cfg5_peer_fused_step_whole_grid(cuda, cfg5, kernel):
+    """The bench's config-5 iteration: the whole-slab march kernel (the
+    headline) and the one-CTA-per-sub-grid kernel."""
     import torch
     from paper_2210_06438_b200.field import PeerSlabFieldIteration
     from paper_2210_06438_b200.parallel_halo import SlabPartition
     f, want = cfg5
     r = PeerSlabFieldIteration(SlabPartition(512, 8, 1, 0), f, VEL,
-                               device=cuda)
+                               device=cuda, kernel=kernel)
     r.iteration()
     torch.cuda.synchronize()
     r.check()

@@ -1,0 +1,123 @@
+"""The whole-slab march kernel (tf_field_march_f64, csrc/field_march.cu):
+one launch per iteration over every sub-grid, warps marching x through
+plane boxes, the next field's periodic halos written by the kernel itself.
+Bit-identical to the reference's whole-grid integrator (reference.py:24-48
+via the oracle's advect_once / reference_step) for every velocity sign
+pattern, both column heights, chunk lengths that do and do not divide the
+slab, and the peer (multi-GPU) form."""
+
+import numpy as np
+import pytest
+
+from oracle import hydro_oracle as HO
+
+pytestmark = pytest.mark.gpu
+
+SIGNED_VELOCITIES = [(1.0, 1.0, 1.0), (-1.0, 0.5, -0.25), (0.7, -1.3, 0.0),
+                     (-0.2, -0.9, 1.1), (0.6, 0.8, -1.0), (-0.5, -0.4, -0.3),
+                     (0.9, -0.1, -0.7), (-0.0, 1.2, 0.5)]
+
+
+@pytest.mark.parametrize("vel", SIGNED_VELOCITIES)
+@pytest.mark.parametrize("rows4", [False, True])
+def test_march_every_sign(cuda, vel, rows4):
+    import torch
+    from paper_2210_06438_b200.field import MarchFieldIteration
+    f = HO.stress_field(64)
+    it = MarchFieldIteration(64, 8, vel, device=cuda, rows4=rows4)
+    it.load(torch.from_numpy(f).to(cuda))
+    for _ in range(3):          # steps 2, 3 read the halos step 1 wrote
+        it.step()
+    torch.cuda.synchronize()
+    assert np.array_equal(it.owned().cpu().numpy(), HO.reference_step(f, vel))
+
+
+@pytest.mark.parametrize("grid,xc", [(32, 0), (32, 5), (64, 1), (64, 7),
+                                     (64, 64), (96, 40), (128, 0)])
+def test_march_chunk_lengths(cuda, grid, xc):
+    """Work items of xc planes (0 = the default 16); a last chunk shorter
+    than xc, one-plane chunks, one chunk for the whole slab."""
+    import torch
+    from paper_2210_06438_b200.field import MarchFieldIteration
+    vel = (-0.6, 1.1, -0.9)
+    f = HO.stress_field(grid)
+    it = MarchFieldIteration(grid, 8, vel, device=cuda, xc=xc)
+    it.load(torch.from_numpy(f).to(cuda))
+    for _ in range(2):
+        it.step()
+    torch.cuda.synchronize()
+    assert np.array_equal(it.owned().cpu().numpy(),
+                          HO.reference_step(f, vel, iterations=2))
+
+
+@pytest.mark.parametrize("vel", [(1.0, 1.0, 1.0), (-0.6, 1.1, -0.9)])
+def test_march_writes_the_periodic_halos(cuda, vel):
+    """After one march step the next field's halo faces (one halo
+    coordinate: what the 6-point stencil reads) equal what the halo kernels
+    make of its owned cells."""
+    import torch
+    from paper_2210_06438_b200.field import HX, HY, HZ, MarchFieldIteration
+    f = HO.stress_field(64)
+    it = MarchFieldIteration(64, 8, vel, device=cuda)
+    it.load(torch.from_numpy(f).to(cuda))
+    it.step()
+    got = it.field.clone()
+    it.halo(True)
+    want = it.field.clone()
+    torch.cuda.synchronize()
+    px, py, pz = got.shape
+    hx = (np.arange(px) < HX) | (np.arange(px) >= px - HX)
+    hy = (np.arange(py) < HY) | (np.arange(py) >= py - HY)
+    hz = (np.arange(pz) < HZ) | (np.arange(pz) >= pz - HZ)
+    nh = hx[:, None, None].astype(int) + hy[None, :, None] + hz[None, None, :]
+    face = nh <= 1
+    assert np.array_equal(got.cpu().numpy()[face], want.cpu().numpy()[face])
+
+
+def test_march_sod_and_blast(cuda):
+    import torch
+    from paper_2210_06438_b200.field import MarchFieldIteration
+    for f in (HO.sod_field(64), HO.initial_field(64)):
+        it = MarchFieldIteration(64, 8, device=cuda)
+        it.load(torch.from_numpy(f).to(cuda))
+        for _ in range(3):
+            it.step()
+        torch.cuda.synchronize()
+        assert np.array_equal(it.owned().cpu().numpy(), HO.reference_step(f))
+
+
+@pytest.mark.parametrize("kernel", ["march", "cols"])
+@pytest.mark.parametrize("vel", [(-1.0, 0.5, -0.25), (1.0, 1.0, 1.0)])
+def test_peer_single_rank_both_kernels(cuda, kernel, vel):
+    import torch
+    from paper_2210_06438_b200.field import PeerSlabFieldIteration
+    from paper_2210_06438_b200.parallel_halo import SlabPartition
+    f = HO.stress_field(64)
+    r = PeerSlabFieldIteration(SlabPartition(64, 8, 1, 0), f, vel,
+                               device=cuda, kernel=kernel)
+    assert r.kernel == kernel
+    for _ in range(3):
+        r.iteration()
+    torch.cuda.synchronize()
+    r.check()
+    assert np.array_equal(r.owned().cpu().numpy(), HO.reference_step(f, vel))
+
+
+def test_march_rejects_bad_shapes(cuda, native_lib):
+    import torch
+    from paper_2210_06438_b200 import _lib
+    P = torch.zeros((12, 20, 24), dtype=torch.float64, device=cuda)
+    Q = torch.zeros_like(P)
+    s = torch.cuda.current_stream().cuda_stream
+    # Gz = 16 is not a multiple of the 32-lane column
+    assert native_lib.tf_field_march_f64(P.data_ptr(), 8, 16, 16, 1.0, 1.0,
+                                         1.0, 0.1, Q.data_ptr(), None, None, 0,
+                                         0, None, s) == _lib.TF_E_INVALID
+    # in == out
+    assert native_lib.tf_field_march_f64(P.data_ptr(), 8, 32, 32, 1.0, 1.0,
+                                         1.0, 0.1, P.data_ptr(), None, None, 0,
+                                         0, None, s) == _lib.TF_E_INVALID
+    # HALO_X together with peer pointers
+    assert native_lib.tf_field_march_f64(
+        P.data_ptr(), 8, 32, 32, 1.0, 1.0, 1.0, 0.1, Q.data_ptr(),
+        Q.data_ptr(), None, _lib.TF_STEP_HALO_X, 0, None, s) == _lib.TF_E_INVALID
