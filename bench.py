@@ -364,6 +364,27 @@ def realtime_runner(wl, max_team, executors, parents=None, overlap=False):
     return step, launches, ex
 
 
+def queue_runner(wl, max_team, parents=None):
+    """Strategy 3 formed ON THE FLY inside every step: the arrivals go
+    through the C++ formation core (cap / solo fast path / drain on 'every
+    published slice completed'), each closed team is published to the
+    device queue, one consumer grid per step (a CTA per published slice,
+    a programmatic dependent of the previous step's grid)."""
+    from paper_2210_06438_b200.strategy3 import (QueueExecutor,
+                                                 default_parents)
+    parents = parents or default_parents(wl.S, max_team)
+    # the pools are produced once, before any step: the first boxes of step
+    # k+1 may load during step k's tail (TF_LAUNCH_OVERLAP_PREV)
+    q = QueueExecutor("reconstruct", max_team, parents, wl.n,
+                      early_loads=True)
+    arrivals = np.arange(wl.S, dtype=np.int32)
+
+    def step(k):
+        q.run(wl.pools[k % len(wl.pools)], VELOCITY, arrivals, wl.um, wl.up,
+              wl.F, amax=wl.amax)
+    return step, q
+
+
 def single_runner(wl, reconstruction="minmod", flux_form=0):
     from paper_2210_06438_b200 import ops
 
@@ -428,24 +449,26 @@ def run_sweep(wl, args, world, stream, peak):
             "launches_per_iter": launches[-1],
             "mean_team": wl.S * len(launches) / max(1, st["teams_formed"]),
             "solo_fast_path": st["solo_fast_path"]}
+    # the headline executor over A: formation inside the timed step, each
+    # closed team published to the device queue.  The device no longer pays
+    # per team (one consumer grid per step, a CTA per slice); the HOST does
+    # — one release store per team, which the fetcher CTA polls over PCIe —
+    # so at small A the formation loop, not the GPU, sets the step time
+    # (host_us: the C++ loop's own clock per step)
     out["realtime_queue"] = {}
-    from paper_2210_06438_b200.strategy3 import (QueueExecutor,
-                                                 default_parents)
-    # an int32 array, so the per-step C call does not convert a list
-    arrivals = np.arange(wl.S, dtype=np.int32)
     for A in (1, 4, 16, 64, 128):
-        q = QueueExecutor("reconstruct", A, default_parents(wl.S, A), wl.n)
-        ms = timed(lambda k: q.run(wl.pools[k % len(wl.pools)], VELOCITY,
-                                   arrivals, wl.um, wl.up, wl.F,
-                                   amax=wl.amax), ks, kw, world, stream)
+        step, q = queue_runner(wl, A)
+        ms = timed(step, ks, kw, world, stream)
+        q.wait()
         st = q.stats()
         out["realtime_queue"][A] = {
             "cell_updates_per_s": rate(wl.S, wl.n, ms), "ms_per_iter": ms,
             "mean_team": st["teams_formed"] and
             sum(k * v for k, v in st["size_histogram"].items())
             / st["teams_formed"],
-            "solo_fast_path": st["solo_fast_path"]}
-        del q
+            "solo_fast_path": st["solo_fast_path"],
+            "host_us": q.host_times()}
+        del q, step
     for E in (1, 8, 32, 128):
         # strategy 2: per-task launches (A = 1) spread over E streams
         step, nk, _, _ = plan_runner(wl, 1, E, parents=E)
@@ -757,33 +780,74 @@ def e2e_faces_leg(wl, step_fn, steps, warmup, world, stream):
 
 
 # ------------------------------------------------- real-time aggregation
-def realtime_leg(wl, args, world, stream, peak):
-    """Strategy 3 formed ON THE FLY inside the timed region: every step
-    submits the 4096 arrivals to the formation core (real-time starvation
-    signal: published slices not yet completed), each closed team is
-    published to the resident consumer grid (strategy3.QueueExecutor)
-    instead of launched.  Same outputs as `value` (checked against the
-    oracle digests), per-sub-grid slots."""
-    from paper_2210_06438_b200.strategy3 import (QueueExecutor,
-                                                 default_parents)
+def plan_leg(wl, args, world, stream, peak):
+    """The same A-teams pre-formed once (form_teams with a saturated device:
+    every busy query answers busy, cap closure) and replayed as ONE CUDA
+    graph per step — one kernel node per team on 2 executor branches,
+    programmatic dependent launches inside a branch; outputs into the packed
+    team leases (the reference's slice_alloc layout).  The steady state of
+    an iterative solver whose teams repeat; checked against the oracle
+    digests like the headline."""
+    step, nk, hist, plans = plan_runner(wl, args.max_team, args.executors,
+                                        overlap=not args.no_overlap,
+                                        team_buffers=True)
+    ms = timed(step, args.steps, args.warmup, world, stream)
+    check = cfg2_output_check(wl, plans, True)
+    if not check["bitexact_vs_oracle_digest"]:
+        raise SystemExit(f"bench.py: plan outputs differ {check}")
+    traffic = ncu_graph_traffic() if args.max_team == 128 else None
+    achieved = wl.S * b_alg(wl.n) / (ms * 1e-3) / 1e9
+    return {"value": rate(wl.S * world, wl.n, ms), "unit": UNIT,
+            "ms_per_step": ms, "max_team": args.max_team,
+            "executors": args.executors, "team_histogram": hist,
+            "launches_per_step": nk, "self_check": check,
+            "roofline": {"achieved": achieved, "peak": peak,
+                         "frac": achieved / peak, "unit": "GB/s",
+                         "traffic": traffic,
+                         "traffic_frac": (traffic / (ms * 1e-3) / 1e9 / peak
+                                          if traffic else None),
+                         "traffic_source": "profiles/r02_ncu_plan_graph_"
+                                           "A128.csv (--graph-profiling "
+                                           "graph --cache-control none)"}}
+
+
+def realtime_leg(wl, args, world, stream, peak, with_queue=True):
+    """Strategy 3 formed ON THE FLY inside the timed region, other
+    executors: (with_queue) the device queue (strategy3.QueueExecutor: each
+    closed team published to a consumer grid), and each closed team
+    launched as its own grid FROM THE DEVICE (strategy3.
+    DeviceLaunchExecutor) over A = 1..128.  Same outputs as `value`
+    (checked against the oracle digests), per-sub-grid slots."""
     arrivals = np.arange(wl.S, dtype=np.int32)
     A = args.max_team
-    q = QueueExecutor("reconstruct", A, default_parents(wl.S, A), wl.n)
-
-    def step(k):
-        q.run(wl.pools[k % len(wl.pools)], VELOCITY, arrivals, wl.um, wl.up,
-              wl.F, amax=wl.amax)
-    with ClockSampler(0) as clk:
-        ms = timed(step, args.steps, args.warmup, world, stream)
-    q.wait()
-    st = q.stats()
-    check = cfg2_output_check(wl, rerun=lambda: (step(0), q.wait()))
-    if not check["bitexact_vs_oracle_digest"]:
-        raise SystemExit(f"bench.py: real-time queue outputs differ {check}")
-    achieved = wl.S * b_alg(wl.n) / (ms * 1e-3) / 1e9
+    out = {}
+    if with_queue:
+        step, q = queue_runner(wl, A)
+        with ClockSampler(0) as clk:
+            ms = timed(step, args.steps, args.warmup, world, stream)
+        q.wait()
+        st = q.stats()
+        check = cfg2_output_check(wl, rerun=lambda: (step(0), q.wait()))
+        if not check["bitexact_vs_oracle_digest"]:
+            raise SystemExit(f"bench.py: real-time queue outputs differ "
+                             f"{check}")
+        achieved = wl.S * b_alg(wl.n) / (ms * 1e-3) / 1e9
+        out.update({
+            "value": rate(wl.S * world, wl.n, ms), "unit": UNIT,
+            "ms_per_step": ms, "max_team": A,
+            "mean_team": sum(k * v for k, v in st["size_histogram"].items())
+            / max(1, st["teams_formed"]),
+            "teams_per_step": st["teams_formed"] / max(1, q.runs),
+            "solo_fast_path": st["solo_fast_path"],
+            "host_us_per_step": q.host_times(),
+            "roofline": {"achieved": achieved, "peak": peak,
+                         "frac": achieved / peak, "unit": "GB/s"},
+            "gpu_launches_per_step": 1, "self_check": check,
+            "clocks": clk.summary()})
     # the same real-time formation with each closed team launched as its
     # own grid from the device (strategy3.DeviceLaunchExecutor): A sweep
-    from paper_2210_06438_b200.strategy3 import DeviceLaunchExecutor
+    from paper_2210_06438_b200.strategy3 import (DeviceLaunchExecutor,
+                                                 default_parents)
     dl = {}
     for a in (1, 4, 16, 64, 128):
         ex = DeviceLaunchExecutor("reconstruct", a,
@@ -801,7 +865,6 @@ def realtime_leg(wl, args, world, stream, peak):
                  / max(1, dst["teams_formed"]),
                  "hbm_frac": wl.S * b_alg(wl.n) / (dms * 1e-3) / 1e9 / peak}
         del ex
-    dcheck = None
     ex = DeviceLaunchExecutor("reconstruct", A, default_parents(wl.S, A),
                               wl.n)
     dcheck = cfg2_output_check(
@@ -810,22 +873,9 @@ def realtime_leg(wl, args, world, stream, peak):
     del ex
     if not dcheck["bitexact_vs_oracle_digest"]:
         raise SystemExit(f"bench.py: device-launch outputs differ {dcheck}")
-    return {"value": rate(wl.S * world, wl.n, ms), "unit": UNIT,
-            "device_launch_sweep": dl,
-            "device_launch_self_check": dcheck["bitexact_vs_oracle_digest"],
-            "ms_per_step": ms, "max_team": A,
-            "mean_team": sum(k * v for k, v in st["size_histogram"].items())
-            / max(1, st["teams_formed"]),
-            "teams_per_step": st["teams_formed"] / max(1, q.runs),
-            "solo_fast_path": st["solo_fast_path"],
-            "roofline": {"achieved": achieved, "peak": peak,
-                         "frac": achieved / peak, "unit": "GB/s"},
-            "gpu_launches_per_step": 1, "self_check": check,
-            "clocks": clk.summary(),
-            "step": "4096 task arrivals -> C++ formation core (cap / solo "
-                    "fast path / drain on 'all published slices "
-                    "completed') -> closed teams published to a ring -> "
-                    "resident consumer grid (one launch per step)"}
+    out["device_launch_sweep"] = dl
+    out["device_launch_self_check"] = dcheck["bitexact_vs_oracle_digest"]
+    return out
 
 
 # ------------------------------------------------ the reference API path
@@ -1159,8 +1209,11 @@ def main():
     # PDL chain of team launches in a graph slows by 12% (33.7 -> 29.6 G)
     # while two branches hold 33.4 G (scripts/exp_sweep_gap.py)
     ap.add_argument("--executors", type=int, default=2)
-    ap.add_argument("--mode", choices=("plan", "realtime", "single"),
-                    default="plan")
+    # queue: teams formed on the fly inside the timed step and published to
+    # the device queue (the headline); plan: the same teams pre-formed and
+    # replayed as a CUDA graph; realtime: one host launch per closed team
+    ap.add_argument("--mode", choices=("queue", "plan", "realtime", "single"),
+                    default="queue")
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--outputs", choices=("team", "subgrid"), default="team",
                     help="team: each team writes its lease of the packed team "
@@ -1203,7 +1256,11 @@ def main():
         return
     wl = Workload()
     plans = None
-    if args.mode == "plan":
+    q = None
+    if args.mode == "queue":
+        step, q = queue_runner(wl, args.max_team)
+        launches_per_step, hist = 1, None
+    elif args.mode == "plan":
         step, nk, hist, plans = plan_runner(
             wl, args.max_team, args.executors, overlap=not args.no_overlap,
             team_buffers=args.outputs == "team")
@@ -1225,34 +1282,79 @@ def main():
         while time.time() < t_end:
             step(k)
             k += 1
+        if q is not None:
+            q.wait()
+            st0 = q.stats()
+            runs0 = q.runs
         ms = timed(step, args.steps, args.warmup, world, stream)
+    if q is not None:
+        q.wait()
+        st = q.stats()
+        runs = q.runs - runs0
+        teams = st["teams_formed"] - st0["teams_formed"]
+        hist = {k: v - st0["size_histogram"].get(k, 0)
+                for k, v in st["size_histogram"].items()
+                if v - st0["size_histogram"].get(k, 0)}
+        formation = {
+            "teams_per_step": teams / max(1, runs),
+            "mean_team": wl.S * runs / max(1, teams),
+            "solo_fast_path_per_step":
+                (st["solo_fast_path"] - st0["solo_fast_path"]) / max(1, runs),
+            "host_us_per_step": q.host_times()}
     if launches_per_step is None:
         launches_per_step = launches[-1]
     total_S = wl.S * world
     value = rate(total_S, wl.n, ms)
     bytes_step = wl.S * b_alg(wl.n)
     achieved = bytes_step / (ms * 1e-3) / 1e9
-    traffic = ncu_graph_traffic() if (args.mode == "plan"
-                                      and args.max_team == 128) else None
-    check = cfg2_output_check(wl, plans, args.outputs == "team") \
-        if plans else None
+    if args.mode == "queue":
+        traffic = ncu_graph_traffic("r02_ncu_queue_consumer.csv")
+        traffic_note = (
+            "traffic = DRAM read+write bytes of one consumer grid over the "
+            "same 4096 slices from ncu (profiles/r02_ncu_queue_consumer.csv,"
+            " --cache-control none; ncu serialises the launch, so the "
+            "capture is of a run whose slices were all published first: "
+            "scripts/exp_consumer.py)")
+    else:
+        traffic = ncu_graph_traffic() if (args.mode == "plan"
+                                          and args.max_team == 128) else None
+        traffic_note = (
+            "traffic = DRAM read+write bytes of one step from the ncu "
+            "capture of this bench's own plan-graph replays "
+            "(profiles/r02_ncu_plan_graph_A128.csv, --graph-profiling graph "
+            "--cache-control none)")
+    if q is not None:
+        check = cfg2_output_check(wl, rerun=lambda: (step(0), q.wait()))
+    else:
+        check = cfg2_output_check(wl, plans, args.outputs == "team") \
+            if plans else None
     if check is not None and not check["bitexact_vs_oracle_digest"]:
         raise SystemExit(f"bench.py: timed outputs differ from the oracle "
                          f"digests {check}")
     # the kernel timed alone: one launch over all slices (aggregation limit)
     ms_single = timed(single_runner(wl), args.steps, args.warmup, world,
                       stream)
+    run = {"max_team": args.max_team, "mode": args.mode,
+           "team_histogram": hist}
+    if args.mode == "queue":
+        run.update(formation)
+        run["outputs"] = "per-sub-grid slots"
+        run["step"] = ("4096 task arrivals -> C++ formation core (cap / "
+                       "solo fast path / drain when every published slice "
+                       "has completed) -> each closed team published to "
+                       "the device queue -> one consumer grid per step "
+                       "(a CTA per published slice; PDL-chained steps)")
+    else:
+        run["executors"] = args.executors
+        run["outputs"] = ("packed team leases (slice_alloc layout)"
+                          if args.outputs == "team" else "per-sub-grid slots")
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic",
         "config": cfg2_config(),
-        "run": {"max_team": args.max_team, "executors": args.executors,
-                "mode": args.mode, "team_histogram": hist,
-                "outputs": ("packed team leases (slice_alloc layout)"
-                            if args.outputs == "team"
-                            else "per-sub-grid slots")},
+        "run": run,
         "self_check": check,
         "gpu_launches": launches_per_step * args.steps,
         "roofline": {
@@ -1264,12 +1366,8 @@ def main():
             "alg_bytes_per_step": bytes_step,
             "per_subgrid_alg_bytes": b_alg(wl.n),
             "note": "achieved = algorithmic bytes of the whole step / step "
-                    "time (every launch in the step is the recon+flux team "
-                    "kernel: 32 launches of 128 slices); traffic = DRAM "
-                    "read+write bytes of one step from the ncu capture of "
-                    "this bench's own plan-graph replays "
-                    "(profiles/r02_ncu_plan_graph_A128.csv, --graph-"
-                    "profiling graph --cache-control none); traffic_frac = "
+                    "time (every launch in the step is the recon+flux "
+                    "kernel); " + traffic_note + "; traffic_frac = "
                     "traffic / step time / peak",
             # also against the 8 TB/s HBM3e spec figure
             "spec_frac_8tbs": achieved / 8000.0,
@@ -1279,7 +1377,10 @@ def main():
                 "frac": bytes_step / (ms_single * 1e-3) / 1e9 / peak}},
         "clocks": clk.summary(),
     }
-    line["realtime"] = realtime_leg(wl, args, world, stream, peak)
+    if args.mode == "queue":
+        line["plan"] = plan_leg(wl, args, world, stream, peak)
+    line["realtime"] = realtime_leg(wl, args, world, stream, peak,
+                                    with_queue=args.mode != "queue")
     line["e2e"] = e2e_leg(args, max(10, args.steps // 2), 3, world, stream)
     # the host link bounds e2e: bytes both ways per step against the
     # measured concurrent copy-engine rate (48.9 GB/s per direction on this

@@ -302,10 +302,19 @@ int tf_executor_sync(tf_executor* ex);
  * memory; busy = published slices not yet completed.  The region must have
  * exactly one executor (the queue).  run() returns once every arrival has
  * been published; the consumer runs on `stream` and completes there.
- * tf_queue_consumer_* are the device side (used by tf_qexec_*).            */
+ * Consecutive runs on one stream overlap: run k+1's grid is a programmatic
+ * dependent of run k's — its CTAs take the SM slots run k's tail frees,
+ * mirror and claim their first slices, and (TF_LAUNCH_OVERLAP_PREV, see
+ * tf_qexec_set_flags) load their stencil boxes; every output store waits
+ * for run k.  tf_queue_consumer_* are the device side (used by tf_qexec_*).*/
 typedef struct tf_qexec tf_qexec;
 int tf_qexec_create(tf_region* region, int32_t n, tf_qexec** out);
 void tf_qexec_destroy(tf_qexec* q);
+/* TF_LAUNCH_OVERLAP_PREV: a run's first stencil boxes may load while the
+ * previous kernel on the stream still runs.  Only valid when that kernel
+ * does not produce the run's pool (e.g. it is the previous run, or a team
+ * kernel).  Default 0: boxes load after the previous kernel completes.     */
+int tf_qexec_set_flags(tf_qexec* q, int32_t flags);
 int tf_qexec_run_recon_flux(tf_qexec* q, const double* pool_ext,
                             int64_t pool_slices, const int32_t* ids,
                             int64_t count, double ax, double ay, double az,
@@ -314,25 +323,33 @@ int tf_qexec_run_recon_flux(tf_qexec* q, const double* pool_ext,
                             int64_t* teams_published);
 /* slices the consumer has completed so far (host view)                     */
 int64_t tf_qexec_completed(const tf_qexec* q);
+/* host time summed over runs: {runs, ns waiting for a queue slot's previous
+ * run, ns in the launch, ns in the formation + publish loop}               */
+int tf_qexec_host_times(const tf_qexec* q, int64_t* out4);
 /* Wait for every run in flight; TF_E_TIMEOUT if a consumer grid gave up
  * (its timeout expired with slices unprocessed).  A run reusing a queue
  * slot reports a timeout of that slot's previous run the same way.        */
 int tf_qexec_wait(tf_qexec* q);
-int tf_queue_consumer_ctas(int32_t n);
 /* ring_h/ctl_h: mapped pinned host ring + control block {published,
  * final_count, completed, status}; ring_d: device mirror of tagged entries
  * (epoch << 32 | id), ring_cap of them (the most this launch may publish),
- * zeroed once at allocation; epoch >= 1, new for every launch on that ring;
- * qdev: {published, final_count, claim, done}, one 128-B line each (zeroed,
- * final_count = -1, before launch); qdev_next (or NULL): another such block
- * the kernel resets on its way out, for the next launch.                    */
+ * zeroed once at allocation; epoch >= 1, new for every launch on that ring; the grid is
+ * one fetcher CTA + one CTA per entry (CTA k computes entry k); qdev: {published,
+ * final_count, spare, done}, one 128-B line each, zeroed once at allocation
+ * and never reset: done is monotonic over the launches on one qdev,
+ * done_base = the slices of the earlier launches; final_count is tagged
+ * (epoch << 32 | count).
+ * flags: TF_QUEUE_CHAIN = launch as a programmatic dependent of the previous
+ * kernel on the stream (its first boxes load after that kernel completes),
+ * | TF_LAUNCH_OVERLAP_PREV = load them before (see tf_qexec_set_flags).    */
+#define TF_QUEUE_CHAIN 2
 int tf_queue_consumer_launch(const double* pool_ext, int64_t pool_slices,
                              int32_t n, const int32_t* ring_h, void* ctl_h,
                              int64_t* ring_d, int64_t ring_cap, void* qdev,
-                             void* qdev_next, int32_t ctas, int32_t epoch,
-                             double ax, double ay, double az, double* um,
-                             double* up, double* F, double* amax,
-                             int32_t flux_form, int64_t timeout_ns,
+                             uint64_t done_base, int32_t epoch, double ax,
+                             double ay, double az, double* um, double* up,
+                             double* F, double* amax, int32_t flux_form,
+                             int64_t timeout_ns, int32_t flags,
                              tf_stream_t stream);
 
 /* ---- device-launch executor (strategy 3, teams launched by the GPU) ----- */

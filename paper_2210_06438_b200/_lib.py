@@ -32,6 +32,7 @@ TF_PLAN_REFGEO = 16
 TF_STEP_HALO_YZ = 4
 TF_STEP_HALO_X = 8
 TF_MARCH_ROWS4 = 16
+TF_QUEUE_CHAIN = 2
 
 
 class EnterResult(C.Structure):
@@ -154,16 +155,18 @@ SIGNATURES = {
     "tf_dlexec_wait": (C.c_int, [_p]),
     "tf_qexec_create": (C.c_int, [_p, _i32, C.POINTER(_p)]),
     "tf_qexec_destroy": (None, [_p]),
-    "tf_qexec_run_recon_flux": (C.c_int, [_p, _p, _i64, _pi32, _i64, _f64,
+    # ids as a raw address (the step loop passes a numpy array's pointer)
+    "tf_qexec_run_recon_flux": (C.c_int, [_p, _p, _i64, _p, _i64, _f64,
                                           _f64, _f64, _p, _p, _p, _p, _i32,
-                                          _p, _pi64]),
+                                          _p, _p]),
+    "tf_qexec_set_flags": (C.c_int, [_p, _i32]),
     "tf_qexec_completed": (_i64, [_p]),
+    "tf_qexec_host_times": (C.c_int, [_p, _pi64]),
     "tf_qexec_wait": (C.c_int, [_p]),
-    "tf_queue_consumer_ctas": (C.c_int, [_i32]),
     "tf_queue_consumer_launch": (C.c_int, [_p, _i64, _i32, _p, _p, _p, _i64,
-                                           _p, _p, _i32, _i32, _f64, _f64,
+                                           _p, C.c_uint64, _i32, _f64, _f64,
                                            _f64, _p, _p, _p, _p, _i32, _i64,
-                                           _p]),  # noqa
+                                           _i32, _p]),
     "tf_version": (C.c_char_p, []),
     "tf_check_device": (C.c_int, [_i32]),
 }

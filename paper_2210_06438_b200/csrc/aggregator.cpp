@@ -666,13 +666,18 @@ struct QueueCtlHost {   // mirrors QueueCtl (hydro_kernels.cu)
 };
 struct QueueDevInit {   // mirrors QueueDev (one 128-B line per word)
   alignas(128) long long published;
-  alignas(128) long long final_count;
-  alignas(128) unsigned long long claim;
+  alignas(128) long long final_count;  // (epoch << 32) | count
+  alignas(128) unsigned long long spare;
   alignas(128) unsigned long long done;
 };
 
 // One queue instance; runs alternate between two so that run k+1 can
-// publish while run k's consumer grid is still draining its tail.
+// publish while run k's consumer grid is still draining its tail.  A slot's
+// device completion count is monotonic across its runs (the host passes
+// each run the slices of the slot's earlier runs) and its close marker is
+// tagged with the run's epoch, so nothing is reset between runs and
+// consecutive runs can overlap (programmatic dependent launch,
+// k_queue_consumer).
 struct QueueSlot {
   QueueCtlHost* ctl_h = nullptr;   // mapped pinned
   void* ctl_hd = nullptr;          // its device alias
@@ -682,7 +687,9 @@ struct QueueSlot {
   int32_t epoch = 0;               // last epoch launched on this slot
   int64_t ring_cap = 0;
   void* qdev = nullptr;            // QueueDevInit on the device
-  cudaEvent_t done_ev = nullptr;
+  uint64_t done_base = 0;          // slices of the slot's earlier runs
+  int64_t count = 0;               // slices the last run published
+  cudaEvent_t ev = nullptr;        // recorded only to order other streams
   cudaStream_t stream = nullptr;   // where this slot's last run went
   bool in_flight = false;
 };
@@ -691,15 +698,24 @@ struct tf_qexec {
   tf_region* region = nullptr;
   QueueSlot slots[2];
   int cur = 1;
-  int32_t ctas = 0;
   int32_t n = 0;
+  int32_t flags = 0;               // TF_LAUNCH_OVERLAP_PREV: early box loads
   int64_t published = 0;
   int64_t seen_published = 0;
+  // host time per phase, summed over runs: waiting for a slot's previous
+  // run, the launch, the formation + publish loop
+  int64_t runs = 0, ns_wait = 0, ns_launch = 0, ns_publish = 0;
   QueueSlot& slot() { return slots[cur]; }
   const QueueSlot& slot() const { return slots[cur]; }
 };
 
 namespace {
+
+int64_t q_now_ns() {
+  return std::chrono::duration_cast<std::chrono::nanoseconds>(
+             std::chrono::steady_clock::now().time_since_epoch())
+      .count();
+}
 
 int64_t q_done(const tf_qexec* q) {
   return __atomic_load_n(&q->slot().ctl_h->completed, __ATOMIC_ACQUIRE);
@@ -732,6 +748,53 @@ void q_publish(tf_qexec* q, int64_t team) {
   r->teams.release(team);
 }
 
+// A timed-out run leaves unprocessed slices and claims the host cannot
+// count: once the stream is idle, start the slot's counters afresh.
+int q_reset_slot(QueueSlot& S) {
+  cudaError_t e = cudaStreamSynchronize(S.stream);
+  QueueDevInit init{};
+  if (e == cudaSuccess)
+    e = cudaMemcpy(S.qdev, &init, sizeof(init), cudaMemcpyHostToDevice);
+  S.done_base = 0;
+  S.ctl_h->status = 0;
+  S.in_flight = false;
+  return e != cudaSuccess ? (int)e : TF_E_TIMEOUT;
+}
+
+// The slot's previous run has completed every slice it published (host
+// view: the fetcher's completion count), or reported a timeout.  Its host
+// memory (ring, control block) is then free; its device-side stragglers
+// (consumers seeing the queue closed) are ordered before the slot's next
+// run by the stream (PDL chain) or by q_order_streams.
+int q_drain_slot(QueueSlot& S) {
+  if (!S.in_flight) return 0;
+  for (uint64_t spins = 0;; ++spins) {
+    if (__atomic_load_n(&S.ctl_h->status, __ATOMIC_ACQUIRE))
+      return q_reset_slot(S);
+    if (__atomic_load_n(&S.ctl_h->completed, __ATOMIC_ACQUIRE) >= S.count)
+      break;
+    if ((spins & 1023) == 1023) {
+      // a failed or finished stream that never reported every slice
+      const cudaError_t e = cudaStreamQuery(S.stream);
+      if (e == cudaSuccess &&
+          __atomic_load_n(&S.ctl_h->completed, __ATOMIC_ACQUIRE) < S.count)
+        return q_reset_slot(S);
+      if (e != cudaSuccess && e != cudaErrorNotReady) return e;
+    }
+    __builtin_ia32_pause();
+  }
+  S.in_flight = false;
+  return 0;
+}
+
+// Order a launch on `st` after a slot's last run on another stream.
+int q_order_streams(QueueSlot& S, cudaStream_t st) {
+  if (S.stream == nullptr || S.stream == st) return 0;
+  cudaError_t e = cudaEventRecord(S.ev, S.stream);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(st, S.ev, 0);
+  return e;
+}
+
 }  // namespace
 
 extern "C" {
@@ -739,11 +802,8 @@ extern "C" {
 int tf_qexec_create(tf_region* region, int32_t n, tf_qexec** out) {
   if (!region || !out || region->executors != 1 || (n != 8 && n != 16))
     return TF_E_INVALID;
-  const int ctas = tf_queue_consumer_ctas(n);
-  if (ctas < 1) return ctas < 0 ? -ctas : TF_E_INVALID;
   tf_qexec* q = new tf_qexec();
   q->region = region;
-  q->ctas = ctas;
   q->n = n;
   cudaError_t e = cudaSuccess;
   for (QueueSlot& S : q->slots) {
@@ -751,13 +811,12 @@ int tf_qexec_create(tf_region* region, int32_t n, tf_qexec** out) {
       e = cudaHostAlloc(&S.ctl_h, sizeof(QueueCtlHost), cudaHostAllocMapped);
     if (e == cudaSuccess) e = cudaHostGetDevicePointer(&S.ctl_hd, S.ctl_h, 0);
     if (e == cudaSuccess) e = cudaMalloc(&S.qdev, sizeof(QueueDevInit));
-    if (e == cudaSuccess) {  // {0, -1, 0, 0}; later runs reset it on device
+    if (e == cudaSuccess) {  // all zero: final_count's epoch tag 0 = open
       QueueDevInit init{};
-      init.final_count = -1;
       e = cudaMemcpy(S.qdev, &init, sizeof(init), cudaMemcpyHostToDevice);
     }
     if (e == cudaSuccess)
-      e = cudaEventCreateWithFlags(&S.done_ev, cudaEventDisableTiming);
+      e = cudaEventCreateWithFlags(&S.ev, cudaEventDisableTiming);
   }
   if (e != cudaSuccess) {
     tf_qexec_destroy(q);
@@ -767,15 +826,22 @@ int tf_qexec_create(tf_region* region, int32_t n, tf_qexec** out) {
   return 0;
 }
 
+int tf_qexec_set_flags(tf_qexec* q, int32_t flags) {
+  if (!q || (flags & ~TF_LAUNCH_OVERLAP_PREV)) return TF_E_INVALID;
+  q->flags = flags;
+  return 0;
+}
+
 void tf_qexec_destroy(tf_qexec* q) {
   if (!q) return;
+  for (QueueSlot& S : q->slots)
+    if (S.in_flight && S.stream) cudaStreamSynchronize(S.stream);
   for (QueueSlot& S : q->slots) {
-    if (S.in_flight) cudaEventSynchronize(S.done_ev);
     if (S.ctl_h) cudaFreeHost(S.ctl_h);
     if (S.ring_h) cudaFreeHost(S.ring_h);
     if (S.ring_d) cudaFree(S.ring_d);
     if (S.qdev) cudaFree(S.qdev);
-    if (S.done_ev) cudaEventDestroy(S.done_ev);
+    if (S.ev) cudaEventDestroy(S.ev);
   }
   delete q;
 }
@@ -791,20 +857,21 @@ int tf_qexec_run_recon_flux(tf_qexec* q, const double* pool_ext,
     if (ids[i] < 0 || ids[i] >= pool_slices) return TF_E_INVALID;
   // alternate queue slots: this run publishes while the previous run's
   // consumer may still drain its tail; the slot's own previous use (two
-  // runs ago) must be gone before its counters reset
+  // runs ago) must have completed its slices before its host ring and
+  // control block are rewritten
+  const int64_t t0 = q_now_ns();
   q->cur ^= 1;
   QueueSlot& S = q->slot();
-  if (S.in_flight) {
-    cudaError_t e = cudaEventSynchronize(S.done_ev);
-    if (e != cudaSuccess) return e;
-    S.in_flight = false;
-    // a consumer grid that gave up left slices unprocessed: report it
-    if (__atomic_load_n(&S.ctl_h->status, __ATOMIC_ACQUIRE)) {
-      S.ctl_h->status = 0;
-      return TF_E_TIMEOUT;
-    }
-  }
+  int drc = q_drain_slot(S);
+  if (drc) return drc;
+  const int64_t t1 = q_now_ns();
+  cudaStream_t st = (cudaStream_t)stream;
   if (count > S.ring_cap || !S.ring_h) {
+    // the device mirror is reallocated: nothing of the slot may be running
+    if (S.stream) {
+      cudaError_t e = cudaStreamSynchronize(S.stream);
+      if (e != cudaSuccess) return e;
+    }
     if (S.ring_h) cudaFreeHost(S.ring_h);
     if (S.ring_d) cudaFree(S.ring_d);
     S.ring_h = nullptr;
@@ -817,9 +884,9 @@ int tf_qexec_run_recon_flux(tf_qexec* q, const double* pool_ext,
                                    S.ring_h, 0);
     if (e == cudaSuccess)
       e = cudaMalloc(reinterpret_cast<void**>(&S.ring_d), sizeof(int64_t) * cap);
-    // no stale entry may carry a live epoch
+    // no stale entry may carry a live epoch (tag 0); the epoch itself keeps
+    // counting — the slot's final_count still carries the last run's tag
     if (e == cudaSuccess) e = cudaMemset(S.ring_d, 0, sizeof(int64_t) * cap);
-    S.epoch = 0;
     if (e != cudaSuccess) return e;
     S.ring_cap = cap;
   }
@@ -830,27 +897,23 @@ int tf_qexec_run_recon_flux(tf_qexec* q, const double* pool_ext,
   S.ctl_h->completed = 0;
   S.ctl_h->status = 0;
   __atomic_thread_fence(__ATOMIC_SEQ_CST);
-  cudaStream_t st = (cudaStream_t)stream;
-  // this slot's device counters are reset by the OTHER slot's previous run
-  // on its way out: when that run went to a different stream, order this
-  // launch after it
+  // runs of this queue on another stream: this one goes after them (the
+  // PDL chain orders runs on one stream)
   QueueSlot& other = q->slots[q->cur ^ 1];
-  if (other.in_flight && other.stream != st) {
-    cudaError_t e = cudaStreamWaitEvent(st, other.done_ev, 0);
-    if (e != cudaSuccess) return e;
-  }
+  int orc = q_order_streams(S, st);
+  if (!orc && other.in_flight) orc = q_order_streams(other, st);
+  if (orc) return orc;
+  const bool chain = S.stream == st && (!other.in_flight || other.stream == st);
   S.stream = st;
-  // the slot's device counters were reset by the previous run's kernel on
-  // its way out (qdev_next), or at creation
   int rc = tf_queue_consumer_launch(
       pool_ext, pool_slices, q->n, S.ring_hd, S.ctl_hd, S.ring_d, count,
-      S.qdev, q->slots[q->cur ^ 1].qdev, q->ctas, ++S.epoch, ax, ay, az, um,
+      S.qdev, S.done_base, ++S.epoch, ax, ay, az, um,
       up, F, amax, flux_form,
-      /*timeout_ns=*/2000000000LL, stream);
+      /*timeout_ns=*/2000000000LL, chain ? (TF_QUEUE_CHAIN | q->flags) : 0,
+      stream);
   if (rc) return rc;
-  const cudaError_t ce = cudaEventRecord(S.done_ev, st);
-  if (ce != cudaSuccess) return ce;
   S.in_flight = true;
+  const int64_t t2 = q_now_ns();
   tf_region* r = q->region;
   int64_t teams = 0;
   std::vector<int64_t> closed;
@@ -872,10 +935,26 @@ int tf_qexec_run_recon_flux(tf_qexec* q, const double* pool_ext,
   }
   drain();  // arrivals done: the queue drains, closing what is left
   // close the queue even on error so the consumer grid exits
+  S.count = q->published;
+  S.done_base += (uint64_t)q->published;
   __atomic_store_n(&S.ctl_h->final_count, (long long)q->published,
                    __ATOMIC_RELEASE);
   *teams_published = teams;
+  const int64_t t3 = q_now_ns();
+  q->runs += 1;
+  q->ns_wait += t1 - t0;
+  q->ns_launch += t2 - t1;
+  q->ns_publish += t3 - t2;
   return rc;
+}
+
+int tf_qexec_host_times(const tf_qexec* q, int64_t* out4) {
+  if (!q || !out4) return TF_E_INVALID;
+  out4[0] = q->runs;
+  out4[1] = q->ns_wait;
+  out4[2] = q->ns_launch;
+  out4[3] = q->ns_publish;
+  return 0;
 }
 
 int64_t tf_qexec_completed(const tf_qexec* q) { return q ? q_done(q) : -1; }
@@ -885,13 +964,13 @@ int tf_qexec_wait(tf_qexec* q) {
   int rc = 0;
   for (QueueSlot& S : q->slots) {
     if (!S.in_flight) continue;
-    cudaError_t e = cudaEventSynchronize(S.done_ev);
+    cudaError_t e = cudaStreamSynchronize(S.stream);
     if (e != cudaSuccess) return e;
-    S.in_flight = false;
     if (__atomic_load_n(&S.ctl_h->status, __ATOMIC_ACQUIRE)) {
-      S.ctl_h->status = 0;
-      rc = TF_E_TIMEOUT;
+      rc = q_reset_slot(S);
+      continue;
     }
+    S.in_flight = false;
   }
   return rc;
 }

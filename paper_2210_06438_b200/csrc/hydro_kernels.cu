@@ -517,14 +517,14 @@ struct QueueCtl {
 };
 // device-side mirror, polled by the consumers through L2 (only the fetcher
 // CTA ever touches host memory, so the pollers do not flood PCIe)
-// Each word on its own 128-B line: the consumers poll `published` /
-// `final_count` while every CTA hits `claim` and `done` with atomics — on
-// one shared line those polls and atomics serialised in the same L2 slice.
+// Each word on its own 128-B line: the consumers poll `final_count` while
+// every CTA hits `done` with atomics — on one shared line those polls and
+// atomics serialised in the same L2 slice.
 struct QueueDev {
   alignas(128) long long published;
-  alignas(128) long long final_count;
-  alignas(128) unsigned long long claim;
-  alignas(128) unsigned long long done;
+  alignas(128) long long final_count;    // (epoch << 32) | count
+  alignas(128) unsigned long long spare; // (the dynamic claim counter once)
+  alignas(128) unsigned long long done;  // monotonic over the slot's runs
 };
 static_assert(sizeof(QueueDev) == 512, "QueueDev layout (aggregator.cpp)");
 
@@ -541,6 +541,12 @@ __device__ __forceinline__ unsigned long long ld_relaxed_gpu_u64(
 }
 __device__ __forceinline__ long long ld_acquire_gpu(const long long* p) {
   long long v;
+  asm volatile("ld.acquire.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned long long ld_acquire_gpu_u64(
+    const unsigned long long* p) {
+  unsigned long long v;
   asm volatile("ld.acquire.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
@@ -562,22 +568,49 @@ __device__ __forceinline__ unsigned long long globaltimer() {
   return t;
 }
 
+// Programmatic dependent launch between consecutive runs of the queue: run
+// k+1's CTAs take the SM slots run k's CTAs leave during its tail, mirror
+// and fetch their first ring entries (and, with early_loads, load their
+// stencil boxes) while run k finishes; a consumer waits for run k
+// (griddepcontrol.wait: complete, its writes visible) before its first
+// output store.  The fetcher waits before it triggers the NEXT run, so a
+// launched run k+2 implies run k is complete — the invariant that lets the
+// queue slot of run k be reused by run k+2 without any counter reset (the
+// `done` count is monotonic, done_base; final_count carries the epoch).
+__device__ __forceinline__ void pdl_wait() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+// final_count mirror on the device, tagged with the run's epoch so that a
+// slot's counters never need resetting: (epoch << 32) | count
+__device__ __forceinline__ long long fin_of(long long tagged, unsigned epoch) {
+  return (unsigned)((unsigned long long)tagged >> 32) == epoch
+             ? (long long)(unsigned)tagged
+             : -1;
+}
+
 // Block 0 is the fetcher: it mirrors newly published ids from the host ring
 // into device memory (all its threads, several independent PCIe reads in
 // flight per thread — one warp reading 32 ids per round trip was the
 // bottleneck), forwards the close marker, and reports the device-side
 // completion count back to the host.  Blocks 1.. are consumers polling the
-// device mirror.
+// device mirror.  The slot's device counters are monotonic across runs:
+// `done` counts from done_base (the slices of the slot's earlier runs).
 template <int THREADS>
 __device__ void queue_fetcher(const int* __restrict__ ring_h, QueueCtl* ctl,
                               unsigned long long* __restrict__ ring_d,
-                              QueueDev* qd, QueueDev* qd_next, unsigned epoch,
+                              QueueDev* qd, unsigned epoch,
+                              unsigned long long done_base,
                               long long timeout_ns) {
   __shared__ long long s_pub, s_fin, s_done;
   __shared__ int s_stop;
   constexpr int U = 4;                  // loads in flight per thread
   constexpr int CHUNK = THREADS * U;    // ids mirrored per publish
   long long fetched = 0, reported = -1;
+  bool triggered = false;
   unsigned long long last_change = globaltimer();
   // phase 1: mirror ids as the host publishes them, until the queue is
   // closed and every id has been mirrored
@@ -593,7 +626,7 @@ __device__ void queue_fetcher(const int* __restrict__ ring_h, QueueCtl* ctl,
       asm volatile("fence.acq_rel.sys;" ::: "memory");
       s_pub = pub;
       s_fin = fin;
-      s_done = (long long)atomicAdd(&qd->done, 0ULL);  // coherent read
+      s_done = (long long)(atomicAdd(&qd->done, 0ULL) - done_base);
     }
     __syncthreads();
     const long long pub = s_pub, fin = s_fin, done = s_done;
@@ -622,15 +655,27 @@ __device__ void queue_fetcher(const int* __restrict__ ring_h, QueueCtl* ctl,
       last_change = globaltimer();
     }
     if (pub > fetched) fetched = pub;
+    if (!triggered) {
+      // the first ids are out: wait for the previous run (its tail overlaps
+      // this mirror), then let the next run launch
+      pdl_wait();
+      pdl_trigger();
+      triggered = true;
+    }
     if (threadIdx.x == 0) {
-      if (fin >= 0 && fetched >= fin) st_release_gpu(&qd->final_count, fin);
+      if (fin >= 0 && fetched >= fin)
+        st_release_gpu(&qd->final_count,
+                       (long long)(((unsigned long long)epoch << 32) |
+                                   (unsigned long long)fin));
       if (done != reported) {
         st_release_sys(&ctl->completed, done);
         last_change = globaltimer();
       }
       int stop = fin >= 0 && fetched >= fin ? 1 : 0;
       if (!stop && (long long)(globaltimer() - last_change) > timeout_ns) {
-        st_release_gpu(&qd->final_count, fetched);
+        st_release_gpu(&qd->final_count,
+                       (long long)(((unsigned long long)epoch << 32) |
+                                   (unsigned long long)fetched));
         st_release_sys(&ctl->status, 1);
         stop = 2;
       }
@@ -646,10 +691,10 @@ __device__ void queue_fetcher(const int* __restrict__ ring_h, QueueCtl* ctl,
   // the host until all are done — device-side polling only, no PCIe reads,
   // so the grid exits as soon as the last slice does
   if (s_stop != 2) {
-    const long long fin = ld_acquire_gpu(&qd->final_count);
+    const long long fin = fin_of(ld_acquire_gpu(&qd->final_count), epoch);
     for (;;) {
-      const long long done = ld_acquire_gpu(
-          reinterpret_cast<const long long*>(&qd->done));
+      const long long done = (long long)(
+          ld_acquire_gpu_u64(&qd->done) - done_base);
       if (done != reported) {
         st_release_sys(&ctl->completed, done);
         reported = done;
@@ -663,111 +708,96 @@ __device__ void queue_fetcher(const int* __restrict__ ring_h, QueueCtl* ctl,
       __nanosleep(32);
     }
   }
-  // reset the OTHER queue slot's device counters for the next run (it last
-  // ran two launches ago and runs next, both stream-ordered around this
-  // kernel): the host then needs no memset launches between runs
-  if (qd_next != nullptr) {
-    qd_next->published = 0;
-    qd_next->final_count = -1;
-    qd_next->claim = 0;
-    qd_next->done = 0;
-  }
 }
 
-// Claim the next published slice for this CTA (thread 0 only): one atomic
-// on the claim counter, then poll the tagged ring slot until it carries this
-// run's epoch.  Returns the sub-grid id, -1 once the queue is closed and
-// drained, -2 on timeout.
-__device__ __forceinline__ int queue_claim(QueueDev* qd,
-                                           const unsigned long long* ring_d,
-                                           long long ring_cap, unsigned epoch,
-                                           long long timeout_ns) {
-  const long long k = (long long)atomicAdd(&qd->claim, 1ULL);
+// One CTA per ring entry: CTA k (blocks 1..) computes the k-th published
+// slice, so the hardware's block scheduler — not a software claim loop —
+// hands slices to free SM slots, exactly as in a one-launch team kernel.
+// A persistent consumer grid (each CTA looping over claimed slices) ran
+// 6 us (10%) slower than the one-launch kernel on the same pre-published
+// slices: every slice ended in a block barrier waiting for the service
+// thread's warp, whether the slice was claimed dynamically (atomic + ring
+// poll) or statically with the entry prefetched (67.7 vs 61.4 us).
+//
+// Wait until ring entry k carries this run's epoch: returns the sub-grid
+// id, -1 once the queue is closed below k, -2 on timeout.
+__device__ __noinline__ int queue_poll(const QueueDev* qd,
+                                       const unsigned long long* ring_d,
+                                       long long k, long long ring_cap,
+                                       unsigned epoch, long long timeout_ns) {
   const unsigned long long t0 = globaltimer();
   for (;;) {
     // this run publishes at most ring_cap ids: a slot beyond them is never
     // filled (and lies outside the ring)
     if (k >= ring_cap) return -1;
     // relaxed polls only: an acquire would invalidate the SM's L1
-    // (CCTL.IVALL) once per slice, under every CTA's spilled registers
     const unsigned long long v = ld_relaxed_gpu_u64(ring_d + k);
     if ((unsigned)(v >> 32) == epoch) return (int)(unsigned)v;
-    const long long fin = ld_relaxed_gpu(&qd->final_count);
+    const long long fin = fin_of(ld_relaxed_gpu(&qd->final_count), epoch);
     if (fin >= 0 && k >= fin) return -1;  // queue closed and drained
     if ((long long)(globaltimer() - t0) > timeout_ns) return -2;
-    __nanosleep(100);
+    __nanosleep(200);
   }
 }
 
-// DEPTH boxes per CTA: with DEPTH = 2 the next slice is claimed and its
-// stencil box is in flight (TMA) while the current one is computed.
-template <int N, int THREADS, int DEPTH>
+template <int N, int THREADS>
 __global__ void __launch_bounds__(THREADS, recon_min_blocks<THREADS>())
     k_queue_consumer(const __grid_constant__ CUtensorMap tmap,
                      const int* __restrict__ ring_h, QueueCtl* ctl,
                      unsigned long long* __restrict__ ring_d,
-                     long long ring_cap, QueueDev* qd, QueueDev* qd_next,
-                     unsigned epoch, double ax,
+                     long long ring_cap, QueueDev* qd,
+                     unsigned long long done_base, unsigned epoch, double ax,
                      double ay, double az, double* __restrict__ um,
                      double* __restrict__ up, double* __restrict__ F,
                      double* __restrict__ amax, int flux_form,
-                     long long timeout_ns) {
+                     long long timeout_ns, int early_loads) {
   using G = Geo<N>;
   constexpr int CELLS = G::CELLS;
   if (blockIdx.x == 0) {
-    queue_fetcher<THREADS>(ring_h, ctl, ring_d, qd, qd_next, epoch,
+    queue_fetcher<THREADS>(ring_h, ctl, ring_d, qd, epoch, done_base,
                            timeout_ns);
     return;
   }
+  // slice CTAs never gate the next run's launch: the fetcher does
+  pdl_trigger();
   extern __shared__ __align__(128) double sbox[];
-  __shared__ __align__(8) uint64_t bar[DEPTH];
+  __shared__ __align__(8) uint64_t bar;
   __shared__ double red[THREADS / 32];
-  __shared__ int s_g[DEPTH];
-  auto claim_into = [&](int d) {
-    const int g = queue_claim(qd, ring_d, ring_cap, epoch, timeout_ns);
-    s_g[d] = g;
+  __shared__ int s_g;
+  if (threadIdx.x == 0) mbar_init(&bar, 1);
+  // the box load waits for the previous kernel on the stream unless the
+  // caller vouched that it does not produce the pool (early_loads)
+  if (!early_loads) pdl_wait();
+  __syncthreads();  // initialised before the first arrive (k_recon_flux)
+  if (threadIdx.x == 0) {
+    const int g = queue_poll(qd, ring_d, (long long)blockIdx.x - 1, ring_cap,
+                             epoch, timeout_ns);
+    s_g = g;
     if (g >= 0) {
-      mbar_expect_tx(&bar[d], G::BOX * (uint32_t)sizeof(double));
-      tma_load_box(sbox + d * G::BOX, &tmap, 0, 1, 1, g, &bar[d]);
+      mbar_expect_tx(&bar, G::BOX * (uint32_t)sizeof(double));
+      tma_load_box(sbox, &tmap, 0, 1, 1, g, &bar);
     } else if (g == -2) {
       // nothing arrived in time: give the GPU back and tell the host
       st_release_sys(&ctl->status, 1);
     }
-  };
-  // the service thread claims slices, issues the box loads and counts
-  // completions: the LAST thread, which the z-pair split leaves idle at
-  // n = 8 (500 pairs over 512 threads), so the next slice's claim and box
-  // load overlap the compute instead of delaying warp 0's share of it
-  constexpr int kSvc = THREADS - 1;
-  const bool svc = threadIdx.x == kSvc;
-  if (svc)
-    for (int d = 0; d < DEPTH; ++d) mbar_init(&bar[d], 1);
-  __syncthreads();  // initialised before the first arrive (k_recon_flux)
-  if (svc) claim_into(0);
-  __syncthreads();
-  uint32_t phases = 0;
-  for (int i = 0;; ++i) {
-    const int d = DEPTH == 1 ? 0 : i % DEPTH;
-    const int g = s_g[d];
-    if (g < 0) break;
-    if (DEPTH > 1 && svc) claim_into((i + 1) % DEPTH);
-    mbar_wait(&bar[d], (phases >> d) & 1u);
-    phases ^= 1u << d;
-    const double speed = slice_compute<N, THREADS, 0, true>(
-        sbox + d * G::BOX, um + (int64_t)g * 3 * CELLS,
-        up + (int64_t)g * 3 * CELLS, F + (int64_t)g * 3 * CELLS, ax, ay, az,
-        flux_form);
-    if (amax != nullptr) block_max_store<THREADS>(speed, red, amax + g);
-    __syncthreads();  // box d consumed, this slice's stores issued
-    // the completion count is the host's busy signal only (the kernel's
-    // exit orders the outputs for the stream), so no fence before it: a
-    // fence here held the CTA until its stores drained (-5 us per run)
-    if (svc) {
-      atomicAdd(&qd->done, 1ULL);
-      if (DEPTH == 1) claim_into(0);
-    }
-    if (DEPTH == 1) __syncthreads();
   }
+  __syncthreads();
+  const int g = s_g;
+  if (g < 0) return;
+  mbar_wait(&bar, 0);
+  // the previous run on the stream writes the same outputs: its writes
+  // land first
+  if (early_loads) pdl_wait();
+  const double speed = slice_compute<N, THREADS, 0, true>(
+      sbox, um + (int64_t)g * 3 * CELLS, up + (int64_t)g * 3 * CELLS,
+      F + (int64_t)g * 3 * CELLS, ax, ay, az, flux_form);
+  if (amax != nullptr)
+    block_max_store<THREADS>(speed, red, amax + g);  // thread 0 stores last
+  else
+    __syncthreads();
+  // the completion count is the host's busy signal only (the kernel's exit
+  // orders the outputs for the stream), so no fence before it
+  if (threadIdx.x == 0) atomicAdd(&qd->done, 1ULL);
 }
 
 }  // namespace
@@ -1030,72 +1060,55 @@ int tf_recon_flux_ppm_f64(const double* pool_ext, int64_t pool_slices,
 
 namespace {
 
-// Box ring depth of the consumer: 2 (the next slice's box in flight while
-// the current one is computed) unless TASKFUSE_QUEUE_DEPTH=1 (A/B runs).
-int queue_depth() {
-  static const int d = [] {
-    const char* e = std::getenv("TASKFUSE_QUEUE_DEPTH");
-    return (e && e[0] == '1') ? 1 : 2;
-  }();
-  return d;
-}
-
-template <int N, int DEPTH>
-int consumer_occupancy(int* res) {
+template <int N>
+int consumer_launch(const CUtensorMap& map, cudaStream_t st,
+                    const int32_t* ring_h, QueueCtl* c, int64_t* ring_d,
+                    int64_t ring_cap, QueueDev* q, uint64_t done_base,
+                    int32_t epoch, double ax, double ay, double az,
+                    double* um, double* up, double* F, double* amax,
+                    int32_t flux_form, int64_t timeout_ns, int32_t flags) {
+  // flags: TF_QUEUE_CHAIN — launched as a programmatic dependent of the
+  // previous kernel on the stream; TF_LAUNCH_OVERLAP_PREV — and the first
+  // stencil boxes may load before that kernel completes
   constexpr int TH = 512;
-  const int smem = DEPTH * Geo<N>::BOX * (int)sizeof(double);
-  cudaError_t e = cudaFuncSetAttribute(
-      k_queue_consumer<N, TH, DEPTH>,
-      cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  if (e == cudaSuccess)
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-        res, k_queue_consumer<N, TH, DEPTH>, TH, smem);
-  return e;
-}
-
-template <int N, int DEPTH>
-void consumer_launch(const CUtensorMap& map, int ctas, cudaStream_t st,
-                     const int32_t* ring_h, QueueCtl* c, int64_t* ring_d,
-                     int64_t ring_cap, QueueDev* q, QueueDev* qn,
-                     int32_t epoch, double ax, double ay, double az,
-                     double* um, double* up, double* F, double* amax,
-                     int32_t flux_form, int64_t timeout_ns) {
-  constexpr int TH = 512;
-  k_queue_consumer<N, TH, DEPTH>
-      <<<ctas + 1, TH, DEPTH * Geo<N>::BOX * sizeof(double), st>>>(
-          map, ring_h, c, reinterpret_cast<unsigned long long*>(ring_d),
-          (long long)ring_cap, q, qn, (unsigned)epoch, ax, ay, az, um, up, F,
-          amax, flux_form, timeout_ns);
+  const int smem = Geo<N>::BOX * (int)sizeof(double);
+  static const cudaError_t attr_ok = cudaFuncSetAttribute(
+      k_queue_consumer<N, TH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      smem);
+  if (attr_ok != cudaSuccess) return attr_ok;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)ring_cap + 1);  // the fetcher + a CTA per entry
+  cfg.blockDim = dim3(TH);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = (flags & (TF_QUEUE_CHAIN | TF_LAUNCH_OVERLAP_PREV)) ? 1 : 0;
+  return cudaLaunchKernelEx(
+      &cfg, k_queue_consumer<N, TH>, map, (const int*)ring_h, c,
+      reinterpret_cast<unsigned long long*>(ring_d), (long long)ring_cap, q,
+      (unsigned long long)done_base, (unsigned)epoch, ax, ay, az, um, up, F,
+      amax, (int)flux_form, (long long)timeout_ns,
+      (flags & TF_LAUNCH_OVERLAP_PREV) ? 1 : 0);
 }
 
 }  // namespace
 
 extern "C" {
 
-int tf_queue_consumer_ctas(int32_t n) {
-  if (!valid_n(n)) return -TF_E_INVALID;
-  int dev = 0, sms = 0, res = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const bool two = queue_depth() == 2;
-  int e = n == 8 ? (two ? consumer_occupancy<8, 2>(&res)
-                        : consumer_occupancy<8, 1>(&res))
-                 : (two ? consumer_occupancy<16, 2>(&res)
-                        : consumer_occupancy<16, 1>(&res));
-  if (e != cudaSuccess) return -e;
-  return sms * (res > 0 ? res : 1);
-}
-
 int tf_queue_consumer_launch(const double* pool_ext, int64_t pool_slices,
                              int32_t n, const int32_t* ring_h, void* ctl_h,
                              int64_t* ring_d, int64_t ring_cap, void* qdev,
-                             void* qdev_next, int32_t ctas, int32_t epoch,
-                             double ax, double ay, double az, double* um,
-                             double* up, double* F, double* amax,
-                             int32_t flux_form, int64_t timeout_ns,
+                             uint64_t done_base, int32_t epoch, double ax,
+                             double ay, double az, double* um, double* up,
+                             double* F, double* amax, int32_t flux_form,
+                             int64_t timeout_ns, int32_t flags,
                              tf_stream_t stream) {
   if (!valid_n(n) || !pool_ext || !ring_h || !ctl_h || !ring_d || !qdev ||
-      ring_cap < 0 || ctas < 1 || epoch < 1 || !um || !up || !F)
+      ring_cap < 0 || ring_cap >= (1LL << 31) - 1 || epoch < 1 || !um ||
+      !up || !F || (flags & ~(TF_QUEUE_CHAIN | TF_LAUNCH_OVERLAP_PREV)))
     return TF_E_INVALID;
   CUtensorMap map;
   int rc = pool_map(pool_ext, pool_slices, n, &map);
@@ -1103,29 +1116,11 @@ int tf_queue_consumer_launch(const double* pool_ext, int64_t pool_slices,
   cudaStream_t st = (cudaStream_t)stream;
   QueueCtl* c = static_cast<QueueCtl*>(ctl_h);
   QueueDev* q = static_cast<QueueDev*>(qdev);
-  QueueDev* qn = static_cast<QueueDev*>(qdev_next);
-  // grid: the fetcher block + `ctas` consumers
-  const bool two = queue_depth() == 2;
-  if (n == 8) {
-    if (two)
-      consumer_launch<8, 2>(map, ctas, st, ring_h, c, ring_d, ring_cap, q, qn,
-                            epoch, ax, ay, az, um, up, F, amax, flux_form,
-                            timeout_ns);
-    else
-      consumer_launch<8, 1>(map, ctas, st, ring_h, c, ring_d, ring_cap, q, qn,
-                            epoch, ax, ay, az, um, up, F, amax, flux_form,
-                            timeout_ns);
-  } else {
-    if (two)
-      consumer_launch<16, 2>(map, ctas, st, ring_h, c, ring_d, ring_cap, q,
-                             qn, epoch, ax, ay, az, um, up, F, amax,
-                             flux_form, timeout_ns);
-    else
-      consumer_launch<16, 1>(map, ctas, st, ring_h, c, ring_d, ring_cap, q,
-                             qn, epoch, ax, ay, az, um, up, F, amax,
-                             flux_form, timeout_ns);
-  }
-  return cudaGetLastError();
+  auto go = [&](auto launch) {
+    return launch(map, st, ring_h, c, ring_d, ring_cap, q, done_base, epoch,
+                  ax, ay, az, um, up, F, amax, flux_form, timeout_ns, flags);
+  };
+  return n == 8 ? go(consumer_launch<8>) : go(consumer_launch<16>);
 }
 
 // device.py:237-252 enqueue_copy: a real stream-ordered copy (pinned host

@@ -11,8 +11,10 @@ from paper_2210_06438_b200.strategy3 import QueueExecutor, default_parents  # no
 
 wl = bench.Workload()
 arr = np.arange(wl.S, dtype=np.int32)
-for A in (1, 16, 64, 128):
-    q = QueueExecutor("reconstruct", A, default_parents(wl.S, A), wl.n)
+for A, early in ((1, False), (16, False), (64, False), (128, False),
+                 (1, True), (128, True)):
+    q = QueueExecutor("reconstruct", A, default_parents(wl.S, A), wl.n,
+                      early_loads=early)
     for k in range(10):
         q.run(wl.pools[k % 2], bench.VELOCITY, arr, wl.um, wl.up, wl.F,
               amax=wl.amax)
@@ -31,8 +33,9 @@ for A in (1, 16, 64, 128):
     torch.cuda.synchronize()
     gpu = e0.elapsed_time(e1) / K
     st = q.stats()
-    print(f"A={A}: gpu {gpu*1e3:.1f} us/iter, host q.run median "
+    print(f"A={A} early={early}: gpu {gpu*1e3:.1f} us/iter, host q.run median "
           f"{np.median(host)*1e6:.1f} us (min {min(host)*1e6:.1f}), "
+          f"{q.host_times()}, "
           f"teams {st['teams_formed']}, solo {st['solo_fast_path']}", flush=True)
     del q
 

@@ -1,0 +1,9 @@
+# Device queue after the PDL chain: its tests, the isolated consumer, the
+# real-time sweep, and the bench's realtime key.
+export TASKFUSE_NO_BUILD=1
+O=gpurun_out/q4
+mkdir -p $O
+timeout 600 python -m pytest tests/test_gpu_strategy3.py -q -x -k "queue" > $O/pytest.log 2>&1; echo "pytest exit $?" >> $O/pytest.log
+timeout 300 python scripts/exp_consumer.py > $O/consumer.log 2>&1
+timeout 300 python scripts/exp_queue.py > $O/queue.log 2>&1
+echo done

@@ -42,6 +42,13 @@ def test_bench_line_contract(cuda):
     # the timed outputs were checked against the oracle's digests
     assert d["self_check"]["bitexact_vs_oracle_digest"] is True
     assert e["result_check"] is True
+    # the headline forms its teams on the fly inside the timed step; the
+    # pre-formed plan rides along as a sub-key, equally checked
+    assert d["run"]["mode"] == "queue" and d["gpu_launches"] == 5
+    assert d["run"]["teams_per_step"] >= 1
+    assert sum(int(k) * v for k, v in d["run"]["team_histogram"].items()) \
+        >= 5 * 4096
+    assert d["plan"]["self_check"]["bitexact_vs_oracle_digest"] is True
 
 
 def test_bench_two_ranks_config5_gloo(cuda):

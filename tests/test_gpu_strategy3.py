@@ -295,21 +295,20 @@ def test_queue_consumer_gives_the_gpu_back_when_nothing_arrives(cuda):
     um, up, F = (torch.empty((S, 3, c, c, c), dtype=torch.float64,
                              device=cuda) for _ in range(3))
     ring_h = torch.zeros(S, dtype=torch.int32).pin_memory()
-    ctl_h = torch.tensor([0, -1, 0], dtype=torch.int64).pin_memory()
-    ring_d = torch.zeros(S, dtype=torch.int64, device=cuda)
-    qdev = torch.zeros(64, dtype=torch.int64, device=cuda)
-    qdev[16] = -1                       # final_count: not closed
-    ctas = lib.tf_queue_consumer_ctas(n)
+    ctl_h = torch.tensor([0, -1, 0, 0], dtype=torch.int64).pin_memory()
+    ring_d = torch.zeros(S + 2, dtype=torch.int64, device=cuda)
+    qdev = torch.zeros(64, dtype=torch.int64, device=cuda)  # epoch tag 0
     t0 = time.time()
     _lib.check(lib.tf_queue_consumer_launch(
         pool.data_ptr(), S, n, ring_h.data_ptr(), ctl_h.data_ptr(),
-        ring_d.data_ptr(), S, qdev.data_ptr(), None, ctas, 1, 1.0, 1.0, 1.0,
+        ring_d.data_ptr(), S, qdev.data_ptr(), 0, 1, 1.0, 1.0, 1.0,
         um.data_ptr(), up.data_ptr(), F.data_ptr(), None, 0,
-        5_000_000, torch.cuda.current_stream().cuda_stream),
+        5_000_000, 0, torch.cuda.current_stream().cuda_stream),
         "tf_queue_consumer_launch")
     torch.cuda.synchronize()
     assert time.time() - t0 < 5.0
     assert int(ctl_h[2]) == 0           # nothing completed
+    assert int(ctl_h[3]) == 1           # the timeout is reported
 
 
 @pytest.mark.parametrize("A", [1, 16, 128])
@@ -335,3 +334,53 @@ def test_device_launch_executor_bit_exact(cuda, cfg2, A):
     st = ex.stats()
     assert sum(k * v for k, v in st["size_histogram"].items()) == 2 * S
     assert max(st["size_histogram"]) <= A
+
+
+@pytest.mark.parametrize("early", [False, True])
+def test_queue_executor_overlapped_runs_bit_exact(cuda, cfg2, early):
+    """Runs issued back to back with no host synchronisation overlap on the
+    device (each consumer grid a programmatic dependent of the previous
+    one; slot counters monotonic, never reset).  Runs of varying size over
+    two different pools, each into its own outputs, some on a second stream
+    (ordered by events), then several runs into the SAME outputs (each
+    store waits for the previous run): every output equals its own run's
+    oracle."""
+    import torch
+    from paper_2210_06438_b200.strategy3 import QueueExecutor, default_parents
+    pool, n, vel, oum, oup, oF = cfg2
+    S = pool.shape[0]
+    grid = round(S ** (1 / 3)) * n
+    hp2 = HO.make_pool(HO.stress_field(grid), n)
+    HO.exchange_ghosts_pool(hp2, n, grid // n)
+    pool2 = torch.from_numpy(hp2).to(cuda)
+    o2 = HO.recon_flux_batch(hp2, n, vel)
+    pools = [(pool, (oum, oup, oF)), (pool2, o2)]
+    rng = np.random.default_rng(7)
+    q = QueueExecutor("flux", 64, default_parents(S, 64), n,
+                      early_loads=early)
+    side = torch.cuda.Stream()
+    runs = []
+    for k, size in enumerate((S, 7, 1500, S, 1, S, 333, S, S)):
+        ids = rng.choice(S, size=size, replace=False).astype(np.int32)
+        p, ref = pools[k % 2]
+        um, up, F = _outs(S, n, cuda)
+        s = side if k in (3, 4, 7) else torch.cuda.current_stream()
+        if s is side:
+            side.wait_stream(torch.cuda.current_stream())  # outputs' fill
+        q.run(p, vel, ids, um, up, F, stream=s)
+        runs.append((ids, ref, F, um, s))
+    # same outputs, alternating pools: the last run's values must win
+    um, up, F = _outs(S, n, cuda)
+    for k in range(6):
+        q.run(pools[k % 2][0], vel, np.arange(S, dtype=np.int32), um, up, F)
+    q.wait()
+    torch.cuda.synchronize()
+    for ids, ref, Fo, umo, _ in runs:
+        Fh, umh = Fo.cpu().numpy(), umo.cpu().numpy()
+        assert np.array_equal(Fh[ids], ref[2][ids])
+        assert np.array_equal(umh[ids], ref[0][ids])
+        rest = np.setdiff1d(np.arange(S), ids)
+        assert np.isnan(Fh[rest]).all()
+    last = pools[5 % 2][1]
+    assert np.array_equal(F.cpu().numpy(), last[2])
+    assert np.array_equal(up.cpu().numpy(), last[1])
