@@ -330,9 +330,13 @@ int tf_qexec_host_times(const tf_qexec* q, int64_t* out4);
  * (its timeout expired with slices unprocessed).  A run reusing a queue
  * slot reports a timeout of that slot's previous run the same way.        */
 int tf_qexec_wait(tf_qexec* q);
-/* ring_h/ctl_h: mapped pinned host ring + control block {published,
- * final_count, completed, status}; ring_d: device mirror of tagged entries
- * (epoch << 32 | id), ring_cap of them (the most this launch may publish),
+/* ring_h/ctl_h: mapped pinned host ring of tagged entries (epoch << 32 | id;
+ * an entry is published once its tag is this launch's epoch) + control
+ * block {published (unused), final_count (host: the count once closed, -1
+ * before), completed ((epoch << 32) | slices done, posted by the fetcher
+ * CTA), status (1: timed out)}; ring_d:
+ * device mirror of the tagged entries, ring_cap of them (the most this
+ * launch may publish),
  * zeroed once at allocation; epoch >= 1, new for every launch on that ring; the grid is
  * one fetcher CTA + one CTA per entry (CTA k computes entry k); qdev: {published,
  * final_count, spare, done}, one 128-B line each, zeroed once at allocation
@@ -344,7 +348,7 @@ int tf_qexec_wait(tf_qexec* q);
  * | TF_LAUNCH_OVERLAP_PREV = load them before (see tf_qexec_set_flags).    */
 #define TF_QUEUE_CHAIN 2
 int tf_queue_consumer_launch(const double* pool_ext, int64_t pool_slices,
-                             int32_t n, const int32_t* ring_h, void* ctl_h,
+                             int32_t n, const int64_t* ring_h, void* ctl_h,
                              int64_t* ring_d, int64_t ring_cap, void* qdev,
                              uint64_t done_base, int32_t epoch, double ax,
                              double ay, double az, double* um, double* up,

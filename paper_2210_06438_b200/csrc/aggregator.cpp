@@ -60,6 +60,8 @@ struct TeamStep {
 struct Team {
   int32_t parent = 0;
   int32_t state = FORMING;  // FORMING or the closure reason
+  uint32_t gen = 0;         // bumped each time the slot is reused
+  bool watching = false;    // holds a stream-idle watch (forming only)
   std::vector<int64_t> tags;
   // member bookkeeping after closure (aggregator.py:76-99,168-234)
   std::vector<TeamStep> steps;
@@ -91,6 +93,8 @@ class TeamTable {
     Slot& s = slots_[id];
     s.alive = true;
     Team& t = s.team;
+    t.gen += 1;
+    t.watching = false;
     t.parent = parent;
     t.state = FORMING;
     t.tags.clear();
@@ -123,6 +127,14 @@ class TeamTable {
   std::vector<int64_t> free_;
 };
 
+// A stream-idle watch: the team's slot id and its generation, so a watch
+// left behind by a team that closed at its cap (the slot since recycled)
+// is recognised as stale instead of searched for and erased at the close.
+struct Watch {
+  int64_t id;
+  uint32_t gen;
+};
+
 }  // namespace
 
 struct tf_region {
@@ -134,8 +146,11 @@ struct tf_region {
   int32_t next_parent = 0;  // == arrivals % parents.size(), kept incrementally
   TeamTable teams;
   // per executor: forming teams holding a stream-idle watch, in watch order
-  std::vector<std::vector<int64_t>> watchers;
-  std::vector<int64_t> fire_scratch;  // tf_region_stream_idle's swap buffer
+  // (plus stale watches of teams that closed at their cap since, skipped
+  // and dropped by the next tf_region_stream_idle), and the live count
+  std::vector<std::vector<Watch>> watchers;
+  std::vector<int32_t> live_watch;
+  std::vector<Watch> fire_scratch;  // tf_region_stream_idle's swap buffer
   int64_t teams_formed = 0;
   int64_t solo_fast_path = 0;
   int64_t histogram[TF_MAX_TEAM + 1] = {0};
@@ -152,10 +167,13 @@ void close_team(tf_region* r, int64_t id, Team& t, int reason) {
   (void)id;
 }
 
-void unwatch(tf_region* r, int32_t executor, int64_t id) {
-  auto& w = r->watchers[executor];
-  auto it = std::find(w.begin(), w.end(), id);
-  if (it != w.end()) w.erase(it);
+// O(1): the watch entry stays in the list, stale (a linear search + erase
+// per cap closure made formation quadratic in the forming teams — A = 4 on
+// 4096 arrivals keeps ~1000 teams forming)
+void unwatch(tf_region* r, int32_t executor, Team& t) {
+  if (!t.watching) return;
+  t.watching = false;
+  r->live_watch[executor] -= 1;
 }
 
 }  // namespace
@@ -176,6 +194,7 @@ int tf_region_create(const char* name, int32_t max_team, int32_t parent_count,
   for (int32_t i = 0; i < parent_count; ++i)
     r->parents[i].executor = (int32_t)((lead + (uint32_t)i) % (uint32_t)executors);
   r->watchers.resize(executors);
+  r->live_watch.assign(executors, 0);
   *out = r;
   return 0;
 }
@@ -208,7 +227,7 @@ int tf_region_enter(tf_region* r, int64_t tag, tf_busy_fn busy, void* ctx,
     // cap reached (max_team 1 closes instantly)           aggregator.py:310
     if (p.forming == id) {
       p.forming = -1;
-      unwatch(r, p.executor, id);
+      unwatch(r, p.executor, t);
     }
     close_team(r, id, t, CAP);
     out->closed = CAP;
@@ -222,7 +241,20 @@ int tf_region_enter(tf_region* r, int64_t tag, tf_busy_fn busy, void* ctx,
       out->closed = SOLO;
     } else {
       p.forming = id;  // watch the stream for its drain  aggregator.py:321
-      r->watchers[p.executor].push_back(id);
+      auto& w = r->watchers[p.executor];
+      if (w.size() > 2 * (size_t)r->live_watch[p.executor] + 64) {
+        // drop the stale watches (order kept) so that a stream that never
+        // drains does not grow the list without bound
+        w.erase(std::remove_if(w.begin(), w.end(),
+                               [&](const Watch& x) {
+                                 const Team* u = r->teams.get(x.id);
+                                 return !u || u->gen != x.gen || !u->watching;
+                               }),
+                w.end());
+      }
+      w.push_back(Watch{id, t.gen});
+      t.watching = true;
+      r->live_watch[p.executor] += 1;
     }
   }
   return 0;
@@ -232,21 +264,26 @@ int tf_region_stream_idle(tf_region* r, int32_t executor, int64_t* out_teams,
                           int32_t cap) {
   if (!r || executor < 0 || executor >= r->executors) return -TF_E_INVALID;
   if (cap < 0 || (cap > 0 && !out_teams)) return -TF_E_INVALID;
-  std::vector<int64_t>& fire = r->fire_scratch;
+  std::vector<Watch>& fire = r->fire_scratch;
   fire.swap(r->watchers[executor]);  // keeps both buffers' capacity
   int32_t n = 0;
-  for (int64_t id : fire) {
+  for (const Watch& w : fire) {
+    const int64_t id = w.id;
     Team* t = r->teams.get(id);
-    if (!t || t->state != FORMING) continue;
+    // stale: the team closed at its cap (and its slot may be reused)
+    if (!t || t->gen != w.gen || !t->watching || t->state != FORMING)
+      continue;
     if (n == cap) {
       // no room to report it: it keeps watching, so the caller's next call
       // (sized by tf_region_watch_count) closes it — a team is never closed
       // without its id reaching the caller
-      r->watchers[executor].push_back(id);
+      r->watchers[executor].push_back(w);
       continue;
     }
     Parent& p = r->parents[t->parent];
     if (p.forming == id) p.forming = -1;  // aggregator.py:328-332
+    t->watching = false;
+    r->live_watch[executor] -= 1;
     close_team(r, id, *t, DRAIN);
     out_teams[n++] = id;
   }
@@ -256,7 +293,7 @@ int tf_region_stream_idle(tf_region* r, int32_t executor, int64_t* out_teams,
 
 int32_t tf_region_watch_count(const tf_region* r, int32_t executor) {
   if (!r || executor < 0 || executor >= r->executors) return -TF_E_INVALID;
-  return (int32_t)r->watchers[executor].size();
+  return r->live_watch[executor];
 }
 
 int tf_region_team_size(const tf_region* r, int64_t team) {
@@ -510,7 +547,7 @@ int launch_team(tf_executor* ex, int64_t team, const ReconArgs& a,
 
 int drain_executor(tf_executor* ex, int32_t e, const ReconArgs& a,
                    int64_t* launches) {
-  std::vector<int64_t> closed(ex->region->watchers[e].size());
+  std::vector<int64_t> closed(ex->region->live_watch[e]);
   if (closed.empty()) return 0;
   const int n = tf_region_stream_idle(ex->region, e, closed.data(),
                                       (int32_t)closed.size());
@@ -584,13 +621,13 @@ int tf_executor_run_recon_flux(tf_executor* ex, const double* pool_ext,
     // team, observe whether that parent's stream has gone idle meanwhile
     const int32_t pi = r->next_parent;
     const int32_t pe = r->parents[pi].executor;
-    if (!r->watchers[pe].empty() && !rt_busy(ex, pe)) {
+    if (r->live_watch[pe] > 0 && !rt_busy(ex, pe)) {
       int rc = drain_executor(ex, pe, a, launches);
       if (rc) return rc;
     }
     if ((i & 31) == 31) {
       for (int32_t e = 0; e < E; ++e)
-        if (e != pe && !r->watchers[e].empty() && !rt_busy(ex, e)) {
+        if (e != pe && r->live_watch[e] > 0 && !rt_busy(ex, e)) {
           int rc = drain_executor(ex, e, a, launches);
           if (rc) return rc;
         }
@@ -661,7 +698,7 @@ int tf_executor_sync(tf_executor* ex) {
 struct QueueCtlHost {   // mirrors QueueCtl (hydro_kernels.cu)
   long long published;
   long long final_count;
-  long long completed;
+  long long completed;    // (epoch << 32) | slices done
   long long status;       // 1: the consumer grid timed out
 };
 struct QueueDevInit {   // mirrors QueueDev (one 128-B line per word)
@@ -681,8 +718,8 @@ struct QueueDevInit {   // mirrors QueueDev (one 128-B line per word)
 struct QueueSlot {
   QueueCtlHost* ctl_h = nullptr;   // mapped pinned
   void* ctl_hd = nullptr;          // its device alias
-  int32_t* ring_h = nullptr;       // mapped pinned
-  int32_t* ring_hd = nullptr;      // its device alias
+  int64_t* ring_h = nullptr;       // mapped pinned, tagged (epoch << 32 | id)
+  int64_t* ring_hd = nullptr;      // its device alias
   int64_t* ring_d = nullptr;       // device mirror, tagged (epoch << 32 | id)
   int32_t epoch = 0;               // last epoch launched on this slot
   int64_t ring_cap = 0;
@@ -717,9 +754,17 @@ int64_t q_now_ns() {
       .count();
 }
 
-int64_t q_done(const tf_qexec* q) {
-  return __atomic_load_n(&q->slot().ctl_h->completed, __ATOMIC_ACQUIRE);
+// a GPU-written count, if it carries the slot's current epoch
+int64_t q_tagged(const long long* word, int32_t epoch) {
+  const uint64_t v = (uint64_t)__atomic_load_n(word, __ATOMIC_ACQUIRE);
+  return (uint32_t)(v >> 32) == (uint32_t)epoch ? (int64_t)(uint32_t)v : 0;
 }
+
+int64_t q_slot_done(const QueueSlot& S) {
+  return q_tagged(&S.ctl_h->completed, S.epoch);
+}
+
+int64_t q_done(const tf_qexec* q) { return q_slot_done(q->slot()); }
 
 // busy = published slices not all completed.  No clock: the completion
 // count lives in host memory (the fetcher CTA writes it), so a read costs a
@@ -741,10 +786,13 @@ void q_publish(tf_qexec* q, int64_t team) {
   if (!t) return;
   QueueSlot& S = q->slot();
   tf_nvtx::TeamRange range("team publish", (int64_t)t->tags.size());
-  for (int64_t tag : t->tags) S.ring_h[q->published++] = (int32_t)tag;
-  // ids first, then the count (release): the consumer acquires the count
-  __atomic_store_n(&S.ctl_h->published, (long long)q->published,
-                   __ATOMIC_RELEASE);
+  // entries carry the run's epoch: the fetcher reads them speculatively and
+  // takes the tagged ones, so a team costs its stores and no shared counter
+  // (a release store per team to a line the GPU polls was the cost of a
+  // closure at small A)
+  const int64_t tagged = (int64_t)((uint64_t)(uint32_t)S.epoch << 32);
+  for (int64_t tag : t->tags)
+    S.ring_h[q->published++] = tagged | (int64_t)(uint32_t)tag;
   r->teams.release(team);
 }
 
@@ -771,13 +819,14 @@ int q_drain_slot(QueueSlot& S) {
   for (uint64_t spins = 0;; ++spins) {
     if (__atomic_load_n(&S.ctl_h->status, __ATOMIC_ACQUIRE))
       return q_reset_slot(S);
-    if (__atomic_load_n(&S.ctl_h->completed, __ATOMIC_ACQUIRE) >= S.count)
+    if (S.count == 0 ||
+        q_slot_done(S) >= S.count)
       break;
     if ((spins & 1023) == 1023) {
       // a failed or finished stream that never reported every slice
       const cudaError_t e = cudaStreamQuery(S.stream);
       if (e == cudaSuccess &&
-          __atomic_load_n(&S.ctl_h->completed, __ATOMIC_ACQUIRE) < S.count)
+          q_slot_done(S) < S.count)
         return q_reset_slot(S);
       if (e != cudaSuccess && e != cudaErrorNotReady) return e;
     }
@@ -877,8 +926,10 @@ int tf_qexec_run_recon_flux(tf_qexec* q, const double* pool_ext,
     S.ring_h = nullptr;
     S.ring_d = nullptr;
     const int64_t cap = count > 0 ? count : 1;
-    cudaError_t e = cudaHostAlloc(&S.ring_h, sizeof(int32_t) * cap,
+    cudaError_t e = cudaHostAlloc(&S.ring_h, sizeof(int64_t) * cap,
                                   cudaHostAllocMapped);
+    // no host entry may carry a live epoch before it is published
+    if (e == cudaSuccess) std::fill(S.ring_h, S.ring_h + cap, int64_t{0});
     if (e == cudaSuccess)
       e = cudaHostGetDevicePointer(reinterpret_cast<void**>(&S.ring_hd),
                                    S.ring_h, 0);
@@ -918,13 +969,13 @@ int tf_qexec_run_recon_flux(tf_qexec* q, const double* pool_ext,
   int64_t teams = 0;
   std::vector<int64_t> closed;
   auto drain = [&]() {
-    closed.assign(r->watchers[0].begin(), r->watchers[0].end());
+    closed.resize(r->live_watch[0]);
     const int k = tf_region_stream_idle(r, 0, closed.data(),
                                         (int32_t)closed.size());
     for (int i = 0; i < k; ++i, ++teams) q_publish(q, closed[i]);
   };
   for (int64_t i = 0; i < count; ++i) {
-    if (!r->watchers[0].empty() && !q_busy(q, 0)) drain();
+    if (r->live_watch[0] > 0 && !q_busy(q, 0)) drain();
     tf_enter_result res;
     rc = tf_region_enter(r, ids[i], q_busy, q, &res);
     if (rc) break;

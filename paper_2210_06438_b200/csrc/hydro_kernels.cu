@@ -510,9 +510,10 @@ bool valid_n(int n) { return n == 8 || n == 16; }
 // pinned memory — a team closure costs a few host stores instead of a
 // kernel launch.  Control block (mapped pinned memory):
 struct QueueCtl {
-  long long published;    // slices published so far (monotonic)
-  long long final_count;  // -1 while more may come
-  long long completed;    // slices finished (written by the fetcher only)
+  long long published;    // (host bookkeeping; the fetcher reads the tags)
+  long long final_count;  // host -> GPU: the run's count once closed, or -1
+  long long completed;    // GPU -> host: (epoch << 32) | slices done (the
+                          //   fetcher is its only writer)
   long long status;       // 0 ok; 1 a fetcher / consumer timed out
 };
 // device-side mirror, polled by the consumers through L2 (only the fetcher
@@ -554,13 +555,11 @@ __device__ __forceinline__ void st_release_gpu(long long* p, long long v) {
   asm volatile("st.release.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
-__device__ __forceinline__ int ld_relaxed_sys(const int* p) {
-  int v;
-  asm volatile("ld.relaxed.sys.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
 __device__ __forceinline__ void st_release_sys(long long* p, long long v) {
   asm volatile("st.release.sys.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void st_relaxed_sys(long long* p, long long v) {
+  asm volatile("st.relaxed.sys.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 __device__ __forceinline__ unsigned long long globaltimer() {
   unsigned long long t;
@@ -592,83 +591,92 @@ __device__ __forceinline__ long long fin_of(long long tagged, unsigned epoch) {
              : -1;
 }
 
-// Block 0 is the fetcher: it mirrors newly published ids from the host ring
-// into device memory (all its threads, several independent PCIe reads in
-// flight per thread — one warp reading 32 ids per round trip was the
-// bottleneck), forwards the close marker, and reports the device-side
-// completion count back to the host.  Blocks 1.. are consumers polling the
-// device mirror.  The slot's device counters are monotonic across runs:
-// `done` counts from done_base (the slices of the slot's earlier runs).
+__device__ __forceinline__ unsigned long long ld_relaxed_sys_u64(
+    const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.sys.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Block 0 is the fetcher: it mirrors the host ring into device memory and
+// reports the device-side completion count back to the host.  Host entries
+// carry the run's epoch like the device ones ((epoch << 32) | id), so a
+// round reads the ring SPECULATIVELY — no round trip for a published count
+// first: every entry read with this run's tag is mirrored (all threads,
+// several independent PCIe reads in flight each), the valid prefix advances
+// the cursor, and the close marker (final_count) rides in the same round
+// trip.  Blocks 1.. compute the slices (k_queue_consumer).  The slot's
+// `done` counter is monotonic across runs: this run counts from done_base.
 template <int THREADS>
-__device__ void queue_fetcher(const int* __restrict__ ring_h, QueueCtl* ctl,
+__device__ void queue_fetcher(const unsigned long long* __restrict__ ring_h,
+                              QueueCtl* ctl,
                               unsigned long long* __restrict__ ring_d,
-                              QueueDev* qd, unsigned epoch,
+                              long long ring_cap, QueueDev* qd, unsigned epoch,
                               unsigned long long done_base,
                               long long timeout_ns) {
-  __shared__ long long s_pub, s_fin, s_done;
-  __shared__ int s_stop;
-  constexpr int U = 4;                  // loads in flight per thread
-  constexpr int CHUNK = THREADS * U;    // ids mirrored per publish
-  long long fetched = 0, reported = -1;
+  __shared__ long long s_fin;
+  __shared__ int s_bad, s_stop;
+  constexpr int U = 8;                  // loads in flight per thread
+  constexpr int CHUNK = THREADS * U;    // entries read per round
+  long long fetched = 0, fin_sent = -1, reported = -1;
+  int span = CHUNK;                     // 32 after a round without progress
   bool triggered = false;
   unsigned long long last_change = globaltimer();
-  // phase 1: mirror ids as the host publishes them, until the queue is
-  // closed and every id has been mirrored
+  // phase 1: mirror entries as the host publishes them, until the queue is
+  // closed and every entry below the close is mirrored
   for (;;) {
+    const long long end = fin_sent >= 0 ? fin_sent : ring_cap;
+    const long long lim = fetched + span < end ? fetched + span : end;
     if (threadIdx.x == 0) {
-      // published and final_count in ONE PCIe round trip (adjacent words;
-      // the fence orders the ring reads after them)
-      long long pub, fin;
-      asm volatile("ld.relaxed.sys.global.v2.b64 {%0, %1}, [%2];"
-                   : "=l"(pub), "=l"(fin)
-                   : "l"(&ctl->published)
-                   : "memory");
-      asm volatile("fence.acq_rel.sys;" ::: "memory");
-      s_pub = pub;
-      s_fin = fin;
-      s_done = (long long)(atomicAdd(&qd->done, 0ULL) - done_base);
+      s_bad = CHUNK;
+      s_fin = (long long)ld_relaxed_sys_u64(
+          reinterpret_cast<const unsigned long long*>(&ctl->final_count));
+    }
+    unsigned long long v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const long long k = fetched + u * THREADS + threadIdx.x;
+      v[u] = k < lim ? ld_relaxed_sys_u64(ring_h + k) : 0ULL;
+    }
+    __syncthreads();  // s_bad initialised
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const long long k = fetched + u * THREADS + threadIdx.x;
+      if (k < lim) {
+        // a consumer that sees its run's epoch in the slot has the id —
+        // no fence, no acquire (and no L1 invalidation) needed
+        if ((unsigned)(v[u] >> 32) == epoch)
+          ring_d[k] = v[u];
+        else
+          atomicMin(&s_bad, u * THREADS + (int)threadIdx.x);
+      }
     }
     __syncthreads();
-    const long long pub = s_pub, fin = s_fin, done = s_done;
-    // publish chunk by chunk: the consumers start on the first CHUNK ids
-    // instead of waiting for the whole backlog to be mirrored
-    for (long long k0 = fetched; k0 < pub; k0 += CHUNK) {
-      int v[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const long long k = k0 + u * THREADS + threadIdx.x;
-        v[u] = k < pub ? ld_relaxed_sys(ring_h + k) : 0;
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const long long k = k0 + u * THREADS + threadIdx.x;
-        // tagged entry: a consumer that sees its run's epoch in the slot
-        // has the id — no acquire (and no L1 invalidation) needed
-        if (k < pub)
-          ring_d[k] = ((unsigned long long)epoch << 32) | (unsigned)v[u];
-      }
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        __threadfence();
-        st_release_gpu(&qd->published, k0 + CHUNK < pub ? k0 + CHUNK : pub);
-      }
-      last_change = globaltimer();
-    }
-    if (pub > fetched) fetched = pub;
+    const long long fin = s_fin;
+    const long long valid = s_bad < lim - fetched ? s_bad : lim - fetched;
+    fetched += valid;
+    span = valid > 0 ? CHUNK : 32;
+    if (valid > 0) last_change = globaltimer();
     if (!triggered) {
-      // the first ids are out: wait for the previous run (its tail overlaps
-      // this mirror), then let the next run launch
+      // the first entries are out: wait for the previous run (its tail
+      // overlaps this mirror), then let the next run launch
       pdl_wait();
       pdl_trigger();
       triggered = true;
     }
     if (threadIdx.x == 0) {
-      if (fin >= 0 && fetched >= fin)
+      if (fin >= 0 && fin_sent < 0)
+        // the close marker as soon as it is known: CTAs beyond it exit
         st_release_gpu(&qd->final_count,
                        (long long)(((unsigned long long)epoch << 32) |
                                    (unsigned long long)fin));
+      const long long done =
+          (long long)(ld_relaxed_gpu_u64(&qd->done) - done_base);
       if (done != reported) {
-        st_release_sys(&ctl->completed, done);
+        st_relaxed_sys(&ctl->completed,
+                       (long long)(((unsigned long long)epoch << 32) |
+                                   (unsigned long long)done));
+        reported = done;
         last_change = globaltimer();
       }
       int stop = fin >= 0 && fetched >= fin ? 1 : 0;
@@ -681,22 +689,25 @@ __device__ void queue_fetcher(const int* __restrict__ ring_h, QueueCtl* ctl,
       }
       s_stop = stop;
     }
-    reported = done;
+    if (fin >= 0 && fin_sent < 0) fin_sent = fin;
     __syncthreads();
     if (s_stop) break;
-    __nanosleep(100);
+    if (valid == 0) __nanosleep(100);
   }
   if (threadIdx.x != 0) return;
-  // phase 2 (one thread): every id is on the device; report completions to
-  // the host until all are done — device-side polling only, no PCIe reads,
-  // so the grid exits as soon as the last slice does
+  // phase 2 (one thread): every entry is on the device; post completions to
+  // the host until all are done — relaxed device loads and relaxed posted
+  // stores (a system-scope release per update cost microseconds each, and
+  // the run's grid ends only when this loop sees the last slice)
   if (s_stop != 2) {
-    const long long fin = fin_of(ld_acquire_gpu(&qd->final_count), epoch);
+    const long long fin = fin_sent;
+    const unsigned long long tag = (unsigned long long)epoch << 32;
     for (;;) {
-      const long long done = (long long)(
-          ld_acquire_gpu_u64(&qd->done) - done_base);
+      const long long done =
+          (long long)(ld_relaxed_gpu_u64(&qd->done) - done_base);
       if (done != reported) {
-        st_release_sys(&ctl->completed, done);
+        st_relaxed_sys(&ctl->completed,
+                       (long long)(tag | (unsigned long long)done));
         reported = done;
         last_change = globaltimer();
       }
@@ -743,8 +754,8 @@ __device__ __noinline__ int queue_poll(const QueueDev* qd,
 template <int N, int THREADS>
 __global__ void __launch_bounds__(THREADS, recon_min_blocks<THREADS>())
     k_queue_consumer(const __grid_constant__ CUtensorMap tmap,
-                     const int* __restrict__ ring_h, QueueCtl* ctl,
-                     unsigned long long* __restrict__ ring_d,
+                     const unsigned long long* __restrict__ ring_h,
+                     QueueCtl* ctl, unsigned long long* __restrict__ ring_d,
                      long long ring_cap, QueueDev* qd,
                      unsigned long long done_base, unsigned epoch, double ax,
                      double ay, double az, double* __restrict__ um,
@@ -754,8 +765,8 @@ __global__ void __launch_bounds__(THREADS, recon_min_blocks<THREADS>())
   using G = Geo<N>;
   constexpr int CELLS = G::CELLS;
   if (blockIdx.x == 0) {
-    queue_fetcher<THREADS>(ring_h, ctl, ring_d, qd, epoch, done_base,
-                           timeout_ns);
+    queue_fetcher<THREADS>(ring_h, ctl, ring_d, ring_cap, qd, epoch,
+                           done_base, timeout_ns);
     return;
   }
   // slice CTAs never gate the next run's launch: the fetcher does
@@ -796,7 +807,8 @@ __global__ void __launch_bounds__(THREADS, recon_min_blocks<THREADS>())
   else
     __syncthreads();
   // the completion count is the host's busy signal only (the kernel's exit
-  // orders the outputs for the stream), so no fence before it
+  // orders the outputs for the stream), so no fence before it: a fence (or
+  // a system-scope store) here holds the CTA until its stores drain
   if (threadIdx.x == 0) atomicAdd(&qd->done, 1ULL);
 }
 
@@ -1062,7 +1074,7 @@ namespace {
 
 template <int N>
 int consumer_launch(const CUtensorMap& map, cudaStream_t st,
-                    const int32_t* ring_h, QueueCtl* c, int64_t* ring_d,
+                    const int64_t* ring_h, QueueCtl* c, int64_t* ring_d,
                     int64_t ring_cap, QueueDev* q, uint64_t done_base,
                     int32_t epoch, double ax, double ay, double az,
                     double* um, double* up, double* F, double* amax,
@@ -1087,7 +1099,8 @@ int consumer_launch(const CUtensorMap& map, cudaStream_t st,
   cfg.attrs = attr;
   cfg.numAttrs = (flags & (TF_QUEUE_CHAIN | TF_LAUNCH_OVERLAP_PREV)) ? 1 : 0;
   return cudaLaunchKernelEx(
-      &cfg, k_queue_consumer<N, TH>, map, (const int*)ring_h, c,
+      &cfg, k_queue_consumer<N, TH>, map,
+      reinterpret_cast<const unsigned long long*>(ring_h), c,
       reinterpret_cast<unsigned long long*>(ring_d), (long long)ring_cap, q,
       (unsigned long long)done_base, (unsigned)epoch, ax, ay, az, um, up, F,
       amax, (int)flux_form, (long long)timeout_ns,
@@ -1099,7 +1112,7 @@ int consumer_launch(const CUtensorMap& map, cudaStream_t st,
 extern "C" {
 
 int tf_queue_consumer_launch(const double* pool_ext, int64_t pool_slices,
-                             int32_t n, const int32_t* ring_h, void* ctl_h,
+                             int32_t n, const int64_t* ring_h, void* ctl_h,
                              int64_t* ring_d, int64_t ring_cap, void* qdev,
                              uint64_t done_base, int32_t epoch, double ax,
                              double ay, double az, double* um, double* up,

@@ -11,8 +11,9 @@ from paper_2210_06438_b200 import _lib  # noqa: E402
 lib = _lib.load(build_if_missing=False)
 wl = bench.Workload()
 S = wl.S
-ring_h = torch.arange(S, dtype=torch.int32).pin_memory()
-ctl_h = torch.tensor([S, S, 0, 0], dtype=torch.int64).pin_memory()
+ids = torch.arange(S, dtype=torch.int64)
+ring_h = ids.clone().pin_memory()  # tagged per run: (epoch << 32) | id
+ctl_h = torch.tensor([S, S, 0, 0, 0], dtype=torch.int64).pin_memory()
 ring_d = torch.zeros(S + 2, dtype=torch.int64, device="cuda")  # tagged entries
 # QueueDev: published, final_count, claim, done, one 128-B line each
 init = torch.zeros(64, dtype=torch.int64, device="cuda")
@@ -23,6 +24,7 @@ st = torch.cuda.current_stream()
 
 
 def run(k):
+    ring_h.copy_(ids | ((k + 1) << 32))
     qdev.copy_(init)
     ctl_h[2] = 0
     rc = lib.tf_queue_consumer_launch(

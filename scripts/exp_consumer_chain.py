@@ -17,18 +17,30 @@ st = torch.cuda.current_stream()
 slots = []
 for _ in range(2):
     slots.append({
-        "ring_h": torch.arange(S, dtype=torch.int32).pin_memory(),
-        "ctl_h": torch.tensor([S, S, 0, 0], dtype=torch.int64).pin_memory(),
+        "ctl_h": torch.tensor([S, S, 0, 0, 0], dtype=torch.int64).pin_memory(),
         "ring_d": torch.zeros(S + 2, dtype=torch.int64, device="cuda"),
         "qdev": torch.zeros(64, dtype=torch.int64, device="cuda"),
         "epoch": 0, "done": 0})
+
+
+rings = {}
+ORDER = torch.arange(S, dtype=torch.int64)
+
+
+def ring(epoch):
+    """The host ring as published for `epoch` (read-only for the GPU, so
+    runs of both slots with the same epoch share it)."""
+    key = (epoch, id(ORDER))
+    if key not in rings:
+        rings[key] = (ORDER | (epoch << 32)).pin_memory()
+    return rings[key]
 
 
 def run(k, flags):
     s = slots[k % 2]
     s["epoch"] += 1
     rc = lib.tf_queue_consumer_launch(
-        wl.pools[k % 2].data_ptr(), S, 8, s["ring_h"].data_ptr(),
+        wl.pools[k % 2].data_ptr(), S, 8, ring(s["epoch"]).data_ptr(),
         s["ctl_h"].data_ptr(), s["ring_d"].data_ptr(), S,
         s["qdev"].data_ptr(), s["done"], s["epoch"], 1.0, 1.0, 1.0,
         wl.um.data_ptr(), wl.up.data_ptr(), wl.F.data_ptr(),
@@ -57,6 +69,14 @@ for name, flags in (("chained+early", 3), ("chained", 2), ("plain", 0)):
     mn, med = timeit(lambda k: run(k, flags))
     print(f"consumer {name:14s}: min {mn:.1f} us  median {med:.1f} us "
           f"per {S} slices", flush=True)
+# the order the formation core publishes at A = 128 (strided teams: parent
+# = arrival % 32, so a team's members are 32 sub-grids apart)
+from paper_2210_06438_b200.strategy3 import form_teams  # noqa: E402
+ORDER = torch.tensor([g for t in form_teams(range(S), 128, 1)
+                      for g in t.ids], dtype=torch.int64)
+mn, med = timeit(lambda k: run(k, 3))
+print(f"consumer chained+early, A=128 team order: min {mn:.1f} us  "
+      f"median {med:.1f} us", flush=True)
 single = bench.single_runner(wl)
 mn, med = timeit(single)
 print(f"one launch           : min {mn:.1f} us  median {med:.1f} us")

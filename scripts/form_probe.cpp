@@ -6,7 +6,7 @@ static volatile long long completed = 0;
 static long long published = 0, seen = 0;
 int busy(void*, int32_t) { if (published != seen) { seen = published; return 1; } return completed < published; }
 int main() {
-  for (int A : {1, 16, 64, 128}) {
+  for (int A : {1, 4, 16, 64, 128}) {
     tf_region* r; int P = 4096 / A; if (P < 1) P = 1;
     tf_region_create("reconstruct", A, P, 1, &r);
     std::vector<int64_t> buf(8192);

@@ -1,5 +1,5 @@
 export TASKFUSE_NO_BUILD=1
-O=gpurun_out/q7
+O=gpurun_out/q10
 mkdir -p $O
 timeout 300 python scripts/exp_consumer_chain.py > $O/chain.log 2>&1
 echo done

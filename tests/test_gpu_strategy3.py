@@ -294,8 +294,8 @@ def test_queue_consumer_gives_the_gpu_back_when_nothing_arrives(cuda):
                        device=cuda)
     um, up, F = (torch.empty((S, 3, c, c, c), dtype=torch.float64,
                              device=cuda) for _ in range(3))
-    ring_h = torch.zeros(S, dtype=torch.int32).pin_memory()
-    ctl_h = torch.tensor([0, -1, 0, 0], dtype=torch.int64).pin_memory()
+    ring_h = torch.zeros(S, dtype=torch.int64).pin_memory()  # untagged
+    ctl_h = torch.tensor([0, -1, 0, 0, 0], dtype=torch.int64).pin_memory()
     ring_d = torch.zeros(S + 2, dtype=torch.int64, device=cuda)
     qdev = torch.zeros(64, dtype=torch.int64, device=cuda)  # epoch tag 0
     t0 = time.time()
@@ -307,7 +307,7 @@ def test_queue_consumer_gives_the_gpu_back_when_nothing_arrives(cuda):
         "tf_queue_consumer_launch")
     torch.cuda.synchronize()
     assert time.time() - t0 < 5.0
-    assert int(ctl_h[2]) == 0           # nothing completed
+    assert int(ctl_h[2]) & 0xFFFFFFFF == 0  # nothing completed (epoch tag)
     assert int(ctl_h[3]) == 1           # the timeout is reported
 
 
