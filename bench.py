@@ -1020,6 +1020,34 @@ def peer_access_ok(part, local) -> bool:
     return True
 
 
+def cfg5_one_gpu(args, local, peak):
+    """Config 5's step on ONE GPU, in the N = 1 line: the denominator of a
+    scaling curve whose N > 1 lines run config 5 (the N = 1 headline itself
+    is config 2, BASELINE's metric config).  Same path as the N > 1
+    headline — the march kernel with the exchange fused (here the periodic
+    x halo), a device peer barrier per iteration."""
+    import torch
+    from paper_2210_06438_b200.field import PeerSlabFieldIteration
+    from paper_2210_06438_b200.parallel_halo import SlabPartition
+    grid, n = args.cfg5_grid, N_SUB
+    part = SlabPartition(grid, n, 1, 0)
+    dev = torch.device("cuda", local)
+    peer = PeerSlabFieldIteration(part, cfg5_slab(part, grid), VELOCITY,
+                                  device=dev)
+    ms = timed(lambda k: peer.iteration(), args.steps, args.warmup, 1,
+               torch.cuda.current_stream())
+    peer.check()
+    del peer
+    torch.cuda.empty_cache()
+    floor = grid ** 3 * 16 / (ms * 1e-3) / 1e9
+    return {"value": rate((grid // n) ** 3, n, ms), "unit": UNIT,
+            "ms_per_step": ms, "subgrids": (grid // n) ** 3,
+            "dram_floor_frac": floor / peak,
+            "note": "config 5 (262 144 8^3 sub-grids) on this one GPU, the "
+                    "N > 1 headline's path (bench.py --gpus N): the scaling "
+                    "curve's N = 1 point"}
+
+
 def cfg5_leg(args, world, rank, local, peak):
     """BASELINE config 5: 262 144 8^3 sub-grids (grid 512^3, blast field)
     slab-partitioned over the ranks (strong scaling: fixed total).  One step
@@ -1401,6 +1429,8 @@ def main():
                                               3, world, stream, peak)
     line["schemes_one_launch"] = scheme_legs(wl, max(10, args.steps // 2), 3,
                                              world, stream, peak)
+    if world == 1:
+        line["config5_1gpu"] = cfg5_one_gpu(args, local, peak)
     if not args.no_sweep:
         line["sweep"] = run_sweep(wl, args, world, stream, peak)
         line["reference_api"] = reference_api_legs(args)

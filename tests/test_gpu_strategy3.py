@@ -384,3 +384,28 @@ def test_queue_executor_overlapped_runs_bit_exact(cuda, cfg2, early):
     last = pools[5 % 2][1]
     assert np.array_equal(F.cpu().numpy(), last[2])
     assert np.array_equal(up.cpu().numpy(), last[1])
+
+
+def test_queue_executor_rejects_bad_ids_and_stays_usable(cuda, cfg2):
+    """An arrival id outside the pool is refused before anything is
+    launched or published (ValidationError), and the same queue then runs
+    a correct iteration; outputs of the wrong shape are refused too."""
+    import torch
+    from paper_2210_06438_b200.errors import ValidationError
+    from paper_2210_06438_b200.strategy3 import QueueExecutor, default_parents
+    pool, n, vel, oum, oup, oF = cfg2
+    S = pool.shape[0]
+    q = QueueExecutor("flux", 16, default_parents(S, 16), n)
+    um, up, F = _outs(S, n, cuda)
+    bad = np.arange(S, dtype=np.int32)
+    bad[7] = S
+    with pytest.raises(ValidationError):
+        q.run(pool, vel, bad, um, up, F)
+    with pytest.raises(ValidationError):
+        q.run(pool, vel, np.arange(S, dtype=np.int32), um[: S // 2], up, F)
+    q.run(pool, vel, np.arange(S, dtype=np.int32), um, up, F)
+    q.wait()
+    torch.cuda.synchronize()
+    assert q.completed() == S
+    assert np.array_equal(F.cpu().numpy(), oF)
+    assert np.array_equal(um.cpu().numpy(), oum)
