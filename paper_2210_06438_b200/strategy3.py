@@ -442,8 +442,15 @@ class AggregatedIteration:
 
     def __init__(self, grid_n: int, n: int, velocity=(1.0, 1.0, 1.0),
                  max_team: int = 128, executors: int = 4, device=None,
-                 overlap: bool = True):
+                 overlap: bool = True, formation: str = "plan"):
+        """formation: "plan" — the teams a saturated device forms, captured
+        once as a CUDA graph (one kernel per team); "queue" — formed on the
+        fly every iteration by the formation core and published to the
+        device queue (QueueExecutor; one consumer grid per iteration)."""
         from . import ops
+        if formation not in ("plan", "queue"):
+            raise ValidationError(f"formation must be 'plan' or 'queue', "
+                                  f"got {formation!r}")
         from .hydro.scenario import dt_over_dx
         self.ops = ops
         dev = torch.device(device) if device is not None else \
@@ -463,13 +470,28 @@ class AggregatedIteration:
         self.F = torch.empty_like(self.um)
         self.amax = torch.empty(S, **f64)
         self.field_dev = torch.empty((grid_n,) * 3, **f64)
+        self.formation = formation
         self.teams = form_teams(range(S), max_team, executors)
-        # one captured plan per pool (the pools swap every iteration)
-        self.plans = [TeamPlan(self.teams, p, n, self.velocity, self.um,
-                               self.up, self.F, executors, amax=self.amax,
-                               overlap=overlap)
-                      for p in self.pools]
+        if formation == "plan":
+            # one captured plan per pool (the pools swap every iteration)
+            self.plans = [TeamPlan(self.teams, p, n, self.velocity, self.um,
+                                   self.up, self.F, executors,
+                                   amax=self.amax, overlap=overlap)
+                          for p in self.pools]
+        else:
+            # the ghost fill before each run produces its pool: the queue's
+            # boxes load after it (no early loads)
+            self.queue = QueueExecutor("reconstruct", max_team,
+                                       default_parents(S, max_team), n)
+            self.arrivals = np.arange(S, dtype=np.int32)
         self.cur = 0
+
+    def _recon_flux(self) -> None:
+        if self.formation == "plan":
+            self.plans[self.cur].launch()
+        else:
+            self.queue.run(self.pool, self.velocity, self.arrivals, self.um,
+                           self.up, self.F, amax=self.amax)
 
     @property
     def pool(self):
@@ -483,7 +505,7 @@ class AggregatedIteration:
         ops, n = self.ops, self.n
         cur, nxt = self.pools[self.cur], self.pools[1 - self.cur]
         ops.ghost_fill(cur, n, self.m)
-        self.plans[self.cur].launch()
+        self._recon_flux()
         ops.update(cur, n, self.F, self.dt_dx, nxt)
         self.cur = 1 - self.cur
 
@@ -515,17 +537,18 @@ class AggregatedIteration:
         self.field_dev.copy_(field_in, non_blocking=True)
         self.load(self.field_dev)
         self.ops.ghost_fill(self.pool, self.n, self.m)
-        self.plans[self.cur].launch()
+        self._recon_flux()
         amax_out[:self.S].copy_(self.amax, non_blocking=True)
 
     @property
     def recon_flux_launches(self) -> int:
-        """Kernels per recon_flux_host call: scatter, ghost fill, teams."""
-        return 2 + len(self.teams)
+        """Kernels per recon_flux_host call: scatter, ghost fill, teams (or
+        the one consumer grid)."""
+        return 2 + (len(self.teams) if self.formation == "plan" else 1)
 
     @property
     def launches_per_step(self) -> int:
-        return 2 + len(self.teams)
+        return 2 + (len(self.teams) if self.formation == "plan" else 1)
 
 
 class ReconFluxHostPipeline:

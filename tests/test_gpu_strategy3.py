@@ -409,3 +409,34 @@ def test_queue_executor_rejects_bad_ids_and_stays_usable(cuda, cfg2):
     assert q.completed() == S
     assert np.array_equal(F.cpu().numpy(), oF)
     assert np.array_equal(um.cpu().numpy(), oum)
+
+
+@pytest.mark.parametrize("grid,n,vel", [(64, 8, (1.0, 1.0, 1.0)),
+                                        (64, 8, (-1.0, 0.5, -0.25))])
+def test_aggregated_iteration_on_the_fly(cuda, grid, n, vel):
+    """AggregatedIteration(formation="queue"): the teams formed on the fly
+    by the formation core and published to the device queue after each
+    ghost fill — recon_flux_host faces and run_host fields equal the
+    oracle's / reference_step's, on repeated calls."""
+    import torch
+    from paper_2210_06438_b200.strategy3 import AggregatedIteration
+    f = HO.stress_field(grid)
+    hp = HO.make_pool(f, n)
+    HO.exchange_ghosts_pool(hp, n, grid // n)
+    oum, oup, oF = HO.recon_flux_batch(hp, n, vel)
+    it = AggregatedIteration(grid, n, vel, max_team=16, executors=1,
+                             formation="queue")
+    host_in = torch.from_numpy(f).pin_memory()
+    amax = torch.empty(it.S, dtype=torch.float64).pin_memory()
+    for _ in range(2):
+        it.um.fill_(float("nan"))
+        it.recon_flux_host(host_in, amax)
+        it.queue.wait()
+        torch.cuda.synchronize()
+        assert np.array_equal(it.um.cpu().numpy(), oum)
+        assert np.array_equal(it.F.cpu().numpy(), oF)
+        assert bool((amax == max(abs(v) for v in vel)).all())
+    host_out = torch.empty_like(host_in).pin_memory()
+    it.run_host(host_in, host_out, iterations=3)
+    torch.cuda.synchronize()
+    assert np.array_equal(host_out.numpy(), HO.reference_step(f, vel))
