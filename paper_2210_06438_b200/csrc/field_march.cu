@@ -36,10 +36,16 @@
 // GPU (TF_STEP_HALO_X) or the ring neighbours' halos over peer memory
 // (peer_lo / peer_hi), so the exchange rides on the compute.
 //
-// Config 5 (grid 512, one B200, full clock): 0.470 ms per iteration vs
-// 0.541 ms for k_step_cols8s = 0.70 of the 16 B/cell DRAM floor.  The
-// kernel is issue-bound (IPC 2.8 of 4, FP64 pipe ~50%, 12 warps/SM at 152
-// registers): ~570 instructions per warp-plane of 256 cells.
+// Work items are ordered interior first (no halo copies), then the items
+// on the field's faces; an interior item runs a loop unrolled twice whose
+// two register sets alternate (no register moves for the x shift), a face
+// item a single-copy loop with the halo-writing finalise — the two loops
+// together outgrow the instruction cache, so the phases are kept apart.
+//
+// Config 5 (grid 512, one B200, full clock): 0.444-0.448 ms per iteration
+// vs 0.541 ms for k_step_cols8s = 0.73-0.74 of the 16 B/cell DRAM floor.
+// The kernel is issue-bound (IPC ~2.7 of 4, FP64 pipe ~50%, 15 warps/SM at
+// 128 registers).
 //
 // Arithmetic: face3 / the update are exactly cols8s_body's (kernels.py:73-111
 // face_flux and update_body, no FMA contraction): bit-identical to the
@@ -50,6 +56,7 @@
 #include <stdint.h>
 
 #include <mutex>
+#include <type_traits>
 #include <unordered_map>
 
 #include "../../include/taskfuse_b200.h"
@@ -113,19 +120,63 @@ struct MarchArgs {
   int nzb;          // z blocks (Gz / 32)
   int ncols;        // warp columns per plane (Gy / R * nzb)
   int nitems;       // ceil(X / xc) * ncols
+  // item order: the n_int interior items (no halo copies: chunks [cl, ch)
+  // x the nyi x nzi columns off the y/z faces) first, then the rest
+  int n_int, cl, ch, nyb, nyi, nzi, yoff, zoff;
   int halo_yz;      // also write the next field's periodic y/z halos
   unsigned* work;   // {claim, done} counters (zero at launch), or null
   double ax, ay, az, dt_dx;
 };
 
+// Work item `it` -> its first plane xa, length len and column origin
+// (y0, z0).  Interior items come first so that, while they last, the warps
+// run only the interior loop (march_warp): the halo-writing loop is a
+// second copy of the plane body, and both together outgrow the SM's
+// instruction cache.  Returns whether the item is interior.
 template <int R>
-__device__ __forceinline__ void item_geo(const MarchArgs& A, int it, int& xa,
+__device__ __forceinline__ bool item_geo(const MarchArgs& A, int it, int& xa,
                                          int& len, int& y0, int& z0) {
-  const int chunk = it / A.ncols, col = it - chunk * A.ncols;
+  int chunk, yg, zb;
+  bool interior = it < A.n_int;
+  if (interior) {
+    const int per = A.nyi * A.nzi;
+    chunk = A.cl + it / per;
+    const int r = it - (chunk - A.cl) * per;
+    yg = A.yoff + r / A.nzi;
+    zb = A.zoff + r % A.nzi;
+  } else {
+    int e = it - A.n_int;
+    const int nch = (A.X + A.xc - 1) / A.xc;
+    const int edge_chunks = nch - (A.ch - A.cl);
+    if (e < edge_chunks * A.ncols) {
+      // the chunks holding x-halo planes, every column
+      const int k = e / A.ncols, col = e - k * A.ncols;
+      chunk = k < A.cl ? k : A.ch + (k - A.cl);
+      yg = col / A.nzb;
+      zb = col - yg * A.nzb;
+    } else {
+      // the interior chunks' columns on the y/z faces (the frame)
+      e -= edge_chunks * A.ncols;
+      const int frame = A.ncols - A.nyi * A.nzi;
+      chunk = A.cl + e / frame;
+      int f = e - (chunk - A.cl) * frame;
+      if (f < A.nzb) {
+        yg = 0, zb = f;
+      } else if (A.nyb > 1 && f < 2 * A.nzb) {
+        yg = A.nyb - 1, zb = f - A.nzb;
+      } else {
+        f -= A.nyb > 1 ? 2 * A.nzb : A.nzb;
+        const int sides = A.nzb < 2 ? A.nzb : 2;
+        yg = 1 + f / sides;
+        zb = (f % sides) ? A.nzb - 1 : 0;
+      }
+    }
+  }
   xa = chunk * A.xc;
   len = min(A.xc, A.X - xa);
-  y0 = (col / A.nzb) * R;
-  z0 = (col - (col / A.nzb) * A.nzb) * MZ;
+  y0 = yg * R;
+  z0 = zb * MZ;
+  return interior;
 }
 
 // The owned rows of plane p (values c = u(p), x faces fx / fxm of its
@@ -135,8 +186,9 @@ __device__ __forceinline__ void item_geo(const MarchArgs& A, int it, int& xa,
 template <int R, bool PY, bool PZ, bool EDGE>
 __device__ __forceinline__ void finalise(const MarchArgs& A,
                                          const double* cb, double* strip,
-                                         const double* c, const double* fx,
-                                         const double* fxm, int p, int y0,
+                                         const double (&c)[R],
+                                         const double (&fx)[R],
+                                         const double (&fxm)[R], int p, int y0,
                                          int z0, bool hy, bool hz, bool hlo,
                                          bool hhi) {
   const int lane = threadIdx.x & 31;
@@ -278,62 +330,57 @@ __device__ __forceinline__ void march_warp(const CUtensorMap* map,
     const int it = iq[ci % IQ];
     if (it < 0) break;
     int xa, len, y0, z0;
-    item_geo<R>(A, it, xa, len, y0, z0);
+    const bool interior = item_geo<R>(A, it, xa, len, y0, z0);
     // warp-uniform: does this column touch a periodic y / z face?
     const bool hy = A.halo_yz && (y0 < HY || y0 + R > A.Gy - HY);
     const bool hz = A.halo_yz && (z0 == 0 || z0 + MZ == A.Gz);
-    double xr0[R], xr1[R], fxm[R];
-    for (int t = 0; t < len + 3; ++t, ++gc) {
+    // One x plane of the march: the state carried from plane to plane
+    // (s0 = u(p-1) or, a >= 0, the backward difference u(p) - u(p-1);
+    // s1 = u(p); sm = the -1/2 x face) comes in as (s0, s1, sm) and the
+    // next state goes out as (d0, d1, dm).
+    auto plane = [&](auto edge_tag, int t, const auto& s0, const auto& s1,
+                     const auto& sm, auto& d0, auto& d1, auto& dm) {
+      constexpr bool EDGE = decltype(edge_tag)::value;
       const unsigned s = gc % NB;
       mbar_wait(&bars[s], (gc / NB) & 1);
       const double* nb =
           reinterpret_cast<const double*>(wbuf + s * PLANE) + 2 * BZW + 2 +
           lane;  // (row 0, own z) of the new plane
-      double nw[R];
 #pragma unroll
-      for (int r = 0; r < R; ++r) nw[r] = nb[r * BZW];
+      for (int r = 0; r < R; ++r) d1[r] = nb[r * BZW];
       int nfree = 0;
-      // a >= 0: xr0 holds the backward difference u(p) - u(p-1) instead of
+      // a >= 0: the backward difference u(p) - u(p-1) is carried instead of
       // u(p-1) — the forward difference of the previous plane, formed once
-      double fw[R];
-      if (PX) {
 #pragma unroll
-        for (int r = 0; r < R; ++r) fw[r] = __dsub_rn(nw[r], xr1[r]);
-      }
+      for (int r = 0; r < R; ++r)
+        d0[r] = PX ? __dsub_rn(d1[r], s1[r]) : s1[r];
       if (t >= 2) {
-        double fx[R];
 #pragma unroll
         for (int r = 0; r < R; ++r)
-          fx[r] = PX ? face_d<true>(xr1[r], fw[r], xr0[r], ax)
-                     : face3<false>(xr0[r], xr1[r], nw[r], ax);
+          dm[r] = PX ? face_d<true>(s1[r], d0[r], s0[r], ax)
+                     : face3<false>(s0[r], s1[r], d1[r], ax);
         if (t >= 3) {
           // finalise plane p = q - D from its own buffer (D planes ago)
           const int p = xa + t - 3;
           const double* cb = reinterpret_cast<const double*>(
               wbuf + ((gc - D) % NB) * PLANE);
-          const bool hlo = A.peer_lo != nullptr && p < HX;
-          const bool hhi = A.peer_hi != nullptr && p >= A.X - HX;
-          const double* c = PX ? xr1 : xr0;
-          if (hy || hz || hlo || hhi)
-            finalise<R, PY, PZ, true>(A, cb, strip, c, fx, fxm, p, y0, z0, hy,
+          const auto& c = PX ? s1 : s0;
+          if (EDGE) {
+            const bool hlo = A.peer_lo != nullptr && p < HX;
+            const bool hhi = A.peer_hi != nullptr && p >= A.X - HX;
+            finalise<R, PY, PZ, true>(A, cb, strip, c, dm, sm, p, y0, z0, hy,
                                       hz, hlo, hhi);
-          else
-            finalise<R, PY, PZ, false>(A, cb, strip, c, fx, fxm, p, y0, z0,
+          } else {
+            finalise<R, PY, PZ, false>(A, cb, strip, c, dm, sm, p, y0, z0,
                                        false, false, false, false);
+          }
           nfree = 1;  // the finalised plane's buffer
         }
-#pragma unroll
-        for (int r = 0; r < R; ++r) fxm[r] = fx[r];
         // the item's last plane: the look-ahead planes are done too
         if (t == len + 2) nfree += D;
       } else {
         // POS: planes xa-2, xa-1 feed only the x faces; NEG: xa-1 only
         nfree = (PX || t == 0) ? 1 : 0;
-      }
-#pragma unroll
-      for (int r = 0; r < R; ++r) {
-        xr0[r] = PX ? fw[r] : xr1[r];
-        xr1[r] = nw[r];
       }
       // every lane's reads of the freed buffer are done (their values are
       // consumed above) before lane 0 lets the TMA rewrite it.  No proxy
@@ -343,12 +390,55 @@ __device__ __forceinline__ void march_warp(const CUtensorMap* map,
       if (lane == 0)
         for (int k = 0; k < nfree; ++k) issue();
       __syncwarp();  // the item queue entry lane 0 may have written
+      ++gc;
+    };
+    double a0[R], a1[R], am[R], b0[R], b1[R], bm[R];
+    const int n = len + 3;
+    if (interior) {
+      // two register sets alternate, so the x shift costs no register
+      // moves (rotating one set in place is 48 moves per plane, 9% of the
+      // instructions).  Plane 0 only loads: n - 1 = len + 2 is even for an
+      // even chunk, so the pair loop's remainder copy stays cold
+      {
+        const unsigned s = gc % NB;
+        mbar_wait(&bars[s], (gc / NB) & 1);
+        const double* nb = reinterpret_cast<const double*>(wbuf + s * PLANE) +
+                           2 * BZW + 2 + lane;
+#pragma unroll
+        for (int r = 0; r < R; ++r) a1[r] = nb[r * BZW];
+        __syncwarp();
+        if (lane == 0) issue();  // plane xa-2 (POS) / xa-1 (NEG) is done
+        __syncwarp();
+        ++gc;
+      }
+      int t = 1;
+      for (; t + 1 < n; t += 2) {
+        plane(std::false_type{}, t, a0, a1, am, b0, b1, bm);
+        plane(std::false_type{}, t + 1, b0, b1, bm, a0, a1, am);
+      }
+      if (t < n) plane(std::false_type{}, t, a0, a1, am, b0, b1, bm);
+    } else {
+      for (int t = 0; t < n; ++t) {
+        plane(std::true_type{}, t, a0, a1, am, b0, b1, bm);
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          a0[r] = b0[r];
+          a1[r] = b1[r];
+          am[r] = bm[r];
+        }
+      }
     }
   }
 }
 
+// <= 128 registers: the register file is split between the SM's four
+// schedulers (16 K each), so 129-136 registers hold 3 warps per scheduler
+// and <= 128 hold 4 — with the shared-memory carveout at its maximum the
+// ring buffers then fit 15 warps per SM instead of 12 (config 5: 458 ->
+// 444 us; the ptxas budget costs 16 bytes of spills in one of the eight
+// velocity-sign variants)
 template <int R, int NB, bool PX, bool PY, bool PZ>
-__global__ void __launch_bounds__(MGeo<R, NB>::W * 32)
+__global__ void __launch_bounds__(MGeo<R, NB>::W * 32, 16)
     k_step_march(const __grid_constant__ CUtensorMap map,
                  const __grid_constant__ MarchArgs A) {
   using G = MGeo<R, NB>;
@@ -445,6 +535,10 @@ int launch_march(const CUtensorMap& map, const MarchArgs& A, int sg,
           reinterpret_cast<const void*>(kern),
           cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
       if (e != cudaSuccess) return e;
+      e = cudaFuncSetAttribute(reinterpret_cast<const void*>(kern),
+                               cudaFuncAttributePreferredSharedMemoryCarveout,
+                               cudaSharedmemCarveoutMaxShared);
+      if (e != cudaSuccess) return e;
       int per_sm = 0, sms = 0;
       e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
           &per_sm, reinterpret_cast<const void*>(kern), G::W * 32, G::SMEM);
@@ -494,11 +588,24 @@ int tf_field_march_f64(const double* padded_in, int32_t X, int32_t Gy,
   A.Gz = Gz;
   A.xc = xc > 0 ? xc : 16;
   A.nzb = Gz / MZ;
-  A.ncols = (Gy / R) * A.nzb;
-  const int64_t items = (int64_t)((X + A.xc - 1) / A.xc) * A.ncols;
+  A.nyb = Gy / R;
+  A.ncols = A.nyb * A.nzb;
+  const int nch = (X + A.xc - 1) / A.xc;
+  const int64_t items = (int64_t)nch * A.ncols;
   if (items > (1 << 30)) return TF_E_INVALID;
   A.nitems = (int)items;
   A.halo_yz = (flags & TF_STEP_HALO_YZ) ? 1 : 0;
+  // interior items: no periodic y/z face (halo_yz) and no x-halo plane
+  A.yoff = A.zoff = A.halo_yz;
+  A.nyi = A.halo_yz ? (A.nyb > 2 ? A.nyb - 2 : 0) : A.nyb;
+  A.nzi = A.halo_yz ? (A.nzb > 2 ? A.nzb - 2 : 0) : A.nzb;
+  // chunk c is clear of the low x halo iff c * xc >= HX, of the high one
+  // iff (c + 1) * xc <= X - HX
+  A.cl = peer_lo ? (HX + A.xc - 1) / A.xc : 0;
+  A.ch = peer_hi ? (X - HX) / A.xc : nch;
+  if (A.ch < A.cl) A.ch = A.cl;
+  if (A.cl > nch) A.cl = A.ch = nch;
+  A.n_int = (A.ch - A.cl) * A.nyi * A.nzi;
   A.work = work;
   A.ax = ax;
   A.ay = ay;
@@ -508,8 +615,11 @@ int tf_field_march_f64(const double* padded_in, int32_t X, int32_t Gy,
   cudaStream_t st = (cudaStream_t)stream;
   // ring depth 4 for both column heights (A/B on config 5, R = 8, xc 16:
   // NB 4 / 5 / 6 = 470 / 473-481 / 530+ us; more buffers cost warps)
-  return R == 4 ? launch_march<4, 4>(map, A, sg, st)
-                : launch_march<8, 4>(map, A, sg, st);
+#ifndef TF_MARCH_NB
+#define TF_MARCH_NB 4
+#endif
+  return R == 4 ? launch_march<4, TF_MARCH_NB>(map, A, sg, st)
+                : launch_march<8, TF_MARCH_NB>(map, A, sg, st);
 }
 
 }  // extern "C"
