@@ -613,8 +613,9 @@ int tf_field_march_f64(const double* padded_in, int32_t X, int32_t Gy,
   A.dt_dx = dt_dx;
   const int sg = (ax >= 0.0 ? 1 : 0) | (ay >= 0.0 ? 2 : 0) | (az >= 0.0 ? 4 : 0);
   cudaStream_t st = (cudaStream_t)stream;
-  // ring depth 4 for both column heights (A/B on config 5, R = 8, xc 16:
-  // NB 4 / 5 / 6 = 470 / 473-481 / 530+ us; more buffers cost warps)
+  // ring depth 4 for both column heights (A/B on config 5, R = 8, xc 16,
+  // 128 registers: NB 3 / 4 / 5 = 450 / 448 / 477 us; more buffers cost
+  // warps, fewer leave one plane in flight).  TF_MARCH_NB: tuning builds
 #ifndef TF_MARCH_NB
 #define TF_MARCH_NB 4
 #endif
