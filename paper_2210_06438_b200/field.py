@@ -214,12 +214,13 @@ class FieldIteration(_FieldBase):
 
     def run_host(self, field_in, field_out, iterations: int = 1) -> None:
         """Host field (pinned) in -> iterations -> host field out."""
-        self.field_dev.copy_(field_in, non_blocking=True)
+        from .strategy3 import copy_split
+        copy_split(self.field_dev, field_in)   # two copy engines
         self.load(self.field_dev)
         for _ in range(iterations):
             self.step()
         self.store(self.field_dev)
-        field_out.copy_(self.field_dev, non_blocking=True)
+        copy_split(field_out, self.field_dev)
 
     @property
     def launches_per_step(self) -> int:
@@ -514,12 +515,13 @@ class PeerSlabFieldIteration(_FieldBase):
             dev = self._host_dev = torch.empty(
                 (self.X, self.G, self.G), dtype=torch.float64,
                 device=self.device)
-        dev.copy_(slab_in, non_blocking=True)
+        from .strategy3 import copy_split
+        copy_split(dev, slab_in)       # two copy engines (strategy3)
         self.load(dev)
         self._prime()
         self.iteration()
         self.store(dev)
-        slab_out.copy_(dev, non_blocking=True)
+        copy_split(slab_out, dev)
 
     def check(self) -> None:
         """Raise if a peer barrier timed out."""
