@@ -432,12 +432,13 @@ class DeviceLaunchExecutor:
 _COPY_STREAMS: dict = {}
 
 
-def copy_split(dst: torch.Tensor, src: torch.Tensor, parts: int = 2) -> None:
+def copy_split(dst: torch.Tensor, src: torch.Tensor, parts: int = 4) -> None:
     """Host<->device copy (one side pinned host memory) split along dim 0
     over `parts` side streams, ordered after the current stream's work and
-    before what follows on it.  One B200 copy engine moved config 2's 16.8
-    MB field at 27-49 GB/s from box to box; two in parallel hold ~49 GB/s
-    (scripts/probe_h2d_streams.py)."""
+    before what follows on it.  One copy engine moved config 2's 16.8 MB
+    field at 17-49 GB/s from box to box; split over streams it ran at
+    49 GB/s (2 or 4 streams) on a healthy host link and 25 GB/s (4) vs
+    17 GB/s (1) on a slow one (scripts/probe_h2d_streams.py)."""
     dev = dst.device if dst.is_cuda else src.device
     cur = torch.cuda.current_stream(dev)
     key = (dev.index, parts)
@@ -627,9 +628,9 @@ class ReconFluxHostPipeline:
         lib = _lib.load()
         ax, ay, az = it.velocity
         self.launches = 0
-        # chunks alternate between two copy streams (two copy engines: one
-        # engine alone ran at 27-49 GB/s from box to box)
-        ups = [torch.cuda.Stream(device=dev) for _ in range(2)]
+        # chunks rotate over four copy streams (copy_split: one engine alone
+        # ran at 17-49 GB/s from box to box)
+        ups = [torch.cuda.Stream(device=dev) for _ in range(4)]
         comp_side = torch.cuda.Stream(device=dev)
         fin = field_in.view(it.grid_n, it.grid_n, it.grid_n)
         dev_f, pool = it.field_dev, it.pool
@@ -656,7 +657,7 @@ class ReconFluxHostPipeline:
             for up in ups:
                 up.wait_stream(comp)
             for c in range(nch):
-                up = ups[c % 2]
+                up = ups[c % len(ups)]
                 with torch.cuda.stream(up):
                     lo, hi = start[c] * n, start[c + 1] * n
                     dev_f[lo:hi].copy_(fin[lo:hi], non_blocking=True)
