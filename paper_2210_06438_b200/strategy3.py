@@ -598,7 +598,8 @@ class ReconFluxHostPipeline:
     `field_in`: every replay rewrites the whole current pool."""
 
     def __init__(self, it: "AggregatedIteration", field_in, amax_out,
-                 layers=(1, 3, 4, 4, 3, 1), executors: int = 2):
+                 layers=(1, 3, 4, 4, 3, 1), executors: int = 2,
+                 copy_streams: int = 2):
         from . import ops
         if not (field_in.is_pinned() and amax_out.is_pinned()):
             raise ValidationError("the pipeline needs pinned host buffers")
@@ -628,9 +629,12 @@ class ReconFluxHostPipeline:
         lib = _lib.load()
         ax, ay, az = it.velocity
         self.launches = 0
-        # chunks rotate over four copy streams (copy_split: one engine alone
-        # ran at 17-49 GB/s from box to box)
-        ups = [torch.cuda.Stream(device=dev) for _ in range(4)]
+        # each chunk's upload is split over two copy streams (two copy
+        # engines: one alone ran at 17-49 GB/s from box to box), chunks in
+        # order on both — rotating whole chunks over the streams instead let
+        # every chunk land at about the same time, which undid the overlap
+        ups = [torch.cuda.Stream(device=dev)
+               for _ in range(max(1, min(2, copy_streams)))]
         comp_side = torch.cuda.Stream(device=dev)
         fin = field_in.view(it.grid_n, it.grid_n, it.grid_n)
         dev_f, pool = it.field_dev, it.pool
@@ -657,15 +661,21 @@ class ReconFluxHostPipeline:
             for up in ups:
                 up.wait_stream(comp)
             for c in range(nch):
-                up = ups[c % len(ups)]
-                with torch.cuda.stream(up):
-                    lo, hi = start[c] * n, start[c + 1] * n
-                    dev_f[lo:hi].copy_(fin[lo:hi], non_blocking=True)
-                    ev = torch.cuda.Event()
-                    ev.record(up)
-                    evs.append(ev)
+                lo, hi = start[c] * n, start[c + 1] * n
+                mid = (lo + hi) // 2 if len(ups) == 2 else hi
+                pair = []
+                for up, (a, b) in zip(ups, ((lo, mid), (mid, hi))):
+                    if a >= b:
+                        continue
+                    with torch.cuda.stream(up):
+                        dev_f[a:b].copy_(fin[a:b], non_blocking=True)
+                        ev = torch.cuda.Event()
+                        ev.record(up)
+                        pair.append(ev)
+                evs.append(pair)
             for c in range(nch):
-                comp.wait_event(evs[c])
+                for ev in evs[c]:
+                    comp.wait_event(ev)
                 ops.field_to_pool_layers(dev_f, n, pool, start[c], layers[c])
                 self.launches += 1
                 if 2 <= c:

@@ -2,7 +2,7 @@
 # workload, ncu captures (queue consumer traffic + full, plan graph traffic,
 # launch list), sanitizers over the queue / recon / field kernels.
 export TASKFUSE_NO_BUILD=1
-O=gpurun_out/final2
+O=gpurun_out/${FINAL_DIR:-final2}
 mkdir -p $O
 timeout 1800 python -m pytest tests -m gpu -q -x --durations=15 > $O/pytest_gpu.log 2>&1; echo "pytest exit $?" >> $O/pytest_gpu.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke exit $?" >> $O/smoke.log
