@@ -679,14 +679,17 @@ def e2e_leg(args, steps, warmup, world, stream):
     # (copy engines differ from box to box): the faster is the call timed
     pipes = {cs: ReconFluxHostPipeline(it, host_in, amax, copy_streams=cs)
              for cs in (1, 2)}
+    # host-link transfers settle slower than kernels: 0.3 s of untimed
+    # calls first (a short warm-up measured the same call 10-15% slower)
     pipe_ms = {cs: timed(lambda k, p=p: p.run(), steps, max(5, warmup),
-                         world, stream) for cs, p in pipes.items()}
+                         world, stream, settle_s=0.3)
+               for cs, p in pipes.items()}
     cs_best = min(pipe_ms, key=pipe_ms.get)
     pipe, ms_pipe = pipes[cs_best], pipe_ms[cs_best]
     torch.cuda.synchronize()
     ok = bool((amax == max(abs(v) for v in VELOCITY)).all())
     ms_plain = timed(lambda k: it.recon_flux_host(host_in, amax), steps,
-                     max(5, warmup), world, stream)
+                     max(5, warmup), world, stream, settle_s=0.3)
     torch.cuda.synchronize()
     ok = ok and bool((amax == max(abs(v) for v in VELOCITY)).all())
     # the same call with the teams formed on the fly (the headline's path):
@@ -694,7 +697,7 @@ def e2e_leg(args, steps, warmup, world, stream):
     itq = AggregatedIteration(GRID, N_SUB, VELOCITY, max_team=args.max_team,
                               executors=1, formation="queue")
     ms_queue = timed(lambda k: itq.recon_flux_host(host_in, amax), steps,
-                     max(5, warmup), world, stream)
+                     max(5, warmup), world, stream, settle_s=0.3)
     itq.queue.wait()
     torch.cuda.synchronize()
     ok = ok and bool((amax == max(abs(v) for v in VELOCITY)).all())
