@@ -525,6 +525,17 @@ def config3_sweep(args, world, stream, peak, ks, kw):
             "cell_updates_per_s": rate(wl3.S, wl3.n, ms), "ms_per_iter": ms,
             "launches": nk,
             "hbm_frac": wl3.S * b_alg(wl3.n) / (ms * 1e-3) / (peak * 1e9)}
+    # the headline's method: teams formed on the fly, the device queue
+    step, q = queue_runner(wl3, 128)
+    ms = timed(step, ks, kw, world, stream)
+    q.wait()
+    st = q.stats()
+    res["on_the_fly_A128"] = {
+        "cell_updates_per_s": rate(wl3.S, wl3.n, ms), "ms_per_iter": ms,
+        "mean_team": sum(k * v for k, v in st["size_histogram"].items())
+        / max(1, st["teams_formed"]),
+        "hbm_frac": wl3.S * b_alg(wl3.n) / (ms * 1e-3) / (peak * 1e9)}
+    del q, step
     for E in (8, 32, 128):
         step, nk, _, _ = plan_runner(wl3, 1, E, parents=E)
         ms = timed(step, max(3, ks // 4), kw, world, stream)
