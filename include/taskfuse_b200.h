@@ -479,8 +479,14 @@ int tf_field_step_peer_f64(const double* padded_in, int32_t X, int32_t Gy,
  * them zeroed), or NULL for a static round-robin split.  Replaces the
  * per-sub-grid loop of advect_once / HydroSim's iteration over a whole
  * rank (reference.py:28-52, step.py:125-143) plus exchange_ghosts
- * (scenario.py:124-142) for the x halos.                                   */
+ * (scenario.py:124-142) for the x halos.
+ * TF_MARCH_PDL_EDGE: launch as a programmatic dependent of the previous
+ * kernel on the stream (a peer barrier launched with TF_BARRIER_PDL): the
+ * items that read or store x-halo planes wait for it (griddepcontrol.wait),
+ * every other item runs at once — the multi-GPU iteration overlaps the
+ * ring synchronisation with its interior.                                  */
 #define TF_MARCH_ROWS4 16
+#define TF_MARCH_PDL_EDGE 32
 int tf_field_march_f64(const double* padded_in, int32_t X, int32_t Gy,
                        int32_t Gz, double ax, double ay, double az,
                        double dt_dx, double* padded_out, double* peer_lo,
@@ -489,6 +495,15 @@ int tf_field_march_f64(const double* padded_in, int32_t X, int32_t Gy,
 int tf_peer_barrier(long long* my_flags, long long* left_flags,
                     long long* right_flags, long long epoch,
                     long long timeout_ns, int* err, tf_stream_t stream);
+/* tf_peer_barrier with flags: TF_BARRIER_PDL = launched as a programmatic
+ * dependent of the previous kernel (it publishes the epoch after that
+ * kernel completes) and letting the NEXT kernel launch at once (a march
+ * with TF_MARCH_PDL_EDGE, whose x-edge items wait for this barrier).       */
+#define TF_BARRIER_PDL 1
+int tf_peer_barrier_ex(long long* my_flags, long long* left_flags,
+                       long long* right_flags, long long epoch,
+                       long long timeout_ns, int* err, int32_t flags,
+                       tf_stream_t stream);
 /* y/z halos of padded layers [first, first+count) only; the periodic x halo
  * (side 1: low halo <- last owned layers, 2: high <- first, 3: both).
  * Used by the chunked host pipeline (FieldIteration.run_host_pipelined).    */

@@ -32,6 +32,8 @@ TF_PLAN_REFGEO = 16
 TF_STEP_HALO_YZ = 4
 TF_STEP_HALO_X = 8
 TF_MARCH_ROWS4 = 16
+TF_MARCH_PDL_EDGE = 32
+TF_BARRIER_PDL = 1
 TF_QUEUE_CHAIN = 2
 
 
@@ -137,6 +139,7 @@ SIGNATURES = {
     "tf_field_march_f64": (C.c_int, [_p, _i32, _i32, _i32, _f64, _f64, _f64,
                                      _f64, _p, _p, _p, _i32, _i32, _p, _p]),
     "tf_peer_barrier": (C.c_int, [_p, _p, _p, _i64, _i64, _p, _p]),
+    "tf_peer_barrier_ex": (C.c_int, [_p, _p, _p, _i64, _i64, _p, _i32, _p]),
     "tf_field_halo_layers_f64": (C.c_int, [_p, _i32, _i32, _i32, _i32, _i32,
                                            _p]),
     "tf_field_halo_xwrap_f64": (C.c_int, [_p, _i32, _i32, _i32, _i32, _p]),

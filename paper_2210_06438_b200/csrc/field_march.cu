@@ -124,6 +124,7 @@ struct MarchArgs {
   // x the nyi x nzi columns off the y/z faces) first, then the rest
   int n_int, cl, ch, nyb, nyi, nzi, yoff, zoff;
   int halo_yz;      // also write the next field's periodic y/z halos
+  int pdl_edge;     // x-edge items wait for the previous kernel (PDL)
   unsigned* work;   // {claim, done} counters (zero at launch), or null
   double ax, ay, az, dt_dx;
 };
@@ -265,7 +266,7 @@ __device__ __forceinline__ void finalise(const MarchArgs& A,
 // One warp's whole share of the slab.  PX/PY/PZ: velocity signs (a >= 0).
 // Items come from the launch's work counter (A.work: dynamic, balanced) or
 // round-robin by warp (A.work == nullptr).
-template <int R, int NB_, bool PX, bool PY, bool PZ>
+template <int R, int NB_, bool PX, bool PY, bool PZ, bool PDL>
 __device__ __forceinline__ void march_warp(const CUtensorMap* map,
                                            const MarchArgs& A,
                                            unsigned char* wbuf,
@@ -301,6 +302,14 @@ __device__ __forceinline__ void march_warp(const CUtensorMap* map,
     if (p_item < 0) return;
     int xa, len, y0, z0;
     item_geo<R>(A, p_item, xa, len, y0, z0);
+    if (PDL && (xa < A.cl * A.xc || xa + len > A.ch * A.xc)) {
+      // an x-edge item reads the halo planes the ring neighbours store and
+      // stores theirs: only it waits for the ring barrier before it loads
+      // (a separate instantiation: the branch costs the plain kernel ~2.5%
+      // in register pressure)
+      asm volatile("griddepcontrol.wait;" ::: "memory");
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+    }
     p_q0 = xa - (PX ? 2 : 1) + HX;  // padded x of the item's first plane
     p_n = len + 3;
     p_py = y0 + HY - 2;             // padded origin of the box rows
@@ -437,7 +446,7 @@ __device__ __forceinline__ void march_warp(const CUtensorMap* map,
 // ring buffers then fit 15 warps per SM instead of 12 (config 5: 458 ->
 // 444 us; the ptxas budget costs 16 bytes of spills in one of the eight
 // velocity-sign variants)
-template <int R, int NB, bool PX, bool PY, bool PZ>
+template <int R, int NB, bool PX, bool PY, bool PZ, bool PDL>
 __global__ void __launch_bounds__(MGeo<R, NB>::W * 32, 16)
     k_step_march(const __grid_constant__ CUtensorMap map,
                  const __grid_constant__ MarchArgs A) {
@@ -454,7 +463,7 @@ __global__ void __launch_bounds__(MGeo<R, NB>::W * 32, 16)
   if ((threadIdx.x & 31) == 0)
     for (int k = 0; k < G::NB; ++k) mbar_init(&bars[k], 1);
   __syncwarp();
-  march_warp<R, NB, PX, PY, PZ>(&map, A, wbuf, bars, strip, iq,
+  march_warp<R, NB, PX, PY, PZ, PDL>(&map, A, wbuf, bars, strip, iq,
                                 blockIdx.x * G::W + w, gridDim.x * G::W);
 }
 
@@ -507,23 +516,32 @@ int launch_march(const CUtensorMap& map, const MarchArgs& A, int sg,
                  cudaStream_t st) {
   using G = MGeo<R, NB>;
   using K = void (*)(const CUtensorMap, const MarchArgs);
-  static const K kerns[8] = {
-      k_step_march<R, NB, false, false, false>,
-      k_step_march<R, NB, true, false, false>,
-      k_step_march<R, NB, false, true, false>,
-      k_step_march<R, NB, true, true, false>,
-      k_step_march<R, NB, false, false, true>,
-      k_step_march<R, NB, true, false, true>,
-      k_step_march<R, NB, false, true, true>,
-      k_step_march<R, NB, true, true, true>};
-  const K kern = kerns[sg];
+  static const K kerns[16] = {
+      k_step_march<R, NB, false, false, false, false>,
+      k_step_march<R, NB, true, false, false, false>,
+      k_step_march<R, NB, false, true, false, false>,
+      k_step_march<R, NB, true, true, false, false>,
+      k_step_march<R, NB, false, false, true, false>,
+      k_step_march<R, NB, true, false, true, false>,
+      k_step_march<R, NB, false, true, true, false>,
+      k_step_march<R, NB, true, true, true, false>,
+      k_step_march<R, NB, false, false, false, true>,
+      k_step_march<R, NB, true, false, false, true>,
+      k_step_march<R, NB, false, true, false, true>,
+      k_step_march<R, NB, true, true, false, true>,
+      k_step_march<R, NB, false, false, true, true>,
+      k_step_march<R, NB, true, false, true, true>,
+      k_step_march<R, NB, false, true, true, true>,
+      k_step_march<R, NB, true, true, true, true>};
+  const K kern = kerns[sg + (A.pdl_edge ? 8 : 0)];
   // persistent grid: as many CTAs as fit on the device at once (per-kernel
   // occupancy and SM count cached once per device)
   static std::mutex mu;
   static std::unordered_map<int64_t, int> grids;
   int dev = 0;
   cudaGetDevice(&dev);
-  const int64_t key = ((int64_t)dev << 16) | (NB << 8) | (sg << 4) | R;
+  const int64_t key = ((int64_t)dev << 16) | (A.pdl_edge << 12) | (NB << 8) |
+                      (sg << 4) | R;
   int grid = 0;
   {
     std::lock_guard<std::mutex> lock(mu);
@@ -551,8 +569,17 @@ int launch_march(const CUtensorMap& map, const MarchArgs& A, int sg,
   }
   const int need = (A.nitems + G::W - 1) / G::W;
   if (grid > need) grid = need;
-  kern<<<grid, G::W * 32, G::SMEM, st>>>(map, A);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(G::W * 32);
+  cfg.dynamicSmemBytes = G::SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = A.pdl_edge ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, map, A);
 }
 
 }  // namespace
@@ -567,7 +594,8 @@ int tf_field_march_f64(const double* padded_in, int32_t X, int32_t Gy,
   const int R = (flags & TF_MARCH_ROWS4) ? 4 : 8;
   if (!padded_in || !padded_out || padded_in == padded_out || X < 1 ||
       Gy < R || Gz < MZ || Gy % R || Gz % MZ || xc < 0 ||
-      (flags & ~(TF_STEP_HALO_YZ | TF_STEP_HALO_X | TF_MARCH_ROWS4)))
+      (flags & ~(TF_STEP_HALO_YZ | TF_STEP_HALO_X | TF_MARCH_ROWS4 |
+                 TF_MARCH_PDL_EDGE)))
     return TF_E_INVALID;
   if (flags & TF_STEP_HALO_X) {
     if (peer_lo || peer_hi) return TF_E_INVALID;
@@ -595,6 +623,7 @@ int tf_field_march_f64(const double* padded_in, int32_t X, int32_t Gy,
   if (items > (1 << 30)) return TF_E_INVALID;
   A.nitems = (int)items;
   A.halo_yz = (flags & TF_STEP_HALO_YZ) ? 1 : 0;
+  A.pdl_edge = (flags & TF_MARCH_PDL_EDGE) ? 1 : 0;
   // interior items: no periodic y/z face (halo_yz) and no x-halo plane
   A.yoff = A.zoff = A.halo_yz;
   A.nyi = A.halo_yz ? (A.nyb > 2 ? A.nyb - 2 : 0) : A.nyb;

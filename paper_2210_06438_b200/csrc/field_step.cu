@@ -638,7 +638,15 @@ int launch_step(const CUtensorMap& map, const int32_t* dev_ids,
 // NVLink.  Slot 0 = from my left neighbour, slot 1 = from my right.
 __global__ void k_peer_barrier(long long* my_flags, long long* left_flags,
                                long long* right_flags, long long epoch,
-                               long long timeout_ns, int* err) {
+                               long long timeout_ns, int* err, int pdl) {
+  if (pdl) {
+    // the iteration this barrier closes (the previous kernel) has completed
+    // and its stores are flushed: the next kernel (a march whose x-edge
+    // items wait for this grid) may launch and run its interior while the
+    // epochs are exchanged below
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  }
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   __threadfence_system();
   asm volatile("st.release.sys.global.b64 [%0], %1;" ::"l"(left_flags + 1),
@@ -769,8 +777,29 @@ int tf_peer_barrier(long long* my_flags, long long* left_flags,
                     long long timeout_ns, int* err, tf_stream_t stream) {
   if (!my_flags || !left_flags || !right_flags || !err) return TF_E_INVALID;
   k_peer_barrier<<<1, 32, 0, (cudaStream_t)stream>>>(
-      my_flags, left_flags, right_flags, epoch, timeout_ns, err);
+      my_flags, left_flags, right_flags, epoch, timeout_ns, err, 0);
   return cudaGetLastError();
+}
+
+int tf_peer_barrier_ex(long long* my_flags, long long* left_flags,
+                       long long* right_flags, long long epoch,
+                       long long timeout_ns, int* err, int32_t flags,
+                       tf_stream_t stream) {
+  if (!my_flags || !left_flags || !right_flags || !err ||
+      (flags & ~TF_BARRIER_PDL))
+    return TF_E_INVALID;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(1);
+  cfg.blockDim = dim3(32);
+  cfg.stream = (cudaStream_t)stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = (flags & TF_BARRIER_PDL) ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, k_peer_barrier, my_flags, left_flags,
+                            right_flags, epoch, timeout_ns, err,
+                            (flags & TF_BARRIER_PDL) ? 1 : 0);
 }
 
 int tf_field_halo_layers_f64(double* padded, int32_t X, int32_t Gy,
