@@ -86,15 +86,20 @@ def test_march_sod_and_blast(cuda):
         assert np.array_equal(it.owned().cpu().numpy(), HO.reference_step(f))
 
 
-@pytest.mark.parametrize("kernel", ["march", "cols"])
+@pytest.mark.parametrize("kernel,overlap", [("march", False),
+                                            ("march", True), ("cols", None)])
 @pytest.mark.parametrize("vel", [(-1.0, 0.5, -0.25), (1.0, 1.0, 1.0)])
-def test_peer_single_rank_both_kernels(cuda, kernel, vel):
+def test_peer_single_rank_both_kernels(cuda, kernel, overlap, vel):
+    """The peer path on one rank (its own ring neighbour), both kernels;
+    the march with and without the barrier overlap (the march a
+    programmatic dependent of the barrier, x-edge items waiting for it)."""
     import torch
     from paper_2210_06438_b200.field import PeerSlabFieldIteration
     from paper_2210_06438_b200.parallel_halo import SlabPartition
     f = HO.stress_field(64)
     r = PeerSlabFieldIteration(SlabPartition(64, 8, 1, 0), f, vel,
-                               device=cuda, kernel=kernel)
+                               device=cuda, kernel=kernel,
+                               overlap_barrier=overlap)
     assert r.kernel == kernel
     for _ in range(3):
         r.iteration()
