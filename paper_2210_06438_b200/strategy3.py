@@ -458,8 +458,6 @@ def copy_split(dst: torch.Tensor, src: torch.Tensor, parts: int = 4) -> None:
         cur.wait_stream(st)
 
 
-upload_split = copy_split
-
 
 class AggregatedIteration:
     """One device-resident hydro iteration with strategy-3 team launches:
@@ -546,7 +544,7 @@ class AggregatedIteration:
 
     def run_host(self, field_in, field_out, iterations: int = 1) -> None:
         """Host (pinned) field in -> `iterations` iterations -> host out."""
-        upload_split(self.field_dev, field_in)
+        copy_split(self.field_dev, field_in)
         self.load(self.field_dev)
         for _ in range(iterations):
             self.step()
@@ -566,7 +564,7 @@ class AggregatedIteration:
             raise ValidationError("recon_flux_host needs pinned host buffers")
         if amax_out.numel() < self.S:
             raise ValidationError(f"amax_out must hold {self.S} values")
-        upload_split(self.field_dev, field_in.view(self.field_dev.shape))
+        copy_split(self.field_dev, field_in.view(self.field_dev.shape))
         self.load(self.field_dev)
         self.ops.ghost_fill(self.pool, self.n, self.m)
         self._recon_flux()
