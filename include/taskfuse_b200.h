@@ -257,8 +257,9 @@ int tf_hydro_iteration(tf_hydro* h, const double* u_pool, double* u_next_pool,
 /* the engine's region k (KERNEL_ORDER index), for tf_region_stats         */
 int tf_hydro_region(const tf_hydro* h, int32_t k, tf_region** out);
 /* kernels, copies, bytes copied, raw device allocs, raw pinned allocs
- * (bucket misses, the reference's count), outstanding leases, buffers
- * materialised (cudaMalloc / cudaHostAlloc calls), device polls           */
+ * (bucket misses, the reference's count), outstanding leases, storage
+ * allocation calls past the reserved staging arenas (cudaMalloc /
+ * cudaHostAlloc), device polls                                             */
 int tf_hydro_counters(const tf_hydro* h, int64_t* out8);
 /* host nanoseconds spent issuing device ops, polling without progress, and
  * in tf_hydro_iteration altogether (cumulative)                           */

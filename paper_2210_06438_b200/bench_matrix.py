@@ -129,9 +129,10 @@ def run_cell(subgrid_n: int, executors: int, max_team: int, steps: int,
                       device.raw_allocations["device"],
                       device.sync_count,
                       device.raw_allocations["pinned_host"],
-                      # native engine: staging buffers materialised lazily
-                      # (real cudaMalloc / cudaHostAlloc calls)
-                      sim.native.counters()["materialised"]
+                      # native engine: real cudaMalloc / cudaHostAlloc
+                      # calls past its reserved staging arenas (chunks are
+                      # carved from the arenas lazily, by size class)
+                      sim.native.counters()["allocated"]
                       if sim.native is not None else 0))
 
     sched.spawn(lambda: driver(sim, steps + 1, on_step), label="bench")

@@ -649,7 +649,9 @@ int tf_hydro_counters(const tf_hydro* h, int64_t* out8) {
   out8[3] = h->pool.raw(KIND_DEVICE);
   out8[4] = h->pool.raw(KIND_PINNED);
   out8[5] = h->pool.outstanding();
-  out8[6] = h->pool.materialised(KIND_DEVICE) + h->pool.materialised(KIND_PINNED);
+  // real cudaMalloc / cudaHostAlloc calls past the reserved arenas (a chunk
+  // carved from an arena is not an allocation)
+  out8[6] = h->pool.spilled();
   out8[7] = h->polls;
   return 0;
 }

@@ -42,7 +42,7 @@ class NativeRegion:
 
 class HydroEngine:
     COUNTERS = ("kernels", "copies", "bytes", "raw_device", "raw_pinned",
-                "outstanding", "materialised", "polls")
+                "outstanding", "allocated", "polls")
 
     def __init__(self, state, scratch, executors, max_team: int, velocity,
                  dt_dx: float, device):
