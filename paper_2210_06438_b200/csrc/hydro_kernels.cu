@@ -702,14 +702,20 @@ __device__ void queue_fetcher(const unsigned long long* __restrict__ ring_h,
   if (s_stop != 2) {
     const long long fin = fin_sent;
     const unsigned long long tag = (unsigned long long)epoch << 32;
+    unsigned long long last_post = 0;
     for (;;) {
       const long long done =
           (long long)(ld_relaxed_gpu_u64(&qd->done) - done_base);
-      if (done != reported) {
+      const unsigned long long now = globaltimer();
+      // at most one post per microsecond until the last one: every post
+      // takes the line from the host core that polls it (a miss there per
+      // post, in the formation loop's busy test)
+      if (done != reported && (done >= fin || now - last_post >= 1000)) {
         st_relaxed_sys(&ctl->completed,
                        (long long)(tag | (unsigned long long)done));
         reported = done;
-        last_change = globaltimer();
+        last_change = now;
+        last_post = now;
       }
       if (done >= fin) break;
       if ((long long)(globaltimer() - last_change) > timeout_ns) {

@@ -12,7 +12,7 @@ from paper_2210_06438_b200.strategy3 import QueueExecutor, default_parents  # no
 wl = bench.Workload()
 arr = np.arange(wl.S, dtype=np.int32)
 for A, early in ((1, False), (16, False), (64, False), (128, False),
-                 (1, True), (128, True)):
+                 (1, True), (4, True), (128, True)):
     q = QueueExecutor("reconstruct", A, default_parents(wl.S, A), wl.n,
                       early_loads=early)
     for k in range(10):
