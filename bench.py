@@ -378,10 +378,13 @@ def queue_runner(wl, max_team, parents=None):
     q = QueueExecutor("reconstruct", max_team, parents, wl.n,
                       early_loads=True)
     arrivals = np.arange(wl.S, dtype=np.int32)
+    # one bound call per input pool (arguments checked once; the formation
+    # and the publishing still run inside every step)
+    calls = [q.bind(p, VELOCITY, arrivals, wl.um, wl.up, wl.F, amax=wl.amax)
+             for p in wl.pools]
 
     def step(k):
-        q.run(wl.pools[k % len(wl.pools)], VELOCITY, arrivals, wl.um, wl.up,
-              wl.F, amax=wl.amax)
+        calls[k % len(calls)]()
     return step, q
 
 

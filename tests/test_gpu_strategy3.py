@@ -440,3 +440,38 @@ def test_aggregated_iteration_on_the_fly(cuda, grid, n, vel):
     it.run_host(host_in, host_out, iterations=3)
     torch.cuda.synchronize()
     assert np.array_equal(host_out.numpy(), HO.reference_step(f, vel))
+
+
+def test_queue_executor_bound_call(cuda, cfg2):
+    """QueueExecutor.bind: arguments checked once, each call one formation +
+    publish run; alternating two bound calls over two pools (back to back,
+    overlapped on the device) leaves the last call's outputs, bit-exact."""
+    import torch
+    from paper_2210_06438_b200.errors import ValidationError
+    from paper_2210_06438_b200.strategy3 import QueueExecutor, default_parents
+    pool, n, vel, oum, oup, oF = cfg2
+    S = pool.shape[0]
+    grid = round(S ** (1 / 3)) * n
+    hp2 = HO.make_pool(HO.stress_field(grid), n)
+    HO.exchange_ghosts_pool(hp2, n, grid // n)
+    pool2 = torch.from_numpy(hp2).to(cuda)
+    o2 = HO.recon_flux_batch(hp2, n, vel)
+    q = QueueExecutor("flux", 128, default_parents(S, 128), n,
+                      early_loads=True)
+    um, up, F = _outs(S, n, cuda)
+    ids = np.arange(S, dtype=np.int32)
+    calls = [q.bind(p, vel, ids, um, up, F) for p in (pool, pool2)]
+    for k in range(7):
+        assert calls[k % 2]() >= 1
+    q.wait()
+    torch.cuda.synchronize()
+    assert np.array_equal(F.cpu().numpy(), oF)       # call 6: pool
+    assert np.array_equal(up.cpu().numpy(), oup)
+    calls[1]()
+    q.wait()
+    torch.cuda.synchronize()
+    assert np.array_equal(um.cpu().numpy(), o2[0])
+    bad = ids.copy()
+    bad[3] = S
+    with pytest.raises(ValidationError):
+        q.bind(pool, vel, bad, um, up, F)
