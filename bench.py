@@ -374,9 +374,11 @@ def queue_runner(wl, max_team, parents=None):
                                                  default_parents)
     parents = parents or default_parents(wl.S, max_team)
     # the pools are produced once, before any step: the first boxes of step
-    # k+1 may load during step k's tail (TF_LAUNCH_OVERLAP_PREV)
+    # k+1 may load during step k's tail (TF_LAUNCH_OVERLAP_PREV); the device
+    # works through each mirrored batch in sub-grid id order
+    # (TF_QUEUE_SORTED: the formed teams' members are strided)
     q = QueueExecutor("reconstruct", max_team, parents, wl.n,
-                      early_loads=True)
+                      early_loads=True, sorted_dispatch=True)
     arrivals = np.arange(wl.S, dtype=np.int32)
     # one bound call per input pool (arguments checked once; the formation
     # and the publishing still run inside every step)

@@ -311,8 +311,8 @@ int tf_executor_sync(tf_executor* ex);
 typedef struct tf_qexec tf_qexec;
 int tf_qexec_create(tf_region* region, int32_t n, tf_qexec** out);
 void tf_qexec_destroy(tf_qexec* q);
-/* TF_LAUNCH_OVERLAP_PREV: a run's first stencil boxes may load while the
- * previous kernel on the stream still runs.  Only valid when that kernel
+/* flags: TF_QUEUE_SORTED (below); TF_LAUNCH_OVERLAP_PREV: a run's first
+ * stencil boxes may load while the previous kernel on the stream still runs.  Only valid when that kernel
  * does not produce the run's pool (e.g. it is the previous run, or a team
  * kernel).  Default 0: boxes load after the previous kernel completes.     */
 int tf_qexec_set_flags(tf_qexec* q, int32_t flags);
@@ -348,6 +348,11 @@ int tf_qexec_wait(tf_qexec* q);
  * kernel on the stream (its first boxes load after that kernel completes),
  * | TF_LAUNCH_OVERLAP_PREV = load them before (see tf_qexec_set_flags).    */
 #define TF_QUEUE_CHAIN 2
+/* TF_QUEUE_SORTED (tf_queue_consumer_launch, tf_qexec_set_flags): each
+ * batch of entries the fetcher mirrors goes to the device ring in sub-grid
+ * id order (a counting sort over 1024 id buckets), so consecutive consumer
+ * CTAs work on neighbouring sub-grids whatever the teams' member order.    */
+#define TF_QUEUE_SORTED 4
 int tf_queue_consumer_launch(const double* pool_ext, int64_t pool_slices,
                              int32_t n, const int64_t* ring_h, void* ctl_h,
                              int64_t* ring_d, int64_t ring_cap, void* qdev,

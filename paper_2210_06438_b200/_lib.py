@@ -35,6 +35,7 @@ TF_MARCH_ROWS4 = 16
 TF_MARCH_PDL_EDGE = 32
 TF_BARRIER_PDL = 1
 TF_QUEUE_CHAIN = 2
+TF_QUEUE_SORTED = 4
 
 
 class EnterResult(C.Structure):

@@ -876,7 +876,8 @@ int tf_qexec_create(tf_region* region, int32_t n, tf_qexec** out) {
 }
 
 int tf_qexec_set_flags(tf_qexec* q, int32_t flags) {
-  if (!q || (flags & ~TF_LAUNCH_OVERLAP_PREV)) return TF_E_INVALID;
+  if (!q || (flags & ~(TF_LAUNCH_OVERLAP_PREV | TF_QUEUE_SORTED)))
+    return TF_E_INVALID;
   q->flags = flags;
   return 0;
 }
@@ -960,7 +961,8 @@ int tf_qexec_run_recon_flux(tf_qexec* q, const double* pool_ext,
       pool_ext, pool_slices, q->n, S.ring_hd, S.ctl_hd, S.ring_d, count,
       S.qdev, S.done_base, ++S.epoch, ax, ay, az, um,
       up, F, amax, flux_form,
-      /*timeout_ns=*/2000000000LL, chain ? (TF_QUEUE_CHAIN | q->flags) : 0,
+      /*timeout_ns=*/2000000000LL,
+      chain ? (TF_QUEUE_CHAIN | q->flags) : (q->flags & TF_QUEUE_SORTED),
       stream);
   if (rc) return rc;
   S.in_flight = true;

@@ -613,9 +613,16 @@ __device__ void queue_fetcher(const unsigned long long* __restrict__ ring_h,
                               unsigned long long* __restrict__ ring_d,
                               long long ring_cap, QueueDev* qd, unsigned epoch,
                               unsigned long long done_base,
-                              long long timeout_ns) {
+                              long long timeout_ns, int sort_shift) {
   __shared__ long long s_fin;
   __shared__ int s_bad, s_stop;
+  // sort_shift >= 0: each round's entries go to the device ring ordered by
+  // sub-grid id (buckets of 2^sort_shift ids, a counting sort): the formed
+  // teams' members are the reference's strided parents (arrival % P), and
+  // consecutive CTAs then work on sub-grids far apart in memory — in id
+  // order the grid streams the pool and the outputs like a one-launch team
+  constexpr int NBUCKET = 1024;
+  __shared__ int s_hist[NBUCKET];
   constexpr int U = 8;                  // loads in flight per thread
   constexpr int CHUNK = THREADS * U;    // entries read per round
   long long fetched = 0, fin_sent = -1, reported = -1;
@@ -638,22 +645,67 @@ __device__ void queue_fetcher(const unsigned long long* __restrict__ ring_h,
       const long long k = fetched + u * THREADS + threadIdx.x;
       v[u] = k < lim ? ld_relaxed_sys_u64(ring_h + k) : 0ULL;
     }
-    __syncthreads();  // s_bad initialised
+    if (sort_shift >= 0)
+      for (int b = threadIdx.x; b < NBUCKET; b += THREADS) s_hist[b] = 0;
+    __syncthreads();  // s_bad (and the histogram) initialised
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const long long k = fetched + u * THREADS + threadIdx.x;
       if (k < lim) {
         // a consumer that sees its run's epoch in the slot has the id —
         // no fence, no acquire (and no L1 invalidation) needed
-        if ((unsigned)(v[u] >> 32) == epoch)
-          ring_d[k] = v[u];
-        else
+        if ((unsigned)(v[u] >> 32) == epoch) {
+          if (sort_shift < 0) ring_d[k] = v[u];
+        } else {
           atomicMin(&s_bad, u * THREADS + (int)threadIdx.x);
+        }
       }
     }
     __syncthreads();
     const long long fin = s_fin;
     const long long valid = s_bad < lim - fetched ? s_bad : lim - fetched;
+    if (sort_shift >= 0 && valid > 0) {
+      // counting sort of the round's valid prefix by id bucket
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int i = u * THREADS + threadIdx.x;
+        if (i < valid)
+          atomicAdd(&s_hist[min((int)((unsigned)v[u] >> sort_shift),
+                                NBUCKET - 1)], 1);
+      }
+      __syncthreads();
+      if (threadIdx.x < 32) {
+        // exclusive scan of the histogram by one warp (32 buckets a lane)
+        constexpr int PER = NBUCKET / 32;
+        int sum = 0;
+#pragma unroll
+        for (int j = 0; j < PER; ++j) sum += s_hist[threadIdx.x * PER + j];
+        int incl = sum;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int t = __shfl_up_sync(0xffffffffu, incl, o);
+          if ((int)threadIdx.x >= o) incl += t;
+        }
+        int run = incl - sum;
+#pragma unroll
+        for (int j = 0; j < PER; ++j) {
+          const int c = s_hist[threadIdx.x * PER + j];
+          s_hist[threadIdx.x * PER + j] = run;
+          run += c;
+        }
+      }
+      __syncthreads();
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int i = u * THREADS + threadIdx.x;
+        if (i < valid) {
+          const int pos = atomicAdd(
+              &s_hist[min((int)((unsigned)v[u] >> sort_shift), NBUCKET - 1)],
+              1);
+          ring_d[fetched + pos] = v[u];
+        }
+      }
+    }
     fetched += valid;
     span = valid > 0 ? CHUNK : 32;
     if (valid > 0) last_change = globaltimer();
@@ -767,12 +819,12 @@ __global__ void __launch_bounds__(THREADS, recon_min_blocks<THREADS>())
                      double ay, double az, double* __restrict__ um,
                      double* __restrict__ up, double* __restrict__ F,
                      double* __restrict__ amax, int flux_form,
-                     long long timeout_ns, int early_loads) {
+                     long long timeout_ns, int early_loads, int sort_shift) {
   using G = Geo<N>;
   constexpr int CELLS = G::CELLS;
   if (blockIdx.x == 0) {
     queue_fetcher<THREADS>(ring_h, ctl, ring_d, ring_cap, qd, epoch,
-                           done_base, timeout_ns);
+                           done_base, timeout_ns, sort_shift);
     return;
   }
   // slice CTAs never gate the next run's launch: the fetcher does
@@ -1084,10 +1136,12 @@ int consumer_launch(const CUtensorMap& map, cudaStream_t st,
                     int64_t ring_cap, QueueDev* q, uint64_t done_base,
                     int32_t epoch, double ax, double ay, double az,
                     double* um, double* up, double* F, double* amax,
-                    int32_t flux_form, int64_t timeout_ns, int32_t flags) {
+                    int32_t flux_form, int64_t timeout_ns, int32_t flags,
+                    int sort_shift) {
   // flags: TF_QUEUE_CHAIN — launched as a programmatic dependent of the
   // previous kernel on the stream; TF_LAUNCH_OVERLAP_PREV — and the first
-  // stencil boxes may load before that kernel completes
+  // stencil boxes may load before that kernel completes.  sort_shift: the
+  // fetcher's id-bucket width for TF_QUEUE_SORTED, or -1
   constexpr int TH = 512;
   const int smem = Geo<N>::BOX * (int)sizeof(double);
   static const cudaError_t attr_ok = cudaFuncSetAttribute(
@@ -1110,7 +1164,7 @@ int consumer_launch(const CUtensorMap& map, cudaStream_t st,
       reinterpret_cast<unsigned long long*>(ring_d), (long long)ring_cap, q,
       (unsigned long long)done_base, (unsigned)epoch, ax, ay, az, um, up, F,
       amax, (int)flux_form, (long long)timeout_ns,
-      (flags & TF_LAUNCH_OVERLAP_PREV) ? 1 : 0);
+      (flags & TF_LAUNCH_OVERLAP_PREV) ? 1 : 0, sort_shift);
 }
 
 }  // namespace
@@ -1127,8 +1181,15 @@ int tf_queue_consumer_launch(const double* pool_ext, int64_t pool_slices,
                              tf_stream_t stream) {
   if (!valid_n(n) || !pool_ext || !ring_h || !ctl_h || !ring_d || !qdev ||
       ring_cap < 0 || ring_cap >= (1LL << 31) - 1 || epoch < 1 || !um ||
-      !up || !F || (flags & ~(TF_QUEUE_CHAIN | TF_LAUNCH_OVERLAP_PREV)))
+      !up || !F ||
+      (flags & ~(TF_QUEUE_CHAIN | TF_LAUNCH_OVERLAP_PREV | TF_QUEUE_SORTED)))
     return TF_E_INVALID;
+  // TF_QUEUE_SORTED: the id-bucket width that fits the pool in 1024 buckets
+  int sort_shift = -1;
+  if (flags & TF_QUEUE_SORTED) {
+    sort_shift = 0;
+    while (((pool_slices - 1) >> sort_shift) >= 1024) ++sort_shift;
+  }
   CUtensorMap map;
   int rc = pool_map(pool_ext, pool_slices, n, &map);
   if (rc) return rc;
@@ -1137,7 +1198,8 @@ int tf_queue_consumer_launch(const double* pool_ext, int64_t pool_slices,
   QueueDev* q = static_cast<QueueDev*>(qdev);
   auto go = [&](auto launch) {
     return launch(map, st, ring_h, c, ring_d, ring_cap, q, done_base, epoch,
-                  ax, ay, az, um, up, F, amax, flux_form, timeout_ns, flags);
+                  ax, ay, az, um, up, F, amax, flux_form, timeout_ns,
+                  flags & ~TF_QUEUE_SORTED, sort_shift);
   };
   return n == 8 ? go(consumer_launch<8>) : go(consumer_launch<16>);
 }

@@ -286,19 +286,23 @@ class QueueExecutor:
     signal is 'every published slice completed'."""
 
     def __init__(self, name: str, max_team: int, parents: int, n: int = 8,
-                 early_loads: bool = False):
+                 early_loads: bool = False, sorted_dispatch: bool = False):
         """early_loads: a run's first stencil boxes may load while the
         previous kernel on the stream still runs — valid only when that
-        kernel does not produce the pool (TF_LAUNCH_OVERLAP_PREV)."""
+        kernel does not produce the pool (TF_LAUNCH_OVERLAP_PREV).
+        sorted_dispatch: the device works through each mirrored batch of
+        published slices in sub-grid id order (TF_QUEUE_SORTED)."""
         self.core = FormationCore(name, max_team, parents, 1)
         self.lib = self.core.lib
         h = C.c_void_p()
         _lib.check(self.lib.tf_qexec_create(self.core.handle, n, C.byref(h)),
                    "tf_qexec_create")
         self.handle = h
-        if early_loads:
-            _lib.check(self.lib.tf_qexec_set_flags(
-                h, _lib.TF_LAUNCH_OVERLAP_PREV), "tf_qexec_set_flags")
+        qflags = (_lib.TF_LAUNCH_OVERLAP_PREV if early_loads else 0) | \
+            (_lib.TF_QUEUE_SORTED if sorted_dispatch else 0)
+        if qflags:
+            _lib.check(self.lib.tf_qexec_set_flags(h, qflags),
+                       "tf_qexec_set_flags")
         self.n = n
         self.runs = 0
         self._vcache = {}
@@ -542,7 +546,8 @@ class AggregatedIteration:
             # the ghost fill before each run produces its pool: the queue's
             # boxes load after it (no early loads)
             self.queue = QueueExecutor("reconstruct", max_team,
-                                       default_parents(S, max_team), n)
+                                       default_parents(S, max_team), n,
+                                       sorted_dispatch=True)
             self.arrivals = np.arange(S, dtype=np.int32)
         self.cur = 0
 

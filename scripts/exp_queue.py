@@ -11,10 +11,10 @@ from paper_2210_06438_b200.strategy3 import QueueExecutor, default_parents  # no
 
 wl = bench.Workload()
 arr = np.arange(wl.S, dtype=np.int32)
-for A, early in ((1, False), (16, False), (64, False), (128, False),
-                 (1, True), (4, True), (128, True)):
+for A, early, srt in ((1, True, False), (4, True, False), (128, True, False),
+                      (1, True, True), (4, True, True), (128, True, True)):
     q = QueueExecutor("reconstruct", A, default_parents(wl.S, A), wl.n,
-                      early_loads=early)
+                      early_loads=early, sorted_dispatch=srt)
     for k in range(10):
         q.run(wl.pools[k % 2], bench.VELOCITY, arr, wl.um, wl.up, wl.F,
               amax=wl.amax)
@@ -33,7 +33,7 @@ for A, early in ((1, False), (16, False), (64, False), (128, False),
     torch.cuda.synchronize()
     gpu = e0.elapsed_time(e1) / K
     st = q.stats()
-    print(f"A={A} early={early}: gpu {gpu*1e3:.1f} us/iter, host q.run median "
+    print(f"A={A} early={early} sorted={srt}: gpu {gpu*1e3:.1f} us/iter, host q.run median "
           f"{np.median(host)*1e6:.1f} us (min {min(host)*1e6:.1f}), "
           f"{q.host_times()}, "
           f"teams {st['teams_formed']}, solo {st['solo_fast_path']}", flush=True)

@@ -336,8 +336,9 @@ def test_device_launch_executor_bit_exact(cuda, cfg2, A):
     assert max(st["size_histogram"]) <= A
 
 
-@pytest.mark.parametrize("early", [False, True])
-def test_queue_executor_overlapped_runs_bit_exact(cuda, cfg2, early):
+@pytest.mark.parametrize("early,sort", [(False, False), (True, False),
+                                        (True, True)])
+def test_queue_executor_overlapped_runs_bit_exact(cuda, cfg2, early, sort):
     """Runs issued back to back with no host synchronisation overlap on the
     device (each consumer grid a programmatic dependent of the previous
     one; slot counters monotonic, never reset).  Runs of varying size over
@@ -357,7 +358,7 @@ def test_queue_executor_overlapped_runs_bit_exact(cuda, cfg2, early):
     pools = [(pool, (oum, oup, oF)), (pool2, o2)]
     rng = np.random.default_rng(7)
     q = QueueExecutor("flux", 64, default_parents(S, 64), n,
-                      early_loads=early)
+                      early_loads=early, sorted_dispatch=sort)
     side = torch.cuda.Stream()
     runs = []
     for k, size in enumerate((S, 7, 1500, S, 1, S, 333, S, S)):
