@@ -230,9 +230,10 @@ def test_realtime_executor_bit_exact(cuda, cfg2, A, E):
     assert np.array_equal(um.cpu().numpy(), oum)
 
 
+@pytest.mark.parametrize("sort", [False, True])
 @pytest.mark.parametrize("n,vel", [(16, (-0.7, 1.3, 0.2)),
                                    (8, (0.4, -0.9, -1.1))])
-def test_queue_executor_other_shapes(cuda, n, vel):
+def test_queue_executor_other_shapes(cuda, n, vel, sort):
     """The device queue for 16^3 sub-grids (single-buffered consumer) and
     for negative velocity components, stress field, scattered arrivals."""
     import torch
@@ -243,7 +244,8 @@ def test_queue_executor_other_shapes(cuda, n, vel):
     oum, oup, oF = HO.recon_flux_batch(hp, n, vel)
     pool = torch.from_numpy(hp).to(cuda)
     S = pool.shape[0]
-    q = QueueExecutor("flux", 8, default_parents(S, 8), n)
+    q = QueueExecutor("flux", 8, default_parents(S, 8), n,
+                      sorted_dispatch=sort)
     um, up, F = _outs(S, n, cuda)
     amax = torch.zeros(S, dtype=torch.float64, device=cuda)
     q.run(pool, vel, np.random.default_rng(3).permutation(S), um, up, F,
