@@ -474,7 +474,7 @@ int tf_field_step_peer_f64(const double* padded_in, int32_t X, int32_t Gy,
  * the (X/n, Gy/n, Gz/n) lattice; what tf_field_step_f64 / _peer_f64 do with
  * ids == NULL and T = S), tiled by warp columns instead of sub-grids: a
  * warp marches R (8, or 4 with TF_MARCH_ROWS4) y rows x 32 z cells through
- * xc x planes (0 = 16) of the field, one TMA plane box at a time
+ * xc x planes (0 = 16, or 8 for X <= 128) of the field, one TMA plane box at a time
  * (csrc/field_march.cu).  Same arithmetic, bit-identical.  Needs
  * Gy % R == 0 and Gz % 32 == 0.  flags: TF_STEP_HALO_YZ (also write the
  * next field's periodic y/z halos), TF_STEP_HALO_X (also its periodic x

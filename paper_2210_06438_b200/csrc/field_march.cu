@@ -614,7 +614,11 @@ int tf_field_march_f64(const double* padded_in, int32_t X, int32_t Gy,
   A.X = X;
   A.Gy = Gy;
   A.Gz = Gz;
-  A.xc = xc > 0 ? xc : 16;
+  // default chunk: 16 planes; 8 for a thin slab (a rank's share of config
+  // 5 at N >= 4: 64 planes in 16-plane chunks are too few items for the
+  // grid and half of them hold x-halo planes — 100 -> 87 us at 64 planes,
+  // 155 -> 142 us at 128; the same at 256 and up)
+  A.xc = xc > 0 ? xc : (X <= 128 ? 8 : 16);
   A.nzb = Gz / MZ;
   A.nyb = Gy / R;
   A.ncols = A.nyb * A.nzb;
