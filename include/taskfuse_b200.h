@@ -474,8 +474,8 @@ int tf_field_step_peer_f64(const double* padded_in, int32_t X, int32_t Gy,
  * the (X/n, Gy/n, Gz/n) lattice; what tf_field_step_f64 / _peer_f64 do with
  * ids == NULL and T = S), tiled by warp columns instead of sub-grids: a
  * warp marches R (8, or 4 with TF_MARCH_ROWS4) y rows x 32 z cells through
- * xc x planes (0 = 16, or 8 for X <= 128) of the field, one TMA plane box at a time
- * (csrc/field_march.cu).  Same arithmetic, bit-identical.  Needs
+ * xc x planes (0 = 16, or 8 when 16 would leave <= 8192 work items) of the
+ * field, one TMA plane box at a time (csrc/field_march.cu).  Same arithmetic, bit-identical.  Needs
  * Gy % R == 0 and Gz % 32 == 0.  flags: TF_STEP_HALO_YZ (also write the
  * next field's periodic y/z halos), TF_STEP_HALO_X (also its periodic x
  * halo: one GPU; peer_lo/peer_hi must then be NULL), TF_MARCH_ROWS4.
@@ -490,9 +490,15 @@ int tf_field_step_peer_f64(const double* padded_in, int32_t X, int32_t Gy,
  * kernel on the stream (a peer barrier launched with TF_BARRIER_PDL): the
  * items that read or store x-halo planes wait for it (griddepcontrol.wait),
  * every other item runs at once — the multi-GPU iteration overlaps the
- * ring synchronisation with its interior.                                  */
+ * ring synchronisation with its interior.
+ * TF_MARCH_ALONG_Y: the warps march along y with R x rows per column (the
+ * roles of x and y swapped; needs X % R == 0, TF_STEP_HALO_YZ and both x
+ * halo destinations): a thin x slab (a rank's share at N >= 4) keeps long
+ * columns instead of many short chunks.  Bit-identical (the update's
+ * (dFx + dFy) sum is commutative).                                         */
 #define TF_MARCH_ROWS4 16
 #define TF_MARCH_PDL_EDGE 32
+#define TF_MARCH_ALONG_Y 64
 int tf_field_march_f64(const double* padded_in, int32_t X, int32_t Gy,
                        int32_t Gz, double ax, double ay, double az,
                        double dt_dx, double* padded_out, double* peer_lo,

@@ -33,6 +33,7 @@ TF_STEP_HALO_YZ = 4
 TF_STEP_HALO_X = 8
 TF_MARCH_ROWS4 = 16
 TF_MARCH_PDL_EDGE = 32
+TF_MARCH_ALONG_Y = 64
 TF_BARRIER_PDL = 1
 TF_QUEUE_CHAIN = 2
 TF_QUEUE_SORTED = 4

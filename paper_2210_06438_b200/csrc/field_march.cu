@@ -109,13 +109,19 @@ __device__ __forceinline__ void tma_plane(void* dst, const CUtensorMap* map,
       : "memory");
 }
 
+// The kernel marches along its "plane" axis and stacks R "rows" per column:
+// physical x and y by default, y and x with TF_MARCH_ALONG_Y (a thin x slab
+// marched along its long y extent).  Names below are the default's.
 struct MarchArgs {
   double* out;      // next padded field
-  double* peer_lo;  // left neighbour's next field (its high x halo), or null
-  double* peer_hi;  // right neighbour's next field (its low x halo), or null
-  int64_t pyz;      // padded layer stride
-  int pz;           // padded row stride
-  int X, Gy, Gz;    // owned extents
+  // halo copies of the owned layers next to each face, or null: the plane
+  // axis's low / high faces go to plo[+pw] / phi[-pw] (x: the ring
+  // neighbours' next fields, or this one), the row axis's to qlo / qhi [+-qw]
+  double *plo, *phi, *qlo, *qhi;
+  int64_t pw, qw;
+  int64_t pyz;      // padded stride of the plane axis
+  int pz;           // padded stride of the row axis
+  int X, Gy, Gz;    // owned extents: plane axis, row axis, z
   int xc;           // planes per work item
   int nzb;          // z blocks (Gz / 32)
   int ncols;        // warp columns per plane (Gy / R * nzb)
@@ -123,8 +129,9 @@ struct MarchArgs {
   // item order: the n_int interior items (no halo copies: chunks [cl, ch)
   // x the nyi x nzi columns off the y/z faces) first, then the rest
   int n_int, cl, ch, nyb, nyi, nzi, yoff, zoff;
-  int halo_yz;      // also write the next field's periodic y/z halos
-  int pdl_edge;     // x-edge items wait for the previous kernel (PDL)
+  int halo_yz;      // also write the next field's periodic z halos
+  int pdl_edge;     // PDL: 1 = items on the plane axis's faces wait for the
+                    // previous kernel, 2 = items on the row axis's faces
   unsigned* work;   // {claim, done} counters (zero at launch), or null
   double ax, ay, az, dt_dx;
 };
@@ -248,17 +255,16 @@ __device__ __forceinline__ void finalise(const MarchArgs& A,
     *orow = v;
     if (EDGE) {
       // periodic y/z copies of the next field, and the slab's two lowest /
-      // highest layers as the ring neighbours' next x halo (one GPU: this
+      // highest x layers as the ring neighbours' next x halo (one GPU: this
       // field's own); halo edges / corners are never read
       const int y = y0 + r;
-      const int64_t gyz = (int64_t)A.Gy * pz, xw = (int64_t)A.X * A.pyz;
-      if (hy && y < HY) orow[gyz] = v;
-      if (hy && y >= A.Gy - HY) orow[-gyz] = v;
+      const int64_t off = orow - A.out;
+      if (hy && A.qlo && y < HY) A.qlo[off + A.qw] = v;
+      if (hy && A.qhi && y >= A.Gy - HY) A.qhi[off - A.qw] = v;
       if (hz && z < HZ) orow[A.Gz] = v;
       if (hz && z >= A.Gz - HZ) orow[-A.Gz] = v;
-      const int64_t off = orow - A.out;
-      if (hlo) A.peer_lo[off + xw] = v;
-      if (hhi) A.peer_hi[off - xw] = v;
+      if (hlo) A.plo[off + A.pw] = v;
+      if (hhi) A.phi[off - A.pw] = v;
     }
   }
 }
@@ -302,8 +308,9 @@ __device__ __forceinline__ void march_warp(const CUtensorMap* map,
     if (p_item < 0) return;
     int xa, len, y0, z0;
     item_geo<R>(A, p_item, xa, len, y0, z0);
-    if (PDL && (xa < A.cl * A.xc || xa + len > A.ch * A.xc)) {
-      // an x-edge item reads the halo planes the ring neighbours store and
+    if (PDL && (A.pdl_edge == 1 ? (xa < A.cl * A.xc || xa + len > A.ch * A.xc)
+                                : (y0 < HY || y0 + R > A.Gy - HY))) {
+      // an x-edge item reads the halo layers the ring neighbours store and
       // stores theirs: only it waits for the ring barrier before it loads
       // (a separate instantiation: the branch costs the plain kernel ~2.5%
       // in register pressure)
@@ -341,7 +348,7 @@ __device__ __forceinline__ void march_warp(const CUtensorMap* map,
     int xa, len, y0, z0;
     const bool interior = item_geo<R>(A, it, xa, len, y0, z0);
     // warp-uniform: does this column touch a periodic y / z face?
-    const bool hy = A.halo_yz && (y0 < HY || y0 + R > A.Gy - HY);
+    const bool hy = (A.qlo && y0 < HY) || (A.qhi && y0 + R > A.Gy - HY);
     const bool hz = A.halo_yz && (z0 == 0 || z0 + MZ == A.Gz);
     // One x plane of the march: the state carried from plane to plane
     // (s0 = u(p-1) or, a >= 0, the backward difference u(p) - u(p-1);
@@ -375,8 +382,8 @@ __device__ __forceinline__ void march_warp(const CUtensorMap* map,
               wbuf + ((gc - D) % NB) * PLANE);
           const auto& c = PX ? s1 : s0;
           if (EDGE) {
-            const bool hlo = A.peer_lo != nullptr && p < HX;
-            const bool hhi = A.peer_hi != nullptr && p >= A.X - HX;
+            const bool hlo = A.plo != nullptr && p < HX;
+            const bool hhi = A.phi != nullptr && p >= A.X - HX;
             finalise<R, PY, PZ, true>(A, cb, strip, c, dm, sm, p, y0, z0, hy,
                                       hz, hlo, hhi);
           } else {
@@ -469,23 +476,27 @@ __global__ void __launch_bounds__(MGeo<R, NB>::W * 32, 16)
 
 struct MapKey {
   const void* p;
-  int X, Gy, Gz, R;
+  int X, Gy, Gz, R, ym;
   bool operator==(const MapKey& o) const {
-    return p == o.p && X == o.X && Gy == o.Gy && Gz == o.Gz && R == o.R;
+    return p == o.p && X == o.X && Gy == o.Gy && Gz == o.Gz && R == o.R &&
+           ym == o.ym;
   }
 };
 struct MapKeyHash {
   size_t operator()(const MapKey& k) const {
     return std::hash<const void*>()(k.p) ^ ((size_t)k.X * 1315423911u) ^
-           ((size_t)k.Gy << 20) ^ ((size_t)k.Gz << 40) ^ (size_t)k.R;
+           ((size_t)k.Gy << 20) ^ ((size_t)k.Gz << 40) ^ (size_t)k.R ^
+           ((size_t)k.ym << 8);
   }
 };
 
-// plane box of a padded field: (36 z, R+4 y, 1 x), no swizzle
-int plane_map(const double* P, int X, int Gy, int Gz, int R, CUtensorMap* out) {
+// plane box of a padded field: (36 z, R+4 y, 1 x), no swizzle; ym: the
+// tensor's two outer dimensions swapped, (36 z, R+4 x, 1 y)
+int plane_map(const double* P, int X, int Gy, int Gz, int R, int ym,
+              CUtensorMap* out) {
   static std::mutex mu;
   static std::unordered_map<MapKey, CUtensorMap, MapKeyHash> cache;
-  const MapKey key{P, X, Gy, Gz, R};
+  const MapKey key{P, X, Gy, Gz, R, ym};
   std::lock_guard<std::mutex> lock(mu);
   auto it = cache.find(key);
   if (it != cache.end()) {
@@ -495,8 +506,8 @@ int plane_map(const double* P, int X, int Gy, int Gz, int R, CUtensorMap* out) {
   auto fn = encode_fn();
   if (!fn) return TF_E_NO_TMA;
   const cuuint64_t pz = Gz + 2 * HZ, py = Gy + 2 * HY, px = X + 2 * HX;
-  cuuint64_t dims[3] = {pz, py, px};
-  cuuint64_t strides[2] = {pz * 8, pz * py * 8};
+  cuuint64_t dims[3] = {pz, ym ? px : py, ym ? py : px};
+  cuuint64_t strides[2] = {(ym ? pz * py : pz) * 8, (ym ? pz : pz * py) * 8};
   cuuint32_t box[3] = {(cuuint32_t)BZW, (cuuint32_t)(R + 4), 1};
   cuuint32_t es[3] = {1, 1, 1};
   CUtensorMap m;
@@ -592,59 +603,76 @@ int tf_field_march_f64(const double* padded_in, int32_t X, int32_t Gy,
                        double* peer_hi, int32_t flags, int32_t xc,
                        uint32_t* work, tf_stream_t stream) {
   const int R = (flags & TF_MARCH_ROWS4) ? 4 : 8;
-  if (!padded_in || !padded_out || padded_in == padded_out || X < 1 ||
-      Gy < R || Gz < MZ || Gy % R || Gz % MZ || xc < 0 ||
+  const bool ym = (flags & TF_MARCH_ALONG_Y) != 0;
+  const bool hyz = (flags & TF_STEP_HALO_YZ) != 0;
+  // the kernel's plane / row extents
+  const int P = ym ? Gy : X, Q = ym ? X : Gy;
+  if (!padded_in || !padded_out || padded_in == padded_out || P < 1 ||
+      Q < R || Gz < MZ || Q % R || Gz % MZ || xc < 0 ||
       (flags & ~(TF_STEP_HALO_YZ | TF_STEP_HALO_X | TF_MARCH_ROWS4 |
-                 TF_MARCH_PDL_EDGE)))
+                 TF_MARCH_PDL_EDGE | TF_MARCH_ALONG_Y)))
     return TF_E_INVALID;
   if (flags & TF_STEP_HALO_X) {
     if (peer_lo || peer_hi) return TF_E_INVALID;
     peer_lo = peer_hi = padded_out;
   }
   if ((peer_lo || peer_hi) && X < HX) return TF_E_INVALID;
+  // along y: both x faces and the y/z halos (the item order's frame is the
+  // row axis's and z's faces together)
+  if (ym && !(hyz && peer_lo && peer_hi)) return TF_E_INVALID;
   CUtensorMap map;
-  int rc = plane_map(padded_in, X, Gy, Gz, R, &map);
+  int rc = plane_map(padded_in, X, Gy, Gz, R, ym ? 1 : 0, &map);
   if (rc) return rc;
+  const int64_t pz = Gz + 2 * HZ, pyz = (int64_t)(Gy + 2 * HY) * pz;
   MarchArgs A;
   A.out = padded_out;
-  A.peer_lo = peer_lo;
-  A.peer_hi = peer_hi;
-  A.pz = Gz + 2 * HZ;
-  A.pyz = (int64_t)(Gy + 2 * HY) * A.pz;
-  A.X = X;
-  A.Gy = Gy;
+  double* own = hyz ? padded_out : nullptr;
+  const int64_t xw = (int64_t)X * pyz, yw = (int64_t)Gy * pz;
+  A.plo = ym ? own : peer_lo;
+  A.phi = ym ? own : peer_hi;
+  A.pw = ym ? yw : xw;
+  A.qlo = ym ? peer_lo : own;
+  A.qhi = ym ? peer_hi : own;
+  A.qw = ym ? xw : yw;
+  A.pz = (int)(ym ? pyz : pz);
+  A.pyz = ym ? pz : pyz;
+  A.X = P;
+  A.Gy = Q;
   A.Gz = Gz;
-  // default chunk: 16 planes; 8 for a thin slab (a rank's share of config
-  // 5 at N >= 4: 64 planes in 16-plane chunks are too few items for the
-  // grid and half of them hold x-halo planes — 100 -> 87 us at 64 planes,
-  // 155 -> 142 us at 128; the same at 256 and up)
-  A.xc = xc > 0 ? xc : (X <= 128 ? 8 : 16);
   A.nzb = Gz / MZ;
-  A.nyb = Gy / R;
+  A.nyb = Q / R;
   A.ncols = A.nyb * A.nzb;
-  const int nch = (X + A.xc - 1) / A.xc;
+  // default chunk: 16 planes, or 8 when 16-plane chunks would give at most
+  // 8192 items (under ~4 per warp of the grid: a rank's share of config 5
+  // at N >= 4, 128 planes 166 -> 152 us along x, 151 -> 143 along y; at 256
+  // planes 16 stays ahead, 236 vs 240 us)
+  A.xc = xc > 0 ? xc
+                : ((int64_t)((P + 15) / 16) * A.ncols > 8192 ? 16 : 8);
+  const int nch = (P + A.xc - 1) / A.xc;
   const int64_t items = (int64_t)nch * A.ncols;
   if (items > (1 << 30)) return TF_E_INVALID;
   A.nitems = (int)items;
-  A.halo_yz = (flags & TF_STEP_HALO_YZ) ? 1 : 0;
-  A.pdl_edge = (flags & TF_MARCH_PDL_EDGE) ? 1 : 0;
-  // interior items: no periodic y/z face (halo_yz) and no x-halo plane
+  A.halo_yz = hyz ? 1 : 0;
+  A.pdl_edge = (flags & TF_MARCH_PDL_EDGE) ? (ym ? 2 : 1) : 0;
+  // interior items: no halo copy on the row axis / z (the frame) and no
+  // halo layer of the plane axis
   A.yoff = A.zoff = A.halo_yz;
   A.nyi = A.halo_yz ? (A.nyb > 2 ? A.nyb - 2 : 0) : A.nyb;
   A.nzi = A.halo_yz ? (A.nzb > 2 ? A.nzb - 2 : 0) : A.nzb;
-  // chunk c is clear of the low x halo iff c * xc >= HX, of the high one
-  // iff (c + 1) * xc <= X - HX
-  A.cl = peer_lo ? (HX + A.xc - 1) / A.xc : 0;
-  A.ch = peer_hi ? (X - HX) / A.xc : nch;
+  // chunk c is clear of the low plane-axis halo iff c * xc >= HX, of the
+  // high one iff (c + 1) * xc <= P - HX
+  A.cl = A.plo ? (HX + A.xc - 1) / A.xc : 0;
+  A.ch = A.phi ? (P - HX) / A.xc : nch;
   if (A.ch < A.cl) A.ch = A.cl;
   if (A.cl > nch) A.cl = A.ch = nch;
   A.n_int = (A.ch - A.cl) * A.nyi * A.nzi;
   A.work = work;
-  A.ax = ax;
-  A.ay = ay;
+  A.ax = ym ? ay : ax;  // the plane axis's velocity
+  A.ay = ym ? ax : ay;
   A.az = az;
   A.dt_dx = dt_dx;
-  const int sg = (ax >= 0.0 ? 1 : 0) | (ay >= 0.0 ? 2 : 0) | (az >= 0.0 ? 4 : 0);
+  const int sg =
+      (A.ax >= 0.0 ? 1 : 0) | (A.ay >= 0.0 ? 2 : 0) | (az >= 0.0 ? 4 : 0);
   cudaStream_t st = (cudaStream_t)stream;
   // ring depth 4 for both column heights (A/B on config 5, R = 8, xc 16,
   // 128 registers: NB 3 / 4 / 5 = 450 / 448 / 477 us; more buffers cost

@@ -352,13 +352,15 @@ class MarchFieldIteration(_FieldBase):
     The config-5 iteration at N = 1 (one team = every sub-grid)."""
 
     def __init__(self, grid_n: int, n: int = 8, velocity=(1.0, 1.0, 1.0),
-                 dt_dx=None, device=None, xc: int = 0, rows4: bool = False):
+                 dt_dx=None, device=None, xc: int = 0, rows4: bool = False,
+                 along_y: bool = False):
         super().__init__(grid_n, grid_n, n, velocity, dt_dx, device)
         if not self.march_ok():
             raise ValidationError("the march kernel needs grid_n % 32 == 0")
         self.xc = xc
         self.flags = _lib.TF_STEP_HALO_YZ | _lib.TF_STEP_HALO_X | \
-            (_lib.TF_MARCH_ROWS4 if rows4 else 0)
+            (_lib.TF_MARCH_ROWS4 if rows4 else 0) | \
+            (_lib.TF_MARCH_ALONG_Y if along_y else 0)
         self.halo_fresh = False
 
     def load(self, field_dev: torch.Tensor, stream=None) -> None:
@@ -419,7 +421,8 @@ class PeerSlabFieldIteration(_FieldBase):
     def __init__(self, part: SlabPartition, slab_field=None,
                  velocity=(1.0, 1.0, 1.0), dt_dx=None, device=None,
                  group=None, timeout_s: float = 10.0, kernel: str = "auto",
-                 xc: int = 0, overlap_barrier: bool | None = None):
+                 xc: int = 0, overlap_barrier: bool | None = None,
+                 march_axis: str = "auto"):
         super().__init__(part.mx * part.n, part.grid_n, part.n, velocity,
                          dt_dx, device)
         self.part = part
@@ -432,6 +435,18 @@ class PeerSlabFieldIteration(_FieldBase):
                 (kernel == "march" and not self.march_ok()):
             raise ValidationError(f"kernel {kernel!r} not usable here")
         self.kernel, self.xc = kernel, xc
+        # march axis: x (planes of the slab), or y for a thin slab (a rank's
+        # share at N >= 4: columns of x rows marching the long y extent;
+        # config 5 at 128 planes 143 vs 152 us, at 64 planes even, at 256
+        # x ahead, 236 vs 260 us — DESIGN §9); "auto" picks y for a slab of
+        # at most 128 planes and a quarter of the y extent
+        if march_axis == "auto":
+            march_axis = "y" if self.X <= 128 and self.X % 8 == 0 and \
+                self.G >= 4 * self.X else "x"
+        if march_axis not in ("x", "y") or \
+                (march_axis == "y" and self.X % 8):
+            raise ValidationError(f"march axis {march_axis!r} not usable here")
+        self.march_axis = march_axis
         # march kernel: overlap the ring barrier with the next iteration's
         # interior (programmatic dependent launches; x-edge items wait).
         # Default: with real neighbours only — on one rank the barrier is a
@@ -499,7 +514,9 @@ class PeerSlabFieldIteration(_FieldBase):
             # the barrier a programmatic dependent of this march
             ov = self.overlap_barrier
             self.march(_lib.TF_STEP_HALO_YZ |
-                       (_lib.TF_MARCH_PDL_EDGE if ov else 0),
+                       (_lib.TF_MARCH_PDL_EDGE if ov else 0) |
+                       (_lib.TF_MARCH_ALONG_Y if self.march_axis == "y"
+                        else 0),
                        self.left["P"][nxt].data_ptr(),
                        self.right["P"][nxt].data_ptr(), self.xc)
             self._barrier(pdl=self.overlap_barrier)

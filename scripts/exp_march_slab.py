@@ -1,7 +1,9 @@
 """The march kernel on one rank's share of config 5 at N = 2 / 4 / 8 (an
 x-slab of 256 / 128 / 64 planes x 512 x 512, periodic x halo standing in
 for the neighbours): time per iteration against the chunk length (the
-x-edge chunks run the halo-writing loop; shorter chunks make them fewer)."""
+x-edge chunks run the halo-writing loop; shorter chunks make them fewer),
+4-row columns, the march along y (TF_MARCH_ALONG_Y: long y columns of x
+rows) and the per-sub-grid kernel."""
 import statistics
 import sys
 sys.path.insert(0, ".")
@@ -28,17 +30,20 @@ def once(fn, iters=20):
     return a.elapsed_time(b) / iters
 
 
-for X in (128, 64, 32):
+for X in (256, 128, 64, 32):
     f = _FieldBase(X, G, 8, (1.0, 1.0, 1.0), None, dev)
     f.load(full[:X].contiguous())
     f.halo(True)
     res = {}
-    for xc in (16, 8, 32, "r4x16", "r4x8", "r4x32"):
+    for xc in (0, 16, 8, "r4x8", "y0", "y16", "y8", "y32"):
         fl = _lib.TF_STEP_HALO_YZ | _lib.TF_STEP_HALO_X
         x = xc
-        if isinstance(xc, str):
+        if isinstance(xc, str) and xc.startswith("r4x"):
             fl |= _lib.TF_MARCH_ROWS4
             x = int(xc[3:])
+        elif isinstance(xc, str):
+            fl |= _lib.TF_MARCH_ALONG_Y
+            x = int(xc[1:])
 
         def step(x=x, fl=fl):
             f.march(fl, xc=x)
