@@ -620,18 +620,19 @@ class ReconFluxHostPipeline:
     """`AggregatedIteration.recon_flux_host` with the upload overlapped,
     captured once as a CUDA graph for FIXED pinned buffers.
 
-    The host field moves in x-chunks of sub-grid layers on a copy stream;
-    chunk i's layers are scattered into the pool as soon as they land, and
-    chunk j's sub-grids are ghost-filled (exchange_ghosts reads the
-    neighbours' OWNED cells, so chunks j-1 and j+1 must be scattered) and
-    run through their own captured team plans (teams formed over the
-    chunk's arrivals with the iteration's cap) right after chunk j+1 lands.
-    Chunk 0 (whose periodic x neighbour is the last chunk) goes last; the
-    per-sub-grid max signal speed returns to `amax_out`.  Pure function of
+    The host field moves in x-chunks of sub-grid layers on a copy stream,
+    the LAST layer first (it is layer 0's periodic neighbour), then layers
+    0, 1, ...; each chunk is scattered into the pool as soon as it lands,
+    and every layer whose two neighbours have landed too is ghost-filled
+    (exchange_ghosts reads the neighbours' OWNED cells) and run through its
+    own captured team plans (teams formed over those arrivals with the
+    iteration's cap) at once — so after the last chunk lands only two
+    layers remain.  Their per-sub-grid max signal speeds return to
+    `amax_out` group by group on a second copy stream.  Pure function of
     `field_in`: every replay rewrites the whole current pool."""
 
     def __init__(self, it: "AggregatedIteration", field_in, amax_out,
-                 layers=(1, 3, 4, 4, 3, 1), executors: int = 2,
+                 layers=(1, 4, 4, 4, 2, 1), executors: int = 2,
                  copy_streams: int = 2):
         from . import ops
         if not (field_in.is_pinned() and amax_out.is_pinned()):
@@ -642,40 +643,66 @@ class ReconFluxHostPipeline:
             base = max(1, m // len(layers))
             layers = [base] * (m // base)
             layers[-1] += m - sum(layers)
-        start = [0]
+        order = [m - 1] + list(range(m - 1)) if m > 1 else [0]
+        chunks, pos = [], 0
         for k in layers:
-            start.append(start[-1] + k)
-        nch = len(layers)
+            chunks.append(order[pos:pos + k])
+            pos += k
+        # compute groups: after chunk c lands, the layers whose neighbours
+        # (periodic) have all landed and that have not run yet
+        landed, done, groups = set(), set(), []
+        for ch in chunks:
+            landed.update(ch)
+            ready = [l for l in range(m) if l not in done and
+                     all((l + d) % m in landed for d in (-1, 0, 1))]
+            done.update(ready)
+            groups.append(ready)
+        nch = len(chunks)
         self.it, self.bufs = it, (field_in, amax_out)
         dev = it.pool.device
         mm = m * m
-        self.ids = [torch.arange(start[c] * mm, start[c + 1] * mm,
-                                 dtype=torch.int32, device=dev)
-                    for c in range(nch)]
+
+        def runs(ls):
+            """maximal runs of consecutive layers: (first, count)"""
+            out = []
+            for l in sorted(ls):
+                if out and out[-1][0] + out[-1][1] == l:
+                    out[-1][1] += 1
+                else:
+                    out.append([l, 1])
+            return out
+        self.group_runs = [runs(g) for g in groups]
+        self.chunk_runs = [runs(c) for c in chunks]
+        self.ids = [torch.cat([torch.arange(a * mm, (a + k) * mm,
+                                            dtype=torch.int32, device=dev)
+                               for a, k in r]) if r else None
+                    for r in self.group_runs]
         cap = max(len(t.ids) for t in it.teams)
-        # each chunk's arrivals formed into teams with the iteration's cap;
+        # each group's arrivals formed into teams with the iteration's cap;
         # a team is one launch with its ids in the kernel parameters
         self.teams = [[np.asarray(t.ids, dtype=np.int32)
-                       for t in form_teams(range(start[c] * mm,
-                                                 start[c + 1] * mm), cap)]
-                      for c in range(nch)]
+                       for t in form_teams(
+                           [i for a, k in r
+                            for i in range(a * mm, (a + k) * mm)], cap)]
+                      for r in self.group_runs]
         lib = _lib.load()
         ax, ay, az = it.velocity
         self.launches = 0
-        # each chunk's upload is split over two copy streams (two copy
+        # each chunk's upload may be split over two copy streams (two copy
         # engines: one alone ran at 17-49 GB/s from box to box), chunks in
         # order on both — rotating whole chunks over the streams instead let
         # every chunk land at about the same time, which undid the overlap
         ups = [torch.cuda.Stream(device=dev)
                for _ in range(max(1, min(2, copy_streams)))]
+        down = torch.cuda.Stream(device=dev)
         comp_side = torch.cuda.Stream(device=dev)
         fin = field_in.view(it.grid_n, it.grid_n, it.grid_n)
         dev_f, pool = it.field_dev, it.pool
 
-        def chunk_compute(c):
-            ops.ghost_fill(pool, n, m, ids=self.ids[c])
+        def group_compute(g):
+            ops.ghost_fill(pool, n, m, ids=self.ids[g])
             st = torch.cuda.current_stream().cuda_stream
-            for k, ids in enumerate(self.teams[c]):
+            for k, ids in enumerate(self.teams[g]):
                 # teams after the first overlap their predecessor (PDL):
                 # same region, independent slices
                 _lib.check(lib.tf_recon_flux_team_ex_f64(
@@ -685,38 +712,45 @@ class ReconFluxHostPipeline:
                     it.F.data_ptr(), 1, it.amax.data_ptr(), 0,
                     _lib.TF_LAUNCH_OVERLAP_PREV if k else 0, st),
                     "tf_recon_flux_team_ex_f64")
-            self.launches += 1 + len(self.teams[c])
+            self.launches += 1 + len(self.teams[g])
+            # this group's max signal speeds go home while the rest runs
+            ev = torch.cuda.Event()
+            ev.record()
+            down.wait_event(ev)
+            with torch.cuda.stream(down):
+                for a, k in self.group_runs[g]:
+                    amax_out[a * mm:(a + k) * mm].copy_(
+                        it.amax[a * mm:(a + k) * mm], non_blocking=True)
 
         def run():
             self.launches = 0
             comp = torch.cuda.current_stream()
             evs = []
-            for up in ups:
+            for up in ups + [down]:
                 up.wait_stream(comp)
             for c in range(nch):
-                lo, hi = start[c] * n, start[c + 1] * n
-                mid = (lo + hi) // 2 if len(ups) == 2 else hi
                 pair = []
-                for up, (a, b) in zip(ups, ((lo, mid), (mid, hi))):
-                    if a >= b:
-                        continue
-                    with torch.cuda.stream(up):
-                        dev_f[a:b].copy_(fin[a:b], non_blocking=True)
-                        ev = torch.cuda.Event()
-                        ev.record(up)
-                        pair.append(ev)
+                for a, k in self.chunk_runs[c]:
+                    lo, hi = a * n, (a + k) * n
+                    mid = (lo + hi) // 2 if len(ups) == 2 else hi
+                    for up, (x0, x1) in zip(ups, ((lo, mid), (mid, hi))):
+                        if x0 >= x1:
+                            continue
+                        with torch.cuda.stream(up):
+                            dev_f[x0:x1].copy_(fin[x0:x1], non_blocking=True)
+                            ev = torch.cuda.Event()
+                            ev.record(up)
+                            pair.append(ev)
                 evs.append(pair)
             for c in range(nch):
                 for ev in evs[c]:
                     comp.wait_event(ev)
-                ops.field_to_pool_layers(dev_f, n, pool, start[c], layers[c])
-                self.launches += 1
-                if 2 <= c:
-                    chunk_compute(c - 1)
-            if nch > 1:
-                chunk_compute(nch - 1)
-            chunk_compute(0)
-            amax_out[:it.S].copy_(it.amax, non_blocking=True)
+                for a, k in self.chunk_runs[c]:
+                    ops.field_to_pool_layers(dev_f, n, pool, a, k)
+                    self.launches += 1
+                if self.group_runs[c]:
+                    group_compute(c)
+            comp.wait_stream(down)
 
         run()                       # warm-up (also sizes the TMA maps)
         torch.cuda.synchronize()

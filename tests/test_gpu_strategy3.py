@@ -159,11 +159,13 @@ def test_aggregated_iteration_host_roundtrip(cuda, grid, n, vel):
     assert np.array_equal(host_out.numpy(), HO.reference_step(f, vel))
 
 
-@pytest.mark.parametrize("grid,n,vel,layers", [
-    (128, 8, (1.0, 1.0, 1.0), (1, 3, 4, 4, 3, 1)),
-    (64, 8, (-1.0, 0.5, -0.25), (1, 3, 4, 4, 3, 1)),
-    (64, 16, (0.7, -1.3, 0.0), (2, 2))])
-def test_recon_flux_host_pipelined(cuda, grid, n, vel, layers):
+@pytest.mark.parametrize("grid,n,vel,layers,cs", [
+    (128, 8, (1.0, 1.0, 1.0), (1, 3, 4, 4, 3, 1), 1),
+    (128, 8, (-0.6, 1.1, -0.9), (1, 3, 4, 4, 2, 1, 1), 2),
+    (128, 8, (0.3, -0.2, 0.9), (16,), 1),
+    (64, 8, (-1.0, 0.5, -0.25), (1, 3, 4, 4, 3, 1), 2),
+    (64, 16, (0.7, -1.3, 0.0), (2, 2), 1)])
+def test_recon_flux_host_pipelined(cuda, grid, n, vel, layers, cs):
     """The e2e call (host field in, aggregated recon+flux, per-sub-grid max
     signal speed out), plain and pipelined (chunked upload overlapped with
     scatter / ghost fill / team launches, one CUDA graph): the faces in HBM
@@ -181,7 +183,8 @@ def test_recon_flux_host_pipelined(cuda, grid, n, vel, layers):
     it.recon_flux_host(host_in, amax)
     torch.cuda.synchronize()
     assert np.array_equal(it.F.cpu().numpy(), oF)
-    pipe = ReconFluxHostPipeline(it, host_in, amax, layers=layers)
+    pipe = ReconFluxHostPipeline(it, host_in, amax, layers=layers,
+                                 copy_streams=cs)
     for _ in range(2):
         for t in (it.um, it.up, it.F, it.amax):
             t.fill_(float("nan"))
