@@ -163,6 +163,8 @@ def test_aggregated_iteration_host_roundtrip(cuda, grid, n, vel):
     (128, 8, (1.0, 1.0, 1.0), (1, 3, 4, 4, 3, 1), 1),
     (128, 8, (-0.6, 1.1, -0.9), (1, 3, 4, 4, 2, 1, 1), 2),
     (128, 8, (0.3, -0.2, 0.9), (16,), 1),
+    (128, 8, (0.5, 0.5, -1.0), (1,) * 16, 1),
+    (64, 16, (-0.3, 0.8, 0.1), (1, 1, 1, 1), 2),
     (64, 8, (-1.0, 0.5, -0.25), (1, 3, 4, 4, 3, 1), 2),
     (64, 16, (0.7, -1.3, 0.0), (2, 2), 1)])
 def test_recon_flux_host_pipelined(cuda, grid, n, vel, layers, cs):
@@ -186,7 +188,10 @@ def test_recon_flux_host_pipelined(cuda, grid, n, vel, layers, cs):
     pipe = ReconFluxHostPipeline(it, host_in, amax, layers=layers,
                                  copy_streams=cs)
     for _ in range(2):
-        for t in (it.um, it.up, it.F, it.amax):
+        # stale device state must not leak in: the staged field (the last
+        # layer's middle planes are scattered before they land, and must
+        # not be read by its neighbours' ghost fill) and the pool
+        for t in (it.um, it.up, it.F, it.amax, it.field_dev, it.pool):
             t.fill_(float("nan"))
         amax.fill_(float("nan"))
         pipe.run()
