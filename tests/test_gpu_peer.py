@@ -37,7 +37,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _rank(rank, world, port, grid, n, vel, q):
+def _rank(rank, world, port, grid, n, vel, q, axis="auto"):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     import torch
     import torch.distributed as dist
@@ -49,7 +49,8 @@ def _rank(rank, world, port, grid, n, vel, q):
         part = SlabPartition(grid, n, world, rank)
         f = HO.stress_field(grid)
         r = PeerSlabFieldIteration(part, part.slab(f), vel,
-                                   device=torch.device("cuda", 0))
+                                   device=torch.device("cuda", 0),
+                                   march_axis=axis)
         for _ in range(3):
             r.iteration()
         torch.cuda.synchronize()
@@ -61,13 +62,18 @@ def _rank(rank, world, port, grid, n, vel, q):
 
 
 @pytest.mark.parametrize("world", [2, 4])
-def test_peer_two_processes_one_gpu(cuda, world):
+@pytest.mark.parametrize("axis", ["x", "y"])
+def test_peer_two_processes_one_gpu(cuda, world, axis):
+    """Both march axes (y: the ranks' thin slabs marched along y, the
+    items on the x faces storing into the neighbours and waiting for the
+    overlapped barrier)."""
     import torch.multiprocessing as mp
     grid, n, vel = 64, 8, (0.7, -1.3, 0.0)
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_rank, args=(r, world, port, grid, n, vel, q))
+    procs = [ctx.Process(target=_rank,
+                         args=(r, world, port, grid, n, vel, q, axis))
              for r in range(world)]
     for p in procs:
         p.start()
