@@ -1129,6 +1129,7 @@ def cfg5_leg(args, world, rank, local, peak):
     ms_peer = None
     clk = None
     ms_cols = None
+    march_axis = None
     if use_peer:
         # the per-sub-grid kernel (one CTA per 8^3 sub-grid + halo kernels)
         # on the same peer path, for the record
@@ -1146,6 +1147,7 @@ def cfg5_leg(args, world, rank, local, peak):
         torch.cuda.empty_cache()
         # headline: the whole-slab march kernel (csrc/field_march.cu)
         peer = PeerSlabFieldIteration(part, slab, VELOCITY, device=dev)
+        march_axis = peer.march_axis
         got = first_iteration(peer, peer.iteration)
         peer.check()
         checks["peer_fused_vs_nccl_ring"] = all_true(world,
@@ -1208,8 +1210,9 @@ def cfg5_leg(args, world, rank, local, peak):
         "dtype": "f64", "data": "synthetic",
         "config": cfg5_config(world, grid),
         "run": {"path": ("peer-fused: ONE march kernel per iteration "
-                         "(warp columns marching x through TMA plane boxes, "
-                         "csrc/field_march.cu) stores the slab's boundary "
+                         f"(warp columns marching {march_axis} through TMA "
+                         "plane boxes, csrc/field_march.cu; a slab of <= 128 "
+                         "planes is marched along y) stores the slab's boundary "
                          "layers into the ring neighbours' next fields over "
                          "CUDA-IPC peer memory and the next field's y/z "
                          "halos, then a device peer barrier"
