@@ -739,8 +739,9 @@ def e2e_leg(args, steps, warmup, world, stream):
                    "pool, ghost fill, aggregated reconstruct+flux teams "
                    "(um/up/F to HBM), per-sub-grid max signal speed -> "
                    "pinned host; pipelined: x-chunked upload on the copy "
-                   "engine, chunk j launched once j-1 and j+1 landed, one "
-                   "CUDA graph",
+                   "engine (the last layer first), each layer launched "
+                   "once it and its two neighbours landed, max speeds "
+                   "home per group, one CUDA graph",
            "pipelined": {"ms_per_step": ms_pipe,
                          "value": rate(it.S * world, N_SUB, ms_pipe),
                          "copy_streams": cs_best,
