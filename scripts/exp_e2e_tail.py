@@ -41,9 +41,10 @@ def upload_amax():
 cfgs = {"upload, one copy": upload_one,
         "upload, 6 chunks": upload_chunks(),
         "upload + amax back": upload_amax}
-for lay in ((1, 3, 4, 4, 3, 1), (1, 3, 4, 4, 2, 1, 1), (1, 2, 3, 3, 3, 2, 1, 1),
-            (2, 4, 4, 3, 2, 1), (1, 4, 4, 4, 2, 1), (4, 4, 4, 4)):
-    for cs in (1, 2):
+TAPERS = ((1, 3, 4, 4, 3, 1), (1, 4, 4, 4, 2, 1), (1, 5, 5, 4, 1),
+          (1, 6, 6, 2, 1), (1, 7, 7, 1), (2, 6, 6, 1, 1), (1, 5, 5, 3, 1, 1))
+for lay in TAPERS:
+    for cs in ((1, 2) if lay == TAPERS[0] else (1,)):
         p = S3.ReconFluxHostPipeline(it, host_in, amax, layers=lay,
                                      copy_streams=cs)
         cfgs[f"pipe {'-'.join(map(str, lay))} cs{cs}"] = p.run
