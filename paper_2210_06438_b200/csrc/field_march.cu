@@ -36,6 +36,12 @@
 // GPU (TF_STEP_HALO_X) or the ring neighbours' halos over peer memory
 // (peer_lo / peer_hi), so the exchange rides on the compute.
 //
+// TF_MARCH_ALONG_Y swaps the roles of x and y (the TMA map's two outer
+// dimensions and the strides exchanged, the x halo copies made by the items
+// on the row faces): a rank's thin x slab is marched along its long y
+// extent.  The update sums (dFx + dFy) + dFz either way — addition is
+// commutative, so the result is bit-identical.
+//
 // Work items are ordered interior first (no halo copies), then the items
 // on the field's faces; an interior item runs a loop unrolled twice whose
 // two register sets alternate (no register moves for the x shift), a face
