@@ -7,9 +7,12 @@ rows) and the per-sub-grid kernel."""
 import statistics
 import sys
 sys.path.insert(0, ".")
+import pathlib
+from paper_2210_06438_b200 import _lib
+if len(sys.argv) > 1:          # another saved build (A/B across processes)
+    _lib.LIB_PATH = pathlib.Path(sys.argv[1]).resolve()
 import torch
 from oracle import hydro_oracle as HO
-from paper_2210_06438_b200 import _lib
 from paper_2210_06438_b200.field import _FieldBase
 
 G = 512
@@ -30,12 +33,16 @@ def once(fn, iters=20):
     return a.elapsed_time(b) / iters
 
 
-for X in (256, 128, 64, 32):
+XS = tuple(int(x) for x in sys.argv[2].split(",")) if len(sys.argv) > 2 \
+    else (256, 128, 64, 32)
+VAR = sys.argv[3].split(",") if len(sys.argv) > 3 else None
+for X in XS:
     f = _FieldBase(X, G, 8, (1.0, 1.0, 1.0), None, dev)
     f.load(full[:X].contiguous())
     f.halo(True)
     res = {}
-    for xc in (0, 16, 8, "r4x8", "y0", "y16", "y8", "y32"):
+    for xc in (VAR or (0, 16, 8, "r4x8", "y0", "y16", "y8", "y32")):
+        xc = int(xc) if isinstance(xc, str) and xc.isdigit() else xc
         fl = _lib.TF_STEP_HALO_YZ | _lib.TF_STEP_HALO_X
         x = xc
         if isinstance(xc, str) and xc.startswith("r4x"):
